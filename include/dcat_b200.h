@@ -1,0 +1,187 @@
+/*
+ * dcat_b200.h — C ABI of the B200-native DCAT scoring path.
+ *
+ * This is the drop-in boundary for the reference's batch scorer
+ *   std::vector<RankingOutputs> seqfm::rank_forward_batch(
+ *       const TransformerParams&, const IdEmbSource&, const RankingHeadParams&,
+ *       const std::vector<RankingExample>&, const FinetuneConfig&)
+ *   (/root/reference/proj/include/seqfm/finetune.hpp:150-154, body finetune.cpp:414-493)
+ * and for the DCAT sub-API it is built from
+ *   dedup_segments   (dcat.hpp:22,   dcat.cpp:91-108)
+ *   context_forward  (dcat.hpp:47-49, dcat.cpp:137-178)
+ *   candidate_inputs (dcat.hpp:53-54, dcat.cpp:180-197)
+ *   cross_forward    (dcat.hpp:59-60, dcat.cpp:199-271).
+ *
+ * Plain C types only: pointers, sizes, status codes. No torch, no C++ types.
+ * Every entry point returns 0 on success or a negative DCAT_E* code; the
+ * message of the last failure on the calling thread is dcat_last_error().
+ * The reference throws std::runtime_error (common.hpp:9-16) where this ABI
+ * returns DCAT_EINVAL; the C++ shim maps one to the other.
+ *
+ * The same structs are consumed by the CPU oracle (oracle/dcat_oracle.h) and
+ * by the reference bridge (oracle/ref_bridge.cpp), so one set of host buffers
+ * feeds all three implementations.
+ */
+#ifndef DCAT_B200_H
+#define DCAT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DCAT_OK 0
+#define DCAT_EINVAL (-1)      /* input violates a reference SEQFM_CHECK      */
+#define DCAT_ECUDA (-2)       /* CUDA runtime / launch failure               */
+#define DCAT_EUNSUPPORTED (-3) /* variant not on the device path (AuxLt, Lite) */
+#define DCAT_ENOMEM (-4)
+#define DCAT_ENONFINITE (-5)  /* non-finite activation (model.cpp:25-28)     */
+
+/* ModelConfig (model.hpp:84-102). pos_learned: 1 = PosMode::Learned, 0 = None. */
+typedef struct dcat_model_config {
+    int32_t d_model;
+    int32_t n_layers;
+    int32_t n_heads;
+    int32_t mlp_ratio;
+    int32_t max_len;
+    int32_t d_emb;
+    int32_t n_actions;
+    int32_t n_surfaces;
+    int32_t pos_learned;
+} dcat_model_config;
+
+/* TransformerParams tensors, fp32 row-major, in the exact order of
+ * TransformerParams::all_params() (model.cpp:268-286):
+ *   log_tau, action_emb, surface_emb, [pos_emb if learned],
+ *   phi_in.{w1,b1,w2,b2}, phi_out.{w1,b1,w2,b2}, psi.{w1,b1,w2,b2},
+ *   per layer: ln1_g, ln1_b, wq, bq, wk, bk, wv, bv, wo, bo, ln2_g, ln2_b,
+ *              fw1, fb1, fw2, fb2.
+ * Linear weights are stored in x out (linear_forward: y = x*W + b, model.hpp:44). */
+typedef struct dcat_params {
+    const float* const* tensors;
+    int32_t n_tensors;
+} dcat_params;
+
+/* HashedEmbeddingTable (embed.hpp:25-57): J sub-tables of R x d_sub fp32. */
+typedef struct dcat_table {
+    int32_t num_subtables;
+    int32_t rows;
+    int32_t d_sub;
+    const uint64_t* seeds;          /* [J] per-subtable hash seeds          */
+    const float* const* subtables;  /* [J] pointers, each R x d_sub         */
+} dcat_table;
+
+/* RankingHeadParams (finetune.hpp:70-85). d_feat = d_module + d_emb + n_ctx. */
+typedef struct dcat_head {
+    int32_t d_module;
+    int32_t d_emb;
+    int32_t n_ctx;
+    int32_t hidden;
+    int32_t d_aux;
+    const float* w1;       /* d_feat x hidden   */
+    const float* b1;       /* hidden            */
+    const float* w2;       /* hidden x 3        */
+    const float* b2;       /* 3                 */
+    const float* mod_w;    /* d_module x 3      */
+    const float* mod_b;    /* 3                 */
+    const float* aux_proj; /* d_aux x d_emb     */
+    const float* lt;       /* d_emb             */
+} dcat_head;
+
+/* FusionVariant (finetune.hpp:29). */
+enum {
+    DCAT_VARIANT_BASE = 0,
+    DCAT_VARIANT_AUX = 1,
+    DCAT_VARIANT_AUXLT = 2,
+    DCAT_VARIANT_LITE_MEAN = 3,
+    DCAT_VARIANT_LITE_LAST = 4
+};
+
+/* The inference-relevant part of FinetuneConfig (finetune.hpp:87-103). */
+typedef struct dcat_finetune_config {
+    int32_t variant;
+    int32_t use_seq_module;
+    int32_t max_events;
+    int32_t d_aux;
+    double fresh_days;
+    double mid_days;
+} dcat_finetune_config;
+
+/* A request batch: the std::vector<RankingExample> of the reference
+ * (finetune.hpp:36-42) as structure-of-arrays. Row i's valid event prefix
+ * (Segment::valid, seqdata.hpp:62-68) is events [row_offset[i],
+ * row_offset[i] + row_valid[i]) of the event pool. Rows may share storage;
+ * padding past `valid` is not represented (it never affects a score).
+ * Event fields follow seqdata.hpp:39-44. aux is n_rows x d_aux or NULL. */
+typedef struct dcat_batch {
+    int64_t n_rows;
+    const int64_t* row_offset;
+    const int32_t* row_valid;
+    int64_t n_events;
+    const uint64_t* ev_ts;
+    const uint8_t* ev_action;
+    const uint8_t* ev_surface;
+    const uint64_t* ev_item;
+    const uint64_t* candidate;
+    const double* age_seconds;
+    const float* aux;
+    int32_t d_aux;
+} dcat_batch;
+
+/* Flags for dcat_rank_forward_batch / dcat_dedup. */
+#define DCAT_INPUT_DEVICE 0x1   /* batch and output pointers are device pointers    */
+#define DCAT_PRECISION_FP32 0x2 /* fp32 storage + SIMT math (parity/debug mode)     */
+#define DCAT_PROFILE 0x4        /* record per-stage CUDA events (dcat_stage_times)  */
+
+typedef struct dcat_model dcat_model;
+
+const char* dcat_last_error(void);
+const char* dcat_version(void);
+
+/* Uploads parameters to `device` (fp32 -> bf16 for the tensor-core path, fp32
+ * kept for the parity path). All host buffers may be freed after return. */
+int dcat_model_create(const dcat_model_config* cfg, const dcat_params* params,
+                      const dcat_table* table, const dcat_head* head, int32_t device,
+                      dcat_model** out);
+int dcat_model_destroy(dcat_model* m);
+
+/* Bit-exact replacement of dedup_segments (dcat.cpp:91-108): rep[n_rows],
+ * first[b_u] (first-appearance order), *b_u. */
+int dcat_dedup(dcat_model* m, const dcat_batch* batch, int32_t* rep, int32_t* first,
+               int32_t* b_u, int32_t flags, void* stream);
+
+/* rank_forward_batch (finetune.cpp:414-493): logits[n_rows*3] and
+ * module_logits[n_rows*3] in fp32 (the reference converts the fp32 values to
+ * double, finetune.cpp:353-356), h_cand[n_rows*d_model] (cross_forward output,
+ * unit-norm rows) when non-NULL. Base and Aux variants and use_seq_module = 0
+ * run on the device; AuxLt and the Lite variants return DCAT_EUNSUPPORTED. */
+int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch,
+                            const dcat_finetune_config* cfg, float* logits,
+                            float* module_logits, float* h_cand, int32_t flags, void* stream);
+
+/* Per-layer K/V of unique u from the last dcat_rank_forward_batch call
+ * (context_forward's KVCache::seqs[u], dcat.hpp:30-41), as fp32 host arrays of
+ * n_u x d_model. *n receives n_u. */
+int dcat_debug_kv(dcat_model* m, int32_t layer, int32_t unique, float* k, float* v, int32_t* n);
+
+/* Stage times (ms) of the last call made with DCAT_PROFILE. Up to `cap`
+ * entries; names[i] points to static strings. Returns the entry count. */
+int dcat_stage_times(dcat_model* m, const char** names, float* ms, int32_t cap);
+
+/* Counters of the last call: kernels launched, unique users, context tokens. */
+typedef struct dcat_call_stats {
+    int64_t kernel_launches;
+    int64_t b_u;
+    int64_t ctx_tokens;
+    int64_t gemm_launches;
+    double gemm_flops;      /* algorithmic flops of all GEMM launches */
+    double attn_flops;      /* algorithmic flops of the attention kernels */
+} dcat_call_stats;
+int dcat_last_stats(dcat_model* m, dcat_call_stats* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DCAT_B200_H */
