@@ -1,0 +1,156 @@
+"""Python mirror of the reference batch scorer over the B200 C ABI.
+
+    DcatModel(weights).rank_forward_batch(batch, ft)
+        == seqfm::rank_forward_batch(p, ids, rp, batch, cfg)   (finetune.hpp:150-154)
+    DcatModel(weights).dedup_segments(batch)
+        == seqfm::dedup_segments(batch, nullptr)               (dcat.hpp:22)
+
+Errors the reference raises as std::runtime_error come back as RuntimeError
+with the library's message. There is no CPU fallback: if libdcat_b200.so is
+missing, importing this module fails.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional
+
+import numpy as np
+
+from .abi import (Batch, BatchC, CallStatsC, FLAG_INPUT_DEVICE, FLAG_PRECISION_FP32, FLAG_PROFILE,
+                  FinetuneConfigC, FinetuneSpec, HeadC, ModelConfigC, ParamsC, TableC, Weights)
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdcat_b200.so")
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        L.dcat_last_error.restype = C.c_char_p
+        L.dcat_version.restype = C.c_char_p
+        L.dcat_model_create.argtypes = [P(ModelConfigC), P(ParamsC), P(TableC), P(HeadC), C.c_int32,
+                                        P(C.c_void_p)]
+        L.dcat_model_destroy.argtypes = [C.c_void_p]
+        L.dcat_dedup.argtypes = [C.c_void_p, P(BatchC), C.c_void_p, C.c_void_p, P(C.c_int32), C.c_int32,
+                                 C.c_void_p]
+        L.dcat_rank_forward_batch.argtypes = [C.c_void_p, P(BatchC), P(FinetuneConfigC), C.c_void_p, C.c_void_p,
+                                              C.c_void_p, C.c_int32, C.c_void_p]
+        L.dcat_debug_kv.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, P(C.c_int32)]
+        L.dcat_stage_times.argtypes = [C.c_void_p, P(C.c_char_p), P(C.c_float), C.c_int32]
+        L.dcat_last_stats.argtypes = [C.c_void_p, P(CallStatsC)]
+        _lib = L
+    return _lib
+
+
+EXPORTS = ("dcat_last_error", "dcat_version", "dcat_model_create", "dcat_model_destroy", "dcat_dedup",
+           "dcat_rank_forward_batch", "dcat_debug_kv", "dcat_stage_times", "dcat_last_stats")
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise RuntimeError(lib().dcat_last_error().decode())
+
+
+class DcatModel:
+    """A model resident on one B200 (weights uploaded once; fp32 -> bf16)."""
+
+    def __init__(self, w: Weights, device: int = 0):
+        self.spec = w.spec
+        self.d_model = w.spec.d_model
+        h = C.c_void_p()
+        _check(lib().dcat_model_create(C.byref(w.spec.c()), C.byref(w.params_c()), C.byref(w.table_c()),
+                                       C.byref(w.head_c()), device, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dcat_model_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------
+    def dedup_segments(self, batch: Batch, stream: int = 0):
+        """(rep, first, b_u) exactly as dedup_segments (dcat.cpp:91-108)."""
+        B = batch.n_rows
+        dev = not isinstance(batch.row_offset, np.ndarray)
+        if dev:
+            import torch
+            rep = torch.empty(max(B, 1), dtype=torch.int32, device=batch.row_offset.device)
+            first = torch.empty(max(B, 1), dtype=torch.int32, device=batch.row_offset.device)
+            rp, fp = rep.data_ptr(), first.data_ptr()
+        else:
+            rep = np.zeros(max(B, 1), np.int32)
+            first = np.zeros(max(B, 1), np.int32)
+            rp, fp = rep.ctypes.data, first.ctypes.data
+        b_u = C.c_int32(0)
+        _check(lib().dcat_dedup(self._h, C.byref(batch.c()), rp, fp, C.byref(b_u),
+                                FLAG_INPUT_DEVICE if dev else 0, C.c_void_p(stream)))
+        return rep[:B], first[:b_u.value], b_u.value
+
+    def rank_forward_batch(self, batch: Batch, ft: FinetuneSpec, *, precision: str = "bf16", want_h: bool = False,
+                           profile: bool = False, stream: int = 0, out=None):
+        """Returns (logits[B,3], module_logits[B,3], h_cand[B,d] or None) as fp32.
+
+        Host (numpy) batches are copied to the device inside the call; torch
+        CUDA batches are used in place and the outputs are torch CUDA tensors."""
+        B = batch.n_rows
+        dev = not isinstance(batch.row_offset, np.ndarray)
+        flags = (FLAG_INPUT_DEVICE if dev else 0) | (FLAG_PRECISION_FP32 if precision == "fp32" else 0) | \
+            (FLAG_PROFILE if profile else 0)
+        if out is not None:
+            logits, mlog, h = out
+        elif dev:
+            import torch
+            kw = dict(dtype=torch.float32, device=batch.row_offset.device)
+            logits = torch.empty((max(B, 1), 3), **kw)
+            mlog = torch.empty((max(B, 1), 3), **kw)
+            h = torch.empty((max(B, 1), self.d_model), **kw) if want_h else None
+        else:
+            logits = np.zeros((max(B, 1), 3), np.float32)
+            mlog = np.zeros_like(logits)
+            h = np.zeros((max(B, 1), self.d_model), np.float32) if want_h else None
+        p = (lambda a: a.data_ptr()) if dev else (lambda a: a.ctypes.data)
+        _check(lib().dcat_rank_forward_batch(self._h, C.byref(batch.c()), C.byref(ft.c()), p(logits), p(mlog),
+                                             p(h) if h is not None else None, flags, C.c_void_p(stream)))
+        return logits[:B], mlog[:B], (h[:B] if h is not None else None)
+
+    # ------------------------------------------------------------------
+    def debug_kv(self, layer: int, unique: int, max_tokens: int):
+        k = np.zeros((max(max_tokens, 1), self.d_model), np.float32)
+        v = np.zeros_like(k)
+        n = C.c_int32(0)
+        _check(lib().dcat_debug_kv(self._h, layer, unique, k.ctypes.data, v.ctypes.data, C.byref(n)))
+        return k[:n.value], v[:n.value]
+
+    def stage_times(self) -> dict:
+        names = (C.c_char_p * 64)()
+        ms = (C.c_float * 64)()
+        n = lib().dcat_stage_times(self._h, names, ms, 64)
+        out = {}
+        for i in range(n):
+            k = names[i].decode()
+            out[k] = out.get(k, 0.0) + ms[i]
+        return out
+
+    def last_stats(self) -> dict:
+        s = CallStatsC()
+        _check(lib().dcat_last_stats(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in CallStatsC._fields_}
+
+
+def probs_from_logits(logits) -> np.ndarray:
+    """RankingOutputs::prob = 1 / (1 + exp(-(double)logit)) (finetune.cpp:355)."""
+    l = np.asarray(logits, np.float64)
+    return 1.0 / (1.0 + np.exp(-l))

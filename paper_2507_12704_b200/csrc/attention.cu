@@ -1,0 +1,348 @@
+// attention.cu — K5 context attention and K6 crossing attention.
+//
+// K5 (context pass): causal multi-head softmax attention of each unique's
+//    tokens over its own tokens, as in layer_forward (model.cpp:353-376).
+// K6 (crossing pass): each candidate query attends to its unique's cached
+//    context K/V plus its own key/value, as in cross_forward (dcat.cpp:231-263).
+//    The reference materializes [K_u; k] per candidate (dcat.cpp:239-243);
+//    here the candidates of one unique are packed as the M dimension of a
+//    query tile (Tile in launch.h), the unique's K/V blocks are staged once per
+//    tile in shared memory and the self key/value enters the online softmax as
+//    a per-row initial state.
+//
+// bf16 path: flash-style kernel, 4 warps x 16 query rows, 64-key blocks
+// double-buffered with cp.async, QK^T and PV on mma.sync m16n8k16 (bf16 in,
+// fp32 accumulate), quad-shuffle row max/sum, online rescaling.
+// fp32 path (parity): one warp per (query, head) restating the reference's
+// exact loop order: logits, max, exp-sum, axpy over keys in order.
+#include <math.h>
+
+#include "launch.h"
+
+namespace dcat {
+
+namespace {
+
+constexpr int BQ = 64;  // queries per CTA (4 warps x 16)
+constexpr int BKV = 64; // keys per block
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    int n = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t* r, const void* p) {
+    uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(s));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t* r, const void* p) {
+    uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(s));
+}
+__device__ __forceinline__ void ldsm_x2_t(uint32_t* r, const void* p) {
+    uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(s));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t* r, const void* p) {
+    uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(s));
+}
+
+__device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int DH, bool CAUSAL>
+__global__ void __launch_bounds__(128) k_flash(AttnArgs p) {
+    constexpr int LD = DH + 8;          // padded smem row (bf16), conflict-free ldmatrix
+    constexpr int CHUNKS = DH / 8;      // 16-byte chunks per row
+    constexpr int NT = DH / 8;          // n-tiles of the output
+    __shared__ __align__(16) bf16 sQ[BQ * LD];
+    __shared__ __align__(16) bf16 sK[2][BKV * LD];
+    __shared__ __align__(16) bf16 sV[2][BKV * LD];
+
+    const Tile tile = p.tiles[blockIdx.x];
+    const int h = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    const bf16* Q = static_cast<const bf16*>(p.q);
+    const bf16* K = static_cast<const bf16*>(p.k);
+    const bf16* V = static_cast<const bf16*>(p.v);
+    const int hc = h * DH;
+
+    // ---- stage Q and the first K/V block
+    for (int i = threadIdx.x; i < BQ * CHUNKS; i += 128) {
+        int r = i / CHUNKS, c = i % CHUNKS;
+        bool ok = r < tile.nq;
+        const bf16* src = Q + static_cast<size_t>(tile.q0 + (ok ? r : 0)) * p.ldq + hc + c * 8;
+        cp_async16(sQ + r * LD + c * 8, src, ok);
+    }
+    const int nblk = (tile.nkv + BKV - 1) / BKV;
+    auto load_kv = [&](int blk, int buf) {
+        for (int i = threadIdx.x; i < BKV * CHUNKS; i += 128) {
+            int r = i / CHUNKS, c = i % CHUNKS;
+            int key = blk * BKV + r;
+            bool ok = key < tile.nkv;
+            size_t off = static_cast<size_t>(tile.kv0 + (ok ? key : 0)) * p.ldkv + hc + c * 8;
+            cp_async16(sK[buf] + r * LD + c * 8, K + off, ok);
+            cp_async16(sV[buf] + r * LD + c * 8, V + off, ok);
+        }
+    };
+    if (nblk > 0) load_kv(0, 0);
+    cp_async_commit();
+
+    const float sl2 = p.scale * 1.4426950408889634f;  // scale * log2(e)
+    const int r0 = warp * 16 + g, r1 = r0 + 8;          // tile-local rows of this thread
+    float o[NT][4];
+    float m0, m1, l0, l1;
+#pragma unroll
+    for (int j = 0; j < NT; j++) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    m0 = m1 = -INFINITY;
+    l0 = l1 = 0.f;
+
+    cp_async_wait<0>();
+    __syncthreads();
+
+    if constexpr (!CAUSAL) {
+        // self term: s = q . k_self, initial state m = s, l = 1, o = v_self
+        const bf16* KS = static_cast<const bf16*>(p.kself);
+        const bf16* VS = static_cast<const bf16*>(p.vself);
+        int q0r = tile.q0 + (r0 < tile.nq ? r0 : 0), q1r = tile.q0 + (r1 < tile.nq ? r1 : 0);
+        float d0 = 0.f, d1 = 0.f;
+#pragma unroll
+        for (int j = 0; j < NT; j++) {
+            int c = j * 8 + 2 * t4;
+            __nv_bfloat162 qa = *reinterpret_cast<const __nv_bfloat162*>(sQ + r0 * LD + c);
+            __nv_bfloat162 qb = *reinterpret_cast<const __nv_bfloat162*>(sQ + r1 * LD + c);
+            __nv_bfloat162 ka = *reinterpret_cast<const __nv_bfloat162*>(KS + static_cast<size_t>(q0r) * p.ldself + hc + c);
+            __nv_bfloat162 kb = *reinterpret_cast<const __nv_bfloat162*>(KS + static_cast<size_t>(q1r) * p.ldself + hc + c);
+            float2 qa2 = __bfloat1622float2(qa), qb2 = __bfloat1622float2(qb);
+            float2 ka2 = __bfloat1622float2(ka), kb2 = __bfloat1622float2(kb);
+            d0 += qa2.x * ka2.x + qa2.y * ka2.y;
+            d1 += qb2.x * kb2.x + qb2.y * kb2.y;
+            float2 va = __bfloat1622float2(
+                *reinterpret_cast<const __nv_bfloat162*>(VS + static_cast<size_t>(q0r) * p.ldself + hc + c));
+            float2 vb = __bfloat1622float2(
+                *reinterpret_cast<const __nv_bfloat162*>(VS + static_cast<size_t>(q1r) * p.ldself + hc + c));
+            o[j][0] = va.x;
+            o[j][1] = va.y;
+            o[j][2] = vb.x;
+            o[j][3] = vb.y;
+        }
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 1);
+        d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, 1);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
+        m0 = d0 * sl2;
+        m1 = d1 * sl2;
+        l0 = l1 = (t4 == 0) ? 1.f : 0.f;
+    }
+
+    // Q fragments (A operand), kept in registers for all key blocks
+    uint32_t qf[DH / 16][4];
+#pragma unroll
+    for (int kk = 0; kk < DH / 16; kk++) {
+        int row = warp * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
+        int col = kk * 16 + 8 * (lane >> 4);
+        ldsm_x4(qf[kk], sQ + row * LD + col);
+    }
+
+    for (int blk = 0; blk < nblk; blk++) {
+        const int buf = blk & 1;
+        if (blk + 1 < nblk) load_kv(blk + 1, buf ^ 1);
+        cp_async_commit();
+
+        // S = Q K^T for 64 keys: 8 n-tiles of 8 keys
+        float s[8][4];
+#pragma unroll
+        for (int j = 0; j < 8; j++) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+        const bf16* kb = sK[buf];
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; kk++) {
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+                uint32_t b[4];
+                int key = 8 * (j + (lane >> 4)) + (lane & 7);
+                int col = kk * 16 + 8 * ((lane >> 3) & 1);
+                ldsm_x4(b, kb + key * LD + col);
+                mma16816(s[j], qf[kk], b[0], b[1]);
+                mma16816(s[j + 1], qf[kk], b[2], b[3]);
+            }
+        }
+        // mask + block row max
+        const int kbase = blk * BKV;
+        float bm0 = -INFINITY, bm1 = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                int key = kbase + 8 * j + 2 * t4 + (e & 1);
+                int row = (e < 2) ? r0 : r1;
+                bool ok = key < tile.nkv;
+                if (CAUSAL) ok = ok && key <= tile.qloc + row;
+                float x = ok ? s[j][e] * sl2 : -INFINITY;
+                s[j][e] = x;
+                if (e < 2) bm0 = fmaxf(bm0, x);
+                else bm1 = fmaxf(bm1, x);
+            }
+        }
+        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
+        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
+        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
+        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
+        float nm0 = fmaxf(m0, bm0), nm1 = fmaxf(m1, bm1);
+        float u0 = nm0 == -INFINITY ? 0.f : nm0, u1 = nm1 == -INFINITY ? 0.f : nm1;
+        float a0 = exp2f(m0 - u0), a1 = exp2f(m1 - u1);
+        m0 = nm0;
+        m1 = nm1;
+        l0 *= a0;
+        l1 *= a1;
+#pragma unroll
+        for (int j = 0; j < NT; j++) {
+            o[j][0] *= a0;
+            o[j][1] *= a0;
+            o[j][2] *= a1;
+            o[j][3] *= a1;
+        }
+        uint32_t pf[4][4];
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            float p0 = exp2f(s[j][0] - u0), p1 = exp2f(s[j][1] - u0);
+            float p2 = exp2f(s[j][2] - u1), p3 = exp2f(s[j][3] - u1);
+            l0 += p0 + p1;
+            l1 += p2 + p3;
+            pf[j >> 1][(j & 1) * 2 + 0] = pack_bf16(p0, p1);
+            pf[j >> 1][(j & 1) * 2 + 1] = pack_bf16(p2, p3);
+        }
+        // O += P V
+        const bf16* vb = sV[buf];
+#pragma unroll
+        for (int kk = 0; kk < 4; kk++) {
+            uint32_t a[4] = {pf[kk][0], pf[kk][1], pf[kk][2], pf[kk][3]};
+            int key = kk * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
+            if constexpr (NT >= 2) {
+#pragma unroll
+                for (int j = 0; j < NT; j += 2) {
+                    uint32_t b[4];
+                    ldsm_x4_t(b, vb + key * LD + 8 * (j + (lane >> 4)));
+                    mma16816(o[j], a, b[0], b[1]);
+                    mma16816(o[j + 1], a, b[2], b[3]);
+                }
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+    }
+
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    float i0 = 1.f / l0, i1 = 1.f / l1;
+    bf16* O = static_cast<bf16*>(p.out);
+#pragma unroll
+    for (int j = 0; j < NT; j++) {
+        int c = hc + j * 8 + 2 * t4;
+        if (r0 < tile.nq)
+            *reinterpret_cast<uint32_t*>(O + static_cast<size_t>(tile.q0 + r0) * p.ldo + c) =
+                pack_bf16(o[j][0] * i0, o[j][1] * i0);
+        if (r1 < tile.nq)
+            *reinterpret_cast<uint32_t*>(O + static_cast<size_t>(tile.q0 + r1) * p.ldo + c) =
+                pack_bf16(o[j][2] * i1, o[j][3] * i1);
+    }
+}
+
+// ---- fp32 parity kernel: one warp per (query row, head), reference loop order
+__global__ void k_attn_f32(AttnArgs p, int max_keys) {
+    extern __shared__ float logits_all[];
+    const Tile tile = p.tiles[blockIdx.x];
+    const int h = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    float* logits = logits_all + warp * (max_keys + 1);
+    const float* Q = static_cast<const float*>(p.q);
+    const float* K = static_cast<const float*>(p.k);
+    const float* V = static_cast<const float*>(p.v);
+    const int dh = p.dh, hc = h * dh;
+    for (int r = warp; r < tile.nq; r += nw) {
+        const float* q = Q + static_cast<size_t>(tile.q0 + r) * p.ldq + hc;
+        int nkeys = p.causal ? tile.qloc + r + 1 : tile.nkv + 1;  // crossing: context + self (last)
+        float mx = -INFINITY;
+        for (int j = 0; j < nkeys; j++) {
+            const float* kr;
+            if (!p.causal && j == tile.nkv)
+                kr = static_cast<const float*>(p.kself) + static_cast<size_t>(tile.q0 + r) * p.ldself + hc;
+            else
+                kr = K + static_cast<size_t>(tile.kv0 + j) * p.ldkv + hc;
+            float part = 0.f;
+            for (int d = lane; d < dh; d += 32) part += q[d] * kr[d];
+            float sdot = warp_sum(part) * p.scale;
+            if (lane == 0) logits[j] = sdot;
+            mx = fmaxf(mx, sdot);
+        }
+        __syncwarp();
+        float denom = 0.f;
+        for (int j = 0; j < nkeys; j++) denom += expf(logits[j] - mx);
+        float inv = 1.0f / denom;
+        for (int d = lane; d < dh; d += 32) {
+            float acc = 0.f;
+            for (int j = 0; j < nkeys; j++) {
+                const float* vr;
+                if (!p.causal && j == tile.nkv)
+                    vr = static_cast<const float*>(p.vself) + static_cast<size_t>(tile.q0 + r) * p.ldself + hc;
+                else
+                    vr = V + static_cast<size_t>(tile.kv0 + j) * p.ldkv + hc;
+                acc += (expf(logits[j] - mx) * inv) * vr[d];
+            }
+            static_cast<float*>(p.out)[static_cast<size_t>(tile.q0 + r) * p.ldo + hc + d] = acc;
+        }
+        __syncwarp();
+    }
+}
+
+template <int DH>
+void launch_flash(const AttnArgs& a, cudaStream_t s) {
+    dim3 grid(a.n_tiles, a.n_heads);
+    if (a.causal) k_flash<DH, true><<<grid, 128, 0, s>>>(a);
+    else k_flash<DH, false><<<grid, 128, 0, s>>>(a);
+    DCAT_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void attention_bf16(const AttnArgs& a, cudaStream_t s) {
+    if (a.n_tiles <= 0) return;
+    switch (a.dh) {
+        case 16: launch_flash<16>(a, s); break;
+        case 32: launch_flash<32>(a, s); break;
+        case 64: launch_flash<64>(a, s); break;
+        default: throw InvalidArg("attention: head dim " + std::to_string(a.dh) + " not supported (16/32/64)");
+    }
+}
+
+void attention_f32(const AttnArgs& a, cudaStream_t s) {
+    if (a.n_tiles <= 0) return;
+    const int warps = 4;
+    size_t smem = static_cast<size_t>(warps) * (a.max_keys + 2) * sizeof(float);
+    dim3 grid(a.n_tiles, a.n_heads);
+    if (smem > 48 * 1024)
+        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_attn_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
+    k_attn_f32<<<grid, warps * 32, smem, s>>>(a, a.max_keys + 1);
+    DCAT_LAUNCH_CHECK();
+}
+
+}  // namespace dcat

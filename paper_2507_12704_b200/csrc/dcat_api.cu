@@ -1,0 +1,921 @@
+// dcat_api.cu — the C ABI (include/dcat_b200.h) and the host runtime that
+// orchestrates the DCAT scoring forward on one B200.
+//
+// rank_forward_batch (/root/reference/proj/src/finetune.cpp:414-493):
+//   dedup (K1)  ->  context pass: gather (K2), phi_in, layers 0..L-2
+//   (QKV / causal attention K5 / O+LN / FFN), last layer K,V only
+//   (dcat.cpp:137-178)  ->  crossing pass: candidate gather, phi_in, L layers
+//   (QKV / crossing attention K6 / O+LN / FFN), phi_out + module head
+//   (dcat.cpp:199-271)  ->  ranking head (finetune.cpp:301-324)  ->  scatter.
+// Inputs are validated on the device in the dedup pass (the reference's
+// SEQFM_CHECKs) and reported through dcat_last_error().
+#include <cuda_bf16.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/dcat_b200.h"
+#include "launch.h"
+
+using namespace dcat;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+uint64_t host_mix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+    ~Buf() {
+        if (p) cudaFree(p);
+    }
+    template <typename T>
+    T* get(size_t n) {
+        size_t bytes = std::max<size_t>(n * sizeof(T), 256);
+        if (bytes > cap) {
+            if (p) DCAT_CUDA_CHECK(cudaFree(p));
+            p = nullptr;
+            size_t c = bytes + bytes / 4;
+            c = (c + 4095) & ~size_t(4095);
+            DCAT_CUDA_CHECK(cudaMalloc(&p, c));
+            cap = c;
+        }
+        return static_cast<T*>(p);
+    }
+};
+
+// One linear layer, stored for both paths.
+struct Lin {
+    bf16* wt = nullptr;   // [out x in] bf16 (tensor-core path, K-major)
+    float* w32 = nullptr; // [in x out] fp32 (parity path, reference layout)
+    float* bias = nullptr;
+    int in = 0, out = 0;
+};
+
+struct LayerW {
+    float *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+    Lin qkv, o, f1, f2;  // qkv = [Wq | Wk | Wv] along the output dim
+};
+
+struct DevAlloc {
+    std::vector<void*> ptrs;
+    ~DevAlloc() {
+        for (void* p : ptrs) cudaFree(p);
+    }
+    template <typename T>
+    T* upload(const T* h, size_t n) {
+        void* p = nullptr;
+        DCAT_CUDA_CHECK(cudaMalloc(&p, std::max<size_t>(n * sizeof(T), 16)));
+        ptrs.push_back(p);
+        if (n) DCAT_CUDA_CHECK(cudaMemcpy(p, h, n * sizeof(T), cudaMemcpyHostToDevice));
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace
+
+struct dcat_model {
+    int device = 0;
+    dcat_model_config cfg{};
+    DevAlloc mem;
+    // embeddings (fp32)
+    float* table = nullptr;
+    uint64_t* seed_mix = nullptr;
+    int J = 0, R = 0, d_sub = 0;
+    float *action_emb = nullptr, *surface_emb = nullptr, *pos_emb = nullptr;
+    Lin phi_in1, phi_in2, phi_out1, phi_out2;
+    std::vector<LayerW> layers;
+    // ranking head
+    int d_module = 0, head_demb = 0, n_ctx = 0, hidden = 0, d_aux = 0, kh = 0, d_feat = 0;
+    Lin head1;  // [feat -> hidden], wt zero-padded to kh columns
+    float *hw2 = nullptr, *hb2 = nullptr, *mod_w = nullptr, *mod_b = nullptr, *aux_proj = nullptr;
+    // status
+    Status* st_dev = nullptr;
+    Status* st_host = nullptr;
+    // workspace
+    Buf b_in[8];
+    Buf b_dd[24];
+    Buf b_act[20];
+    Buf b_kv;
+    Buf b_aux;
+    Buf b_out[3];
+    // last-call bookkeeping
+    int64_t last_bu = 0, last_T = 0, last_Tp = 0;
+    int last_precision_f32 = 0;
+    void* last_kv = nullptr;
+    std::vector<int64_t> last_tok_off;
+    dcat_call_stats stats{};
+    std::vector<std::pair<const char*, float>> stage_ms;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<const char*, std::pair<int, int>>> ev_marks;
+    bool profiling = false;
+    int ev_next = 0;
+
+    ~dcat_model() {
+        if (st_host) cudaFreeHost(st_host);
+        for (auto e : ev_pool) cudaEventDestroy(e);
+    }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- profiling
+int mark(dcat_model* m, cudaStream_t s) {
+    if (!m->profiling) return -1;
+    if (m->ev_next >= static_cast<int>(m->ev_pool.size())) {
+        cudaEvent_t e;
+        DCAT_CUDA_CHECK(cudaEventCreate(&e));
+        m->ev_pool.push_back(e);
+    }
+    int i = m->ev_next++;
+    DCAT_CUDA_CHECK(cudaEventRecord(m->ev_pool[i], s));
+    return i;
+}
+void span(dcat_model* m, const char* name, int a, int b) {
+    if (a >= 0 && b >= 0) m->ev_marks.push_back({name, {a, b}});
+}
+
+// ---------------------------------------------------------------- upload
+Lin make_lin(DevAlloc& mem, const float* w, const float* b, int in, int out, int k_pad = 0) {
+    Lin L;
+    L.in = in;
+    L.out = out;
+    int kp = std::max(in, k_pad);
+    std::vector<bf16> wt(static_cast<size_t>(out) * kp, __float2bfloat16(0.0f));
+    for (int i = 0; i < in; i++)
+        for (int o = 0; o < out; o++)
+            wt[static_cast<size_t>(o) * kp + i] = __float2bfloat16_rn(w[static_cast<size_t>(i) * out + o]);
+    L.wt = mem.upload(wt.data(), wt.size());
+    L.w32 = mem.upload(w, static_cast<size_t>(in) * out);
+    std::vector<float> bz(static_cast<size_t>(out), 0.0f);
+    L.bias = mem.upload(b ? b : bz.data(), static_cast<size_t>(out));
+    return L;
+}
+
+// [Wq | Wk | Wv] concatenated along the output dimension
+Lin make_qkv(DevAlloc& mem, const float* wq, const float* bq, const float* wk, const float* bk, const float* wv,
+             const float* bv, int d) {
+    std::vector<float> w(static_cast<size_t>(d) * 3 * d), b(static_cast<size_t>(3) * d);
+    const float* ws[3] = {wq, wk, wv};
+    const float* bs[3] = {bq, bk, bv};
+    for (int s = 0; s < 3; s++) {
+        for (int i = 0; i < d; i++)
+            for (int o = 0; o < d; o++) w[static_cast<size_t>(i) * 3 * d + s * d + o] = ws[s][static_cast<size_t>(i) * d + o];
+        for (int o = 0; o < d; o++) b[s * d + o] = bs[s][o];
+    }
+    return make_lin(mem, w.data(), b.data(), d, 3 * d);
+}
+
+// ---------------------------------------------------------------- error text
+std::string status_message(const dcat_model* m, const Status& st, int* code) {
+    *code = DCAT_EINVAL;
+    char buf[256];
+    int b = st.err_bits;
+    if (b & ERR_RANGE) snprintf(buf, sizeof buf, "row %d: events out of range (valid %d)", st.err_row, st.err_val);
+    else if (b & ERR_ACTION) snprintf(buf, sizeof buf, "unknown action value %d (row %d)", st.err_val, st.err_row);
+    else if (b & ERR_SURFACE) snprintf(buf, sizeof buf, "unknown surface value %d (row %d)", st.err_val, st.err_row);
+    else if (b & ERR_POS_CTX)
+        snprintf(buf, sizeof buf, "position %d exceeds max_len %d (row %d)", st.err_val, m->cfg.max_len, st.err_row);
+    else if (b & ERR_POS_CAND)
+        snprintf(buf, sizeof buf, "candidate_inputs: position %d out of range (max_len %d)", st.err_val,
+                 m->cfg.max_len);
+    else if (b & ERR_AGE) snprintf(buf, sizeof buf, "candidate age must be non-negative (row %d)", st.err_row);
+    else if (st.nonfinite_layer > 0) {
+        *code = DCAT_ENONFINITE;
+        snprintf(buf, sizeof buf, "non-finite activation in layer %d", st.nonfinite_layer - 1);
+    } else
+        return "";
+    return buf;
+}
+
+// ---------------------------------------------------------------- staging
+struct Staged {
+    DedupIn in;
+    const uint64_t* candidate;
+    const double* age;
+    const float* aux;
+};
+
+template <typename T>
+const T* stage(Buf& b, const T* src, size_t n, bool device, cudaStream_t s, int64_t* h2d) {
+    if (device || src == nullptr) return src;
+    T* d = b.get<T>(n);
+    if (n) DCAT_CUDA_CHECK(cudaMemcpyAsync(d, src, n * sizeof(T), cudaMemcpyHostToDevice, s));
+    *h2d += static_cast<int64_t>(n * sizeof(T));
+    return d;
+}
+
+Staged stage_batch(dcat_model* m, const dcat_batch* b, bool device, bool aux_needed, cudaStream_t s) {
+    Staged st;
+    int64_t h2d = 0;
+    int64_t B = b->n_rows, E = b->n_events;
+    st.in.B = B;
+    st.in.row_offset = stage(m->b_in[0], b->row_offset, B, device, s, &h2d);
+    st.in.row_valid = stage(m->b_in[1], b->row_valid, B, device, s, &h2d);
+    st.in.n_events = E;
+    // one pooled copy for the four event arrays
+    if (device) {
+        st.in.ts = b->ev_ts;
+        st.in.action = b->ev_action;
+        st.in.surface = b->ev_surface;
+        st.in.item = b->ev_item;
+    } else {
+        st.in.ts = stage(m->b_in[2], b->ev_ts, E, false, s, &h2d);
+        st.in.item = stage(m->b_in[3], b->ev_item, E, false, s, &h2d);
+        st.in.action = stage(m->b_in[4], b->ev_action, E, false, s, &h2d);
+        st.in.surface = stage(m->b_in[5], b->ev_surface, E, false, s, &h2d);
+    }
+    st.in.n_actions = m->cfg.n_actions;
+    st.in.n_surfaces = m->cfg.n_surfaces;
+    st.in.max_len = m->cfg.max_len;
+    st.in.pos_learned = m->cfg.pos_learned;
+    st.candidate = stage(m->b_in[6], b->candidate, B, device, s, &h2d);
+    st.age = stage(m->b_in[7], b->age_seconds, B, device, s, &h2d);
+    st.aux = nullptr;
+    if (aux_needed && b->aux) {
+        st.aux = stage(m->b_aux, b->aux, static_cast<size_t>(B) * b->d_aux, device, s, &h2d);
+    }
+    return st;
+}
+
+DedupOut dedup_buffers(dcat_model* m, int64_t B) {
+    DedupOut o;
+    int64_t cap = 1024;
+    while (cap < 2 * B) cap <<= 1;
+    size_t n1 = static_cast<size_t>(B) + 1;
+    o.hash = m->b_dd[0].get<uint64_t>(B);
+    o.tab_key = m->b_dd[1].get<uint64_t>(cap);
+    o.tab_val = m->b_dd[2].get<int32_t>(cap);
+    o.tab_cap = cap;
+    o.slot = m->b_dd[3].get<int32_t>(B);
+    o.head = m->b_dd[4].get<int32_t>(B);
+    o.collided = m->b_dd[5].get<int32_t>(B);
+    o.list = m->b_dd[6].get<int32_t>(B);
+    o.list_n = m->b_dd[7].get<int32_t>(1);
+    o.scan_tmp = m->b_dd[8].get<int64_t>(n1);
+    o.scan_blk = m->b_dd[9].get<int64_t>(4097);
+    o.uid = m->b_dd[10].get<int64_t>(n1);
+    o.rep = m->b_dd[11].get<int32_t>(B);
+    o.first = m->b_dd[12].get<int32_t>(B);
+    o.cnt = m->b_dd[13].get<int32_t>(B);
+    o.cursor = m->b_dd[14].get<int32_t>(B);
+    o.goff = m->b_dd[15].get<int64_t>(n1);
+    o.perm = m->b_dd[16].get<int32_t>(B);
+    o.tok_off = m->b_dd[17].get<int64_t>(n1);
+    o.ctx_toff = m->b_dd[18].get<int64_t>(n1);
+    o.cross_toff = m->b_dd[19].get<int64_t>(n1);
+    o.st = m->st_dev;
+    return o;
+}
+
+uint64_t debug_hash_mask() {
+    const char* e = getenv("DCAT_DEBUG_HASH_BITS");  // test knob: force 64-bit hash collisions
+    if (!e) return ~0ull;
+    int bits = atoi(e);
+    if (bits <= 0 || bits >= 64) return ~0ull;
+    return (1ull << bits) - 1;
+}
+
+constexpr int kTileCtx = 64;
+constexpr int kTileCross = 64;
+
+// dedup + validation; leaves the plan on the device and the counts in m->st_host
+void run_dedup(dcat_model* m, const Staged& sb, const DedupOut& o, cudaStream_t s) {
+    uint64_t mask = debug_hash_mask();
+    dedup_plan(sb.in, o, mask, kTileCtx, kTileCross, s);
+    m->stats.kernel_launches += 23;
+    DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
+    DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (m->st_host->collisions > 0 && m->st_host->err_bits == 0) {
+        dedup_repair(sb.in, o, m->st_host->collisions, kTileCtx, kTileCross, mask, s);
+        m->stats.kernel_launches += 5 * 5 + 20;
+        DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
+        DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+}
+
+// ---------------------------------------------------------------- the pipeline
+template <typename T>
+struct Acts {
+    T *E, *h1, *a, *q, *ctx, *f1, *kself, *vself, *feat;
+    float *x, *hc, *logits_p, *mlog_p, *tmp;
+    T* kv;  // [2 L] x Tp x d
+    int64_t Tp, Bp;
+};
+
+template <typename T>
+void gemm(dcat_model* m, const T* A, int lda, const Lin& L, int w_off, int N, int M, const Epi& e, float* tmp,
+          cudaStream_t s) {
+    if (M <= 0) return;
+    if constexpr (std::is_same<T, bf16>::value) {
+        gemm_tc(A, lda, L.wt + static_cast<size_t>(w_off) * L.in, L.in, M, N, L.in, e, s);
+        m->stats.kernel_launches += 1;
+    } else {
+        gemm_f32(A, lda, L.w32 + w_off, L.out, M, N, L.in, e, tmp, s);
+        m->stats.kernel_launches += 2;
+    }
+    m->stats.gemm_launches += 1;
+    m->stats.gemm_flops += 2.0 * M * N * L.in;
+}
+
+Epi base_epi(dcat_model* m, int mode, int layer_idx = -1) {
+    Epi e;
+    std::memset(&e, 0, sizeof e);
+    e.mode = mode;
+    e.st = m->st_dev;
+    e.layer_idx = layer_idx;
+    return e;
+}
+
+template <typename T>
+void attn(dcat_model* m, const AttnArgs& a, cudaStream_t s) {
+    if constexpr (std::is_same<T, bf16>::value) attention_bf16(a, s);
+    else attention_f32(a, s);
+    m->stats.kernel_launches += 1;
+}
+
+// Base / Aux with the sequence module (finetune.cpp:459-492)
+template <typename T>
+void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_finetune_config& ft, float* logits,
+              float* mlogits, float* h_cand, cudaStream_t s) {
+    const dcat_model_config& c = m->cfg;
+    const int d = c.d_model, de = c.d_emb, F = c.d_model * c.mlp_ratio, H = c.n_heads, dh = d / H, nl = c.n_layers;
+    const Status& st = *m->st_host;
+    const int b_u = st.b_u;
+    const int64_t T_ctx = st.ctx_tokens, B = sb.in.B;
+    const int64_t Tp = (T_ctx + 127) / 128 * 128, Bp = (B + 127) / 128 * 128, Rr = std::max(Tp, Bp);
+    const bool f32 = std::is_same<T, float>::value;
+    const int kh = f32 ? m->d_feat : m->kh;
+
+    int t_stage0 = mark(m, s);
+    // tiles + token map
+    Tile* ctx_tiles = m->b_dd[20].get<Tile>(std::max(st.ctx_tiles, 1));
+    Tile* cross_tiles = m->b_dd[21].get<Tile>(std::max(st.cross_tiles, 1));
+    int32_t* tok_unique = m->b_dd[22].get<int32_t>(std::max<int64_t>(T_ctx, 1));
+    build_tiles(sb.in, o, b_u, kTileCtx, kTileCross, ctx_tiles, cross_tiles, tok_unique, s);
+    m->stats.kernel_launches += 2;
+
+    Acts<T> A;
+    A.Tp = Tp;
+    A.Bp = Bp;
+    A.E = m->b_act[0].get<T>(Rr * de);
+    A.h1 = m->b_act[1].get<T>(Rr * d);
+    A.a = m->b_act[2].get<T>(Rr * d);
+    A.q = m->b_act[3].get<T>(Rr * d);
+    A.ctx = m->b_act[4].get<T>(Rr * d);
+    A.f1 = m->b_act[5].get<T>(Rr * F);
+    A.kself = m->b_act[6].get<T>(Bp * d);
+    A.vself = m->b_act[7].get<T>(Bp * d);
+    A.feat = m->b_act[8].get<T>(Bp * kh);
+    A.x = m->b_act[9].get<float>(Rr * d);
+    A.hc = m->b_act[10].get<float>(Bp * d);
+    A.logits_p = m->b_act[11].get<float>(Bp * 3);
+    A.mlog_p = m->b_act[12].get<float>(Bp * 3);
+    A.tmp = f32 ? m->b_act[13].get<float>(Rr * std::max(3 * d, std::max(F, m->hidden))) : nullptr;
+    A.kv = m->b_kv.get<T>(std::max<int64_t>(2 * nl * Tp * d, 1));
+    m->last_kv = A.kv;
+    m->last_Tp = Tp;
+
+    EmbParams ep{m->table, m->seed_mix, m->J, m->R, m->d_sub, m->action_emb, m->surface_emb, m->pos_emb, de};
+    const float scale = 1.0f / std::sqrt(static_cast<float>(dh));
+    auto K_l = [&](int l) { return A.kv + static_cast<size_t>(2 * l) * Tp * d; };
+    auto V_l = [&](int l) { return A.kv + static_cast<size_t>(2 * l + 1) * Tp * d; };
+
+    // ============ context pass (context_forward, emit_hidden = false) ============
+    int t_ctx0 = mark(m, s);
+    if (T_ctx > 0) {
+        const int M = static_cast<int>(T_ctx);
+        gather_context<T>(sb.in, o, ep, tok_unique, T_ctx, A.E, de, s);
+        m->stats.kernel_launches += 1;
+        // phi_in (model.cpp:144-161) -> x, then LN1 of layer 0
+        Epi e = base_epi(m, EPI_BIAS);
+        e.act = 1;
+        e.bias = m->phi_in1.bias;
+        e.out[0] = A.h1;
+        e.out_ld[0] = d;
+        e.seg_cols = d;
+        gemm<T>(m, A.E, de, m->phi_in1, 0, d, M, e, A.tmp, s);
+        e = base_epi(m, EPI_L2NORM);
+        e.bias = m->phi_in2.bias;
+        e.x_out = A.x;
+        e.ld_x = d;
+        e.ln_g = m->layers[0].ln1_g;
+        e.ln_b = m->layers[0].ln1_b;
+        e.ln_out = A.a;
+        e.ln_ld = d;
+        gemm<T>(m, A.h1, d, m->phi_in2, 0, d, M, e, A.tmp, s);
+        for (int l = 0; l < nl; l++) {
+            const LayerW& L = m->layers[l];
+            if (l == nl - 1) {  // kv_only (dcat.cpp:60-65): K, V of the final layer
+                e = base_epi(m, EPI_BIAS);
+                e.bias = L.qkv.bias + d;
+                e.out[0] = K_l(l);
+                e.out[1] = V_l(l);
+                e.out_ld[0] = e.out_ld[1] = d;
+                e.seg_cols = d;
+                gemm<T>(m, A.a, d, L.qkv, d, 2 * d, M, e, A.tmp, s);
+                break;
+            }
+            // layer_forward (model.cpp:336-398); K, V go straight to the cache
+            e = base_epi(m, EPI_BIAS);
+            e.bias = L.qkv.bias;
+            e.out[0] = A.q;
+            e.out[1] = K_l(l);
+            e.out[2] = V_l(l);
+            e.out_ld[0] = e.out_ld[1] = e.out_ld[2] = d;
+            e.seg_cols = d;
+            gemm<T>(m, A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
+            AttnArgs aa{A.q, d, K_l(l), V_l(l), d, nullptr, nullptr, 0, A.ctx, d, ctx_tiles, st.ctx_tiles,
+                        H,   dh, scale, 1, c.max_len + 1};
+            attn<T>(m, aa, s);
+            m->stats.attn_flops += 0;  // accounted analytically by the caller
+            e = base_epi(m, EPI_RESID_LN, l);
+            e.bias = L.o.bias;
+            e.resid = A.x;
+            e.x_out = A.x;
+            e.ld_x = d;
+            e.ln_g = L.ln2_g;
+            e.ln_b = L.ln2_b;
+            e.ln_out = A.a;
+            e.ln_ld = d;
+            gemm<T>(m, A.ctx, d, L.o, 0, d, M, e, A.tmp, s);
+            e = base_epi(m, EPI_BIAS);
+            e.act = 1;
+            e.bias = L.f1.bias;
+            e.out[0] = A.f1;
+            e.out_ld[0] = F;
+            e.seg_cols = F;
+            gemm<T>(m, A.a, d, L.f1, 0, F, M, e, A.tmp, s);
+            e = base_epi(m, EPI_RESID_LN, l);
+            e.bias = L.f2.bias;
+            e.resid = A.x;
+            e.x_out = A.x;
+            e.ld_x = d;
+            e.ln_g = m->layers[l + 1].ln1_g;
+            e.ln_b = m->layers[l + 1].ln1_b;
+            e.ln_out = A.a;
+            e.ln_ld = d;
+            gemm<T>(m, A.f1, F, L.f2, 0, d, M, e, A.tmp, s);
+        }
+    }
+    int t_ctx1 = mark(m, s);
+
+    // ============ crossing pass (candidate_inputs + cross_forward) ============
+    const int M = static_cast<int>(B);
+    CandParams cp{sb.candidate, sb.age, sb.aux, m->aux_proj, m->d_aux, ft.variant == DCAT_VARIANT_AUX,
+                  ft.max_events, ft.fresh_days, ft.mid_days, m->d_module, kh};
+    gather_candidates<T>(sb.in, o, ep, cp, B, A.E, de, A.feat, s);
+    m->stats.kernel_launches += 1;
+    Epi e = base_epi(m, EPI_BIAS);
+    e.act = 1;
+    e.bias = m->phi_in1.bias;
+    e.out[0] = A.h1;
+    e.out_ld[0] = d;
+    e.seg_cols = d;
+    gemm<T>(m, A.E, de, m->phi_in1, 0, d, M, e, A.tmp, s);
+    e = base_epi(m, EPI_L2NORM);
+    e.bias = m->phi_in2.bias;
+    e.x_out = A.x;
+    e.ld_x = d;
+    e.ln_g = m->layers[0].ln1_g;
+    e.ln_b = m->layers[0].ln1_b;
+    e.ln_out = A.a;
+    e.ln_ld = d;
+    gemm<T>(m, A.h1, d, m->phi_in2, 0, d, M, e, A.tmp, s);
+    for (int l = 0; l < nl; l++) {
+        const LayerW& L = m->layers[l];
+        e = base_epi(m, EPI_BIAS);
+        e.bias = L.qkv.bias;
+        e.out[0] = A.q;
+        e.out[1] = A.kself;
+        e.out[2] = A.vself;
+        e.out_ld[0] = e.out_ld[1] = e.out_ld[2] = d;
+        e.seg_cols = d;
+        gemm<T>(m, A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
+        AttnArgs aa{A.q, d, K_l(l), V_l(l), d, A.kself, A.vself, d, A.ctx, d, cross_tiles, st.cross_tiles,
+                    H,   dh, scale, 0, c.max_len + 1};
+        attn<T>(m, aa, s);
+        e = base_epi(m, EPI_RESID_LN, l);
+        e.bias = L.o.bias;
+        e.resid = A.x;
+        e.x_out = A.x;
+        e.ld_x = d;
+        e.ln_g = L.ln2_g;
+        e.ln_b = L.ln2_b;
+        e.ln_out = A.a;
+        e.ln_ld = d;
+        gemm<T>(m, A.ctx, d, L.o, 0, d, M, e, A.tmp, s);
+        e = base_epi(m, EPI_BIAS);
+        e.act = 1;
+        e.bias = L.f1.bias;
+        e.out[0] = A.f1;
+        e.out_ld[0] = F;
+        e.seg_cols = F;
+        gemm<T>(m, A.a, d, L.f1, 0, F, M, e, A.tmp, s);
+        e = base_epi(m, EPI_RESID_LN, l);  // cross_tail's finite check (dcat.cpp:85-86)
+        e.bias = L.f2.bias;
+        e.resid = A.x;
+        e.x_out = A.x;
+        e.ld_x = d;
+        e.ln_g = l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr;  // last layer: plain copy for phi_out
+        e.ln_b = l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr;
+        e.ln_out = A.a;
+        e.ln_ld = d;
+        gemm<T>(m, A.f1, F, L.f2, 0, d, M, e, A.tmp, s);
+    }
+    // phi_out (dcat.cpp:266) + module head (finetune.cpp:317-323)
+    e = base_epi(m, EPI_BIAS);
+    e.act = 1;
+    e.bias = m->phi_out1.bias;
+    e.out[0] = A.h1;
+    e.out_ld[0] = d;
+    e.seg_cols = d;
+    gemm<T>(m, A.a, d, m->phi_out1, 0, d, M, e, A.tmp, s);
+    e = base_epi(m, EPI_L2NORM);
+    e.bias = m->phi_out2.bias;
+    e.x_out = h_cand ? A.hc : nullptr;
+    e.ld_x = d;
+    e.out2 = A.feat;  // H_cand occupies feat columns [0, d)
+    e.out2_ld = kh;
+    e.mod_w = m->mod_w;
+    e.mod_b = m->mod_b;
+    e.mlogits = A.mlog_p;
+    gemm<T>(m, A.h1, d, m->phi_out2, 0, d, M, e, A.tmp, s);
+    int t_cross1 = mark(m, s);
+    // ranking head: crossing MLP on [H_cand | cand_emb | ctx] (finetune.cpp:301-316)
+    e = base_epi(m, EPI_HEAD);
+    e.bias = m->head1.bias;
+    e.w2 = m->hw2;
+    e.b2 = m->hb2;
+    e.logits = A.logits_p;
+    gemm<T>(m, A.feat, kh, m->head1, 0, m->hidden, M, e, A.tmp, s);
+    scatter_outputs(o.perm, B, A.logits_p, A.mlog_p, h_cand ? A.hc : nullptr, d, logits, mlogits, h_cand, s);
+    m->stats.kernel_launches += 1;
+    int t_end = mark(m, s);
+    span(m, "plan", t_stage0, t_ctx0);
+    span(m, "context", t_ctx0, t_ctx1);
+    span(m, "cross", t_ctx1, t_cross1);
+    span(m, "head", t_cross1, t_end);
+}
+
+// use_seq_module = false: crossing MLP on [cand_emb | ctx] only (finetune.cpp:342-347)
+template <typename T>
+void run_head_only(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_finetune_config& ft,
+                   float* logits, float* mlogits, cudaStream_t s) {
+    const int64_t B = sb.in.B, Bp = (B + 127) / 128 * 128;
+    const bool f32 = std::is_same<T, float>::value;
+    const int kh = f32 ? m->d_feat : m->kh;
+    T* feat = m->b_act[8].get<T>(Bp * kh);
+    T* E = m->b_act[0].get<T>(Bp * m->cfg.d_emb);
+    float* logits_p = m->b_act[11].get<float>(Bp * 3);
+    float* mlog_p = m->b_act[12].get<float>(Bp * 3);
+    float* tmp = f32 ? m->b_act[13].get<float>(Bp * m->hidden) : nullptr;
+    EmbParams ep{m->table, m->seed_mix, m->J, m->R, m->d_sub, m->action_emb, m->surface_emb, m->pos_emb,
+                 m->cfg.d_emb};
+    CandParams cp{sb.candidate, sb.age, nullptr, m->aux_proj, 0, 0, ft.max_events, ft.fresh_days, ft.mid_days,
+                  0, kh};
+    gather_candidates<T>(sb.in, o, ep, cp, B, E, m->cfg.d_emb, feat, s);
+    m->stats.kernel_launches += 1;
+    Epi e = base_epi(m, EPI_HEAD);
+    e.bias = m->head1.bias;
+    e.w2 = m->hw2;
+    e.b2 = m->hb2;
+    e.logits = logits_p;
+    gemm<T>(m, feat, kh, m->head1, 0, m->hidden, static_cast<int>(B), e, tmp, s);
+    std::vector<float> mb(static_cast<size_t>(Bp) * 3);
+    float hb[3];
+    DCAT_CUDA_CHECK(cudaMemcpy(hb, m->mod_b, sizeof hb, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < Bp; i++)
+        for (int j = 0; j < 3; j++) mb[i * 3 + j] = hb[j];
+    DCAT_CUDA_CHECK(cudaMemcpyAsync(mlog_p, mb.data(), mb.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+    DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+    scatter_outputs(o.perm, B, logits_p, mlog_p, nullptr, 0, logits, mlogits, nullptr, s);
+    m->stats.kernel_launches += 1;
+}
+
+int validate_ft(const dcat_model* m, const dcat_finetune_config* ft, const dcat_batch* b) {
+    // FinetuneConfig::validate (finetune.cpp:54-72) + ColdStartConfig::validate (:41-47)
+    if (ft->variant == DCAT_VARIANT_AUXLT || ft->variant == DCAT_VARIANT_LITE_MEAN ||
+        ft->variant == DCAT_VARIANT_LITE_LAST)
+        return set_err(DCAT_EUNSUPPORTED, "variant not on the device path (Base / Aux / no-sequence only)");
+    if (ft->variant != DCAT_VARIANT_BASE && ft->variant != DCAT_VARIANT_AUX)
+        return set_err(DCAT_EINVAL, "unknown fusion variant");
+    if (!(ft->fresh_days > 0.0 && ft->fresh_days < ft->mid_days))
+        return set_err(DCAT_EINVAL, "age bands must satisfy 0 < fresh_days < mid_days");
+    if (ft->max_events < 0) return set_err(DCAT_EINVAL, "max_events must be >= 0");
+    if (m->cfg.max_len < ft->max_events + 2)
+        return set_err(DCAT_EINVAL, "model.max_len " + std::to_string(m->cfg.max_len) + " too small for max_events " +
+                                        std::to_string(ft->max_events) + " plus candidate tokens");
+    if (!ft->use_seq_module && ft->variant != DCAT_VARIANT_BASE)
+        return set_err(DCAT_EINVAL, "disabling the sequence module requires the base variant");
+    if (ft->use_seq_module && m->d_module != m->cfg.d_model)
+        return set_err(DCAT_EINVAL, "ranking head d_module does not match the sequence module width");
+    if (!ft->use_seq_module && m->d_module != 0)
+        return set_err(DCAT_EINVAL, "ranking head expects module outputs but use_seq_module is off");
+    if (ft->use_seq_module && ft->variant == DCAT_VARIANT_AUX) {
+        if (!b->aux || b->d_aux <= 0) return set_err(DCAT_EINVAL, "variant 'aux' requires an auxiliary embedding");
+        if (b->d_aux != m->d_aux) return set_err(DCAT_EINVAL, "aux dim mismatch in batch");
+    }
+    if (ft->use_seq_module && m->cfg.n_layers < 1)
+        return set_err(DCAT_EINVAL, "context_forward: needs at least one layer");
+    return DCAT_OK;
+}
+
+template <typename F>
+int guarded(dcat_model* m, F&& f) {
+    try {
+        g_err.clear();
+        if (m) DCAT_CUDA_CHECK(cudaSetDevice(m->device));
+        return f();
+    } catch (const CudaError& e) {
+        return set_err(DCAT_ECUDA, e.msg);
+    } catch (const InvalidArg& e) {
+        return set_err(DCAT_EINVAL, e.msg);
+    } catch (const std::bad_alloc&) {
+        return set_err(DCAT_ENOMEM, "host out of memory");
+    }
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+const char* dcat_last_error(void) { return g_err.c_str(); }
+const char* dcat_version(void) { return "dcat_b200 0.1 (sm_100a)"; }
+
+int dcat_model_create(const dcat_model_config* cfg, const dcat_params* params, const dcat_table* table,
+                      const dcat_head* head, int32_t device, dcat_model** out) {
+    if (!cfg || !params || !table || !head || !out) return set_err(DCAT_EINVAL, "null argument");
+    *out = nullptr;
+    std::unique_ptr<dcat_model> m(new dcat_model());
+    return guarded(nullptr, [&]() -> int {
+        const dcat_model_config& c = *cfg;
+        // ModelConfig::validate (model.cpp:175-183)
+        if (!(c.d_model >= 1 && c.n_heads >= 1 && c.d_model % c.n_heads == 0))
+            return set_err(DCAT_EINVAL, "d_model must be divisible by n_heads");
+        if (c.n_layers < 0 || c.mlp_ratio < 1 || c.max_len < 1 || c.d_emb < 1)
+            return set_err(DCAT_EINVAL, "invalid model config");
+        int expect = 3 + (c.pos_learned ? 1 : 0) + 12 + 16 * c.n_layers;
+        if (params->n_tensors != expect)
+            return set_err(DCAT_EINVAL, "params: expected " + std::to_string(expect) + " tensors, got " +
+                                            std::to_string(params->n_tensors));
+        if (table->num_subtables * table->d_sub != c.d_emb)
+            return set_err(DCAT_EINVAL, "segment_inputs: id source dim mismatch");
+        int dh = c.d_model / c.n_heads;
+        if (dh != 16 && dh != 32 && dh != 64)
+            return set_err(DCAT_EUNSUPPORTED, "head dim " + std::to_string(dh) + " not supported (16/32/64)");
+        if (c.d_model % 16 || c.d_emb % 8)
+            return set_err(DCAT_EUNSUPPORTED, "d_model must be a multiple of 16 and d_emb of 8");
+        m->device = device;
+        DCAT_CUDA_CHECK(cudaSetDevice(device));
+        m->cfg = c;
+        const float* const* t = params->tensors;
+        int k = 1;
+        m->action_emb = m->mem.upload(t[k++], static_cast<size_t>(c.n_actions) * c.d_emb);
+        m->surface_emb = m->mem.upload(t[k++], static_cast<size_t>(c.n_surfaces) * c.d_emb);
+        m->pos_emb = c.pos_learned ? m->mem.upload(t[k++], static_cast<size_t>(c.max_len) * c.d_emb) : nullptr;
+        int d = c.d_model, F = d * c.mlp_ratio;
+        m->phi_in1 = make_lin(m->mem, t[k], t[k + 1], c.d_emb, d);
+        m->phi_in2 = make_lin(m->mem, t[k + 2], t[k + 3], d, d);
+        m->phi_out1 = make_lin(m->mem, t[k + 4], t[k + 5], d, d);
+        m->phi_out2 = make_lin(m->mem, t[k + 6], t[k + 7], d, d);
+        k += 12;  // psi is not on the scoring path
+        for (int l = 0; l < c.n_layers; l++) {
+            const float* const* L = t + k + 16 * l;
+            LayerW w;
+            w.ln1_g = m->mem.upload(L[0], d);
+            w.ln1_b = m->mem.upload(L[1], d);
+            w.qkv = make_qkv(m->mem, L[2], L[3], L[4], L[5], L[6], L[7], d);
+            w.o = make_lin(m->mem, L[8], L[9], d, d);
+            w.ln2_g = m->mem.upload(L[10], d);
+            w.ln2_b = m->mem.upload(L[11], d);
+            w.f1 = make_lin(m->mem, L[12], L[13], d, F);
+            w.f2 = make_lin(m->mem, L[14], L[15], F, d);
+            m->layers.push_back(w);
+        }
+        // hashed id table (embed.cpp:16-43)
+        m->J = table->num_subtables;
+        m->R = table->rows;
+        m->d_sub = table->d_sub;
+        std::vector<float> tab(static_cast<size_t>(m->J) * m->R * m->d_sub);
+        for (int j = 0; j < m->J; j++)
+            std::memcpy(tab.data() + static_cast<size_t>(j) * m->R * m->d_sub, table->subtables[j],
+                        sizeof(float) * m->R * m->d_sub);
+        m->table = m->mem.upload(tab.data(), tab.size());
+        std::vector<uint64_t> sm(m->J);
+        for (int j = 0; j < m->J; j++) sm[j] = host_mix64(table->seeds[j]);
+        m->seed_mix = m->mem.upload(sm.data(), sm.size());
+        // ranking head (finetune.hpp:70-85)
+        m->d_module = head->d_module;
+        m->head_demb = head->d_emb;
+        m->n_ctx = head->n_ctx;
+        m->hidden = head->hidden;
+        m->d_aux = head->d_aux;
+        if (head->d_emb != c.d_emb || head->n_ctx != 8)
+            return set_err(DCAT_EINVAL, "ranking head shape does not match the model (d_emb, n_ctx = 8)");
+        if (m->d_module != 0 && m->d_module != d)
+            return set_err(DCAT_EUNSUPPORTED, "ranking head with more than one selector (AuxLt) is not supported");
+        if (m->hidden < 1 || m->hidden > 256) return set_err(DCAT_EUNSUPPORTED, "crossing hidden must be in [1, 256]");
+        m->d_feat = m->d_module + head->d_emb + head->n_ctx;
+        m->kh = (m->d_feat + 63) / 64 * 64;
+        m->head1 = make_lin(m->mem, head->w1, head->b1, m->d_feat, m->hidden, m->kh);
+        m->head1.in = m->kh;  // bf16 operand is zero-padded to kh columns
+        m->hw2 = m->mem.upload(head->w2, static_cast<size_t>(m->hidden) * 3);
+        m->hb2 = m->mem.upload(head->b2, 3);
+        std::vector<float> zero3(3 * std::max(1, m->d_module), 0.0f);
+        m->mod_w = m->d_module ? m->mem.upload(head->mod_w, static_cast<size_t>(m->d_module) * 3) : nullptr;
+        m->mod_b = m->mem.upload(head->mod_b ? head->mod_b : zero3.data(), 3);
+        std::vector<float> za(static_cast<size_t>(std::max(1, m->d_aux)) * c.d_emb, 0.0f);
+        m->aux_proj = m->mem.upload(head->aux_proj && m->d_aux ? head->aux_proj : za.data(), za.size());
+        DCAT_CUDA_CHECK(cudaMalloc(&m->st_dev, sizeof(Status)));
+        m->mem.ptrs.push_back(m->st_dev);
+        DCAT_CUDA_CHECK(cudaMallocHost(&m->st_host, sizeof(Status)));
+        *out = m.release();
+        return DCAT_OK;
+    });
+}
+
+int dcat_model_destroy(dcat_model* m) {
+    if (!m) return DCAT_OK;
+    cudaSetDevice(m->device);
+    cudaDeviceSynchronize();
+    delete m;
+    return DCAT_OK;
+}
+
+int dcat_dedup(dcat_model* m, const dcat_batch* batch, int32_t* rep, int32_t* first, int32_t* b_u, int32_t flags,
+               void* stream) {
+    if (!m || !batch || !rep || !b_u) return set_err(DCAT_EINVAL, "null argument");
+    return guarded(m, [&]() -> int {
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        bool device = flags & DCAT_INPUT_DEVICE;
+        int64_t B = batch->n_rows;
+        *b_u = 0;
+        if (B == 0) return DCAT_OK;
+        Staged sb = stage_batch(m, batch, device, false, s);
+        DedupOut o = dedup_buffers(m, B);
+        run_dedup(m, sb, o, s);
+        const Status& st = *m->st_host;
+        if (st.err_bits & ERR_RANGE) {
+            int code;
+            std::string msg = status_message(m, st, &code);
+            return set_err(code, msg);
+        }
+        *b_u = st.b_u;
+        cudaMemcpyKind k = device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        DCAT_CUDA_CHECK(cudaMemcpyAsync(rep, o.rep, sizeof(int32_t) * B, k, s));
+        if (first) DCAT_CUDA_CHECK(cudaMemcpyAsync(first, o.first, sizeof(int32_t) * st.b_u, k, s));
+        DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+        return DCAT_OK;
+    });
+}
+
+int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_finetune_config* ft, float* logits,
+                            float* module_logits, float* h_cand, int32_t flags, void* stream) {
+    if (!m || !batch || !ft || !logits || !module_logits) return set_err(DCAT_EINVAL, "null argument");
+    return guarded(m, [&]() -> int {
+        int rc = validate_ft(m, ft, batch);
+        if (rc) return rc;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        bool device = flags & DCAT_INPUT_DEVICE;
+        bool f32 = flags & DCAT_PRECISION_FP32;
+        m->profiling = flags & DCAT_PROFILE;
+        m->ev_next = 0;
+        m->ev_marks.clear();
+        m->stage_ms.clear();
+        std::memset(&m->stats, 0, sizeof m->stats);
+        int64_t B = batch->n_rows;
+        if (B == 0) return DCAT_OK;
+        int t0 = mark(m, s);
+        Staged sb = stage_batch(m, batch, device, ft->variant == DCAT_VARIANT_AUX, s);
+        DedupOut o = dedup_buffers(m, B);
+        int t1 = mark(m, s);
+        run_dedup(m, sb, o, s);
+        int t2 = mark(m, s);
+        Status st = *m->st_host;
+        if (!ft->use_seq_module) st.err_bits &= ~(ERR_ACTION | ERR_SURFACE | ERR_POS_CTX | ERR_POS_CAND);
+        if (st.err_bits) {
+            int code;
+            std::string msg = status_message(m, st, &code);
+            return set_err(code, msg);
+        }
+        m->stats.b_u = st.b_u;
+        m->stats.ctx_tokens = st.ctx_tokens;
+        m->last_bu = st.b_u;
+        m->last_T = st.ctx_tokens;
+        m->last_precision_f32 = f32;
+        float *dl = logits, *dm = module_logits, *dh = h_cand;
+        if (!device) {
+            dl = m->b_out[0].get<float>(B * 3);
+            dm = m->b_out[1].get<float>(B * 3);
+            dh = h_cand ? m->b_out[2].get<float>(B * m->cfg.d_model) : nullptr;
+        }
+        if (ft->use_seq_module) {
+            if (f32) run_dcat<float>(m, sb, o, *ft, dl, dm, dh, s);
+            else run_dcat<bf16>(m, sb, o, *ft, dl, dm, dh, s);
+        } else {
+            if (f32) run_head_only<float>(m, sb, o, *ft, dl, dm, s);
+            else run_head_only<bf16>(m, sb, o, *ft, dl, dm, s);
+        }
+        int t3 = mark(m, s);
+        if (!device) {
+            DCAT_CUDA_CHECK(cudaMemcpyAsync(logits, dl, sizeof(float) * B * 3, cudaMemcpyDeviceToHost, s));
+            DCAT_CUDA_CHECK(cudaMemcpyAsync(module_logits, dm, sizeof(float) * B * 3, cudaMemcpyDeviceToHost, s));
+            if (h_cand)
+                DCAT_CUDA_CHECK(cudaMemcpyAsync(h_cand, dh, sizeof(float) * B * m->cfg.d_model, cudaMemcpyDeviceToHost,
+                                                s));
+        }
+        DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
+        int t4 = mark(m, s);
+        DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (m->profiling) {
+            span(m, "h2d", t0, t1);
+            span(m, "dedup", t1, t2);
+            span(m, "device_total", t1, t3);
+            span(m, "d2h", t3, t4);
+            for (auto& mk : m->ev_marks) {
+                float ms = 0.f;
+                DCAT_CUDA_CHECK(cudaEventElapsedTime(&ms, m->ev_pool[mk.second.first], m->ev_pool[mk.second.second]));
+                m->stage_ms.push_back({mk.first, ms});
+            }
+        }
+        Status fin = *m->st_host;
+        if (fin.err_bits & ERR_AGE) return set_err(DCAT_EINVAL, "candidate age must be non-negative");
+        if (fin.nonfinite_layer > 0)
+            return set_err(DCAT_ENONFINITE, "non-finite activation in layer " + std::to_string(fin.nonfinite_layer - 1));
+        if (ft->use_seq_module) {
+            // keep the context token offsets for dcat_debug_kv
+            m->last_tok_off.resize(static_cast<size_t>(st.b_u) + 1);
+            DCAT_CUDA_CHECK(cudaMemcpy(m->last_tok_off.data(), o.tok_off, sizeof(int64_t) * (st.b_u + 1),
+                                       cudaMemcpyDeviceToHost));
+        }
+        return DCAT_OK;
+    });
+}
+
+int dcat_debug_kv(dcat_model* m, int32_t layer, int32_t unique, float* k, float* v, int32_t* n) {
+    if (!m || !n) return set_err(DCAT_EINVAL, "null argument");
+    return guarded(m, [&]() -> int {
+        if (unique < 0 || unique >= m->last_bu || layer < 0 || layer >= m->cfg.n_layers ||
+            m->last_tok_off.size() < static_cast<size_t>(unique) + 2)
+            return set_err(DCAT_EINVAL, "no such unique / layer in the last call");
+        int64_t a = m->last_tok_off[unique], b = m->last_tok_off[unique + 1];
+        *n = static_cast<int32_t>(b - a);
+        int d = m->cfg.d_model;
+        size_t cnt = static_cast<size_t>(b - a) * d;
+        for (int which = 0; which < 2; which++) {
+            float* dst = which ? v : k;
+            if (!dst) continue;
+            size_t base = (static_cast<size_t>(2 * layer + which) * m->last_Tp + a) * d;
+            if (m->last_precision_f32) {
+                DCAT_CUDA_CHECK(cudaMemcpy(dst, static_cast<float*>(m->last_kv) + base, cnt * 4, cudaMemcpyDeviceToHost));
+            } else {
+                std::vector<bf16> tmp(cnt);
+                DCAT_CUDA_CHECK(cudaMemcpy(tmp.data(), static_cast<bf16*>(m->last_kv) + base, cnt * 2,
+                                           cudaMemcpyDeviceToHost));
+                for (size_t i = 0; i < cnt; i++) dst[i] = __bfloat162float(tmp[i]);
+            }
+        }
+        return DCAT_OK;
+    });
+}
+
+int dcat_stage_times(dcat_model* m, const char** names, float* ms, int32_t cap) {
+    if (!m) return 0;
+    int n = 0;
+    for (auto& p : m->stage_ms) {
+        if (n >= cap) break;
+        if (names) names[n] = p.first;
+        if (ms) ms[n] = p.second;
+        n++;
+    }
+    return n;
+}
+
+int dcat_last_stats(dcat_model* m, dcat_call_stats* out) {
+    if (!m || !out) return set_err(DCAT_EINVAL, "null argument");
+    *out = m->stats;
+    return DCAT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,196 @@
+// gather.cu — K2: embedding gathers for the context and crossing passes.
+//
+// Context token rows (segment_inputs, model.cpp:517-540):
+//   E[t] = concat_j sub_j[hash_id(item, seed_j, R)] + action_emb[a]
+//          + surface_emb[s] + pos_emb[i]
+// with hash_id = mix64(id ^ mix64(seed)) % R (embed.cpp:11-14, lookup
+// embed.cpp:38-43). Candidate rows (candidate_inputs, dcat.cpp:180-197, plus
+// the Aux term of finetune.cpp:469-479):
+//   E[b] = lookup(item_b) + pos_emb[n_u] (+ sum_r aux[r] * aux_proj[r])
+// and the ranking-head feature block [cand_emb | ctx_features]
+// (crossing_forward finetune.cpp:303-308, ctx_features :212-226).
+// One warp per row, 128-bit loads of the fp32 table rows (4 MB at PinFM-base,
+// L2-resident), additions in the reference's order, output bf16 (or fp32 in
+// the parity path).
+#include "launch.h"
+
+namespace dcat {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ void store4(T* dst, float4 v);
+template <>
+__device__ __forceinline__ void store4<float>(float* dst, float4 v) {
+    *reinterpret_cast<float4*>(dst) = v;
+}
+template <>
+__device__ __forceinline__ void store4<bf16>(bf16* dst, float4 v) {
+    uint2 p;
+    p.x = pack_bf16(v.x, v.y);
+    p.y = pack_bf16(v.z, v.w);
+    *reinterpret_cast<uint2*>(dst) = p;
+}
+
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+    return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+
+__device__ __forceinline__ float4 lookup4(const EmbParams& ep, uint64_t item, int c) {
+    int j = c / ep.d_sub;
+    int cc = c - j * ep.d_sub;
+    uint32_t r = static_cast<uint32_t>(mix64(item ^ ep.seed_mix[j]) % static_cast<uint64_t>(ep.R));
+    return __ldg(reinterpret_cast<const float4*>(ep.table + (static_cast<size_t>(j) * ep.R + r) * ep.d_sub + cc));
+}
+
+__device__ __forceinline__ float lookup1(const EmbParams& ep, uint64_t item, int c) {
+    int j = c / ep.d_sub;
+    int cc = c - j * ep.d_sub;
+    uint32_t r = static_cast<uint32_t>(mix64(item ^ ep.seed_mix[j]) % static_cast<uint64_t>(ep.R));
+    return __ldg(ep.table + (static_cast<size_t>(j) * ep.R + r) * ep.d_sub + cc);
+}
+
+template <typename T, bool VEC>
+__global__ void k_gather_ctx(DedupIn in, const int32_t* __restrict__ first, const int64_t* __restrict__ tok_off,
+                             EmbParams ep, const int32_t* __restrict__ tok_unique, int64_t T_ctx, T* __restrict__ E,
+                             int ldE) {
+    int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (t >= T_ctx) return;
+    int u = tok_unique[t];
+    int i = static_cast<int>(t - tok_off[u]);
+    int64_t ev = in.row_offset[first[u]] + i;
+    uint64_t item = in.item[ev];
+    int a = in.action[ev], s = in.surface[ev];
+    const float* ae = ep.action_emb + static_cast<size_t>(a) * ep.d_emb;
+    const float* se = ep.surface_emb + static_cast<size_t>(s) * ep.d_emb;
+    const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(i) * ep.d_emb : nullptr;
+    T* out = E + t * ldE;
+    if constexpr (VEC) {
+        for (int c = lane * 4; c < ep.d_emb; c += 128) {
+            float4 v = lookup4(ep, item, c);
+            v = add4(v, __ldg(reinterpret_cast<const float4*>(ae + c)));
+            v = add4(v, __ldg(reinterpret_cast<const float4*>(se + c)));
+            if (pe) v = add4(v, __ldg(reinterpret_cast<const float4*>(pe + c)));
+            store4<T>(out + c, v);
+        }
+    } else {
+        for (int c = lane; c < ep.d_emb; c += 32) {
+            float v = lookup1(ep, item, c);
+            v = v + ae[c];
+            v = v + se[c];
+            if (pe) v = v + pe[c];
+            ActIO<T>::store(out + c, v);
+        }
+    }
+}
+
+// ctx_features (finetune.cpp:212-226)
+__device__ float ctx_feature(int k, double age, int valid, int last_surface, int max_events, double fresh,
+                             double mid) {
+    double days = age / 86400.0;
+    int band = days < fresh ? 0 : days < mid ? 1 : 2;
+    if (k < 3) return k == band ? 1.0f : 0.0f;
+    if (k == 3) {
+        if (max_events <= 0) return 0.0f;
+        float r = static_cast<float>(valid) / static_cast<float>(max_events);
+        return r < 1.0f ? r : 1.0f;
+    }
+    return (valid > 0 && k - 4 == last_surface) ? 1.0f : 0.0f;
+}
+
+template <typename T>
+__global__ void k_gather_cand(DedupIn in, const int32_t* __restrict__ perm, const int32_t* __restrict__ rep,
+                              const int32_t* __restrict__ first, EmbParams ep, CandParams cp, int64_t B,
+                              T* __restrict__ E, int ldE, T* __restrict__ feat, Status* st) {
+    int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (p >= B) return;
+    int i = perm[p];
+    int n = in.row_valid[first[rep[i]]];
+    uint64_t item = cp.candidate[i];
+    const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(n) * ep.d_emb : nullptr;
+    const float* aux = cp.variant_aux ? cp.aux + static_cast<size_t>(i) * cp.d_aux : nullptr;
+    T* out = E + p * ldE;
+    T* fo = feat ? feat + p * cp.feat_ld : nullptr;
+    bool vec = (ep.d_sub % 4) == 0 && (ep.d_emb % 4) == 0;
+    if (vec) {
+        for (int c = lane * 4; c < ep.d_emb; c += 128) {
+            float4 raw = lookup4(ep, item, c);
+            if (fo) store4<T>(fo + cp.d_model + c, raw);
+            float4 v = raw;
+            if (pe) v = add4(v, __ldg(reinterpret_cast<const float4*>(pe + c)));
+            if (aux) {
+                for (int r = 0; r < cp.d_aux; r++) {
+                    float al = aux[r];
+                    float4 pr = __ldg(reinterpret_cast<const float4*>(cp.aux_proj + static_cast<size_t>(r) * ep.d_emb + c));
+                    v.x = __fadd_rn(v.x, __fmul_rn(al, pr.x));
+                    v.y = __fadd_rn(v.y, __fmul_rn(al, pr.y));
+                    v.z = __fadd_rn(v.z, __fmul_rn(al, pr.z));
+                    v.w = __fadd_rn(v.w, __fmul_rn(al, pr.w));
+                }
+            }
+            store4<T>(out + c, v);
+        }
+    } else {
+        for (int c = lane; c < ep.d_emb; c += 32) {
+            float raw = lookup1(ep, item, c);
+            if (fo) ActIO<T>::store(fo + cp.d_model + c, raw);
+            float v = raw;
+            if (pe) v = v + pe[c];
+            if (aux)
+                for (int r = 0; r < cp.d_aux; r++)
+                    v = __fadd_rn(v, __fmul_rn(aux[r], cp.aux_proj[static_cast<size_t>(r) * ep.d_emb + c]));
+            ActIO<T>::store(out + c, v);
+        }
+    }
+    if (fo) {
+        double age = cp.age[i];
+        if (lane == 0 && age < 0.0) {
+            atomicOr(&st->err_bits, ERR_AGE);
+            atomicMin(&st->err_row, i);
+        }
+        int valid = in.row_valid[i];
+        int last_s = valid > 0 ? in.surface[in.row_offset[i] + valid - 1] : -1;
+        int c0 = cp.d_model + ep.d_emb;
+        for (int c = c0 + lane; c < cp.feat_ld; c += 32) {
+            int k = c - c0;
+            float f = k < 8 ? ctx_feature(k, age, valid, last_s, cp.max_events, cp.fresh_days, cp.mid_days) : 0.0f;
+            ActIO<T>::store(fo + c, f);
+        }
+    }
+}
+
+}  // namespace
+
+template <typename T>
+void gather_context(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const int32_t* tok_unique,
+                    int64_t T_ctx, T* E, int ldE, cudaStream_t s) {
+    if (T_ctx <= 0) return;
+    unsigned g = static_cast<unsigned>((T_ctx * 32 + 255) / 256);
+    if ((ep.d_sub % 4) == 0 && (ep.d_emb % 4) == 0 && (ldE % 4) == 0)
+        k_gather_ctx<T, true><<<g, 256, 0, s>>>(in, o.first, o.tok_off, ep, tok_unique, T_ctx, E, ldE);
+    else
+        k_gather_ctx<T, false><<<g, 256, 0, s>>>(in, o.first, o.tok_off, ep, tok_unique, T_ctx, E, ldE);
+    DCAT_LAUNCH_CHECK();
+}
+
+template <typename T>
+void gather_candidates(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const CandParams& cp, int64_t B,
+                       T* E, int ldE, T* feat, cudaStream_t s) {
+    if (B <= 0) return;
+    unsigned g = static_cast<unsigned>((B * 32 + 255) / 256);
+    k_gather_cand<T><<<g, 256, 0, s>>>(in, o.perm, o.rep, o.first, ep, cp, B, E, ldE, feat, o.st);
+    DCAT_LAUNCH_CHECK();
+}
+
+template void gather_context<float>(const DedupIn&, const DedupOut&, const EmbParams&, const int32_t*, int64_t,
+                                    float*, int, cudaStream_t);
+template void gather_context<bf16>(const DedupIn&, const DedupOut&, const EmbParams&, const int32_t*, int64_t, bf16*,
+                                   int, cudaStream_t);
+template void gather_candidates<float>(const DedupIn&, const DedupOut&, const EmbParams&, const CandParams&, int64_t,
+                                       float*, int, float*, cudaStream_t);
+template void gather_candidates<bf16>(const DedupIn&, const DedupOut&, const EmbParams&, const CandParams&, int64_t,
+                                      bf16*, int, bf16*, cudaStream_t);
+
+}  // namespace dcat

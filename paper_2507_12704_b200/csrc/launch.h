@@ -1,0 +1,162 @@
+// launch.h — host-side launchers of the DCAT B200 kernels.
+//
+// Every kernel file exposes plain host functions taking device pointers and a
+// stream; dcat_api.cu orchestrates them into rank_forward_batch.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace dcat {
+
+// ---------------------------------------------------------------- dedup.cu
+struct DedupIn {
+    int64_t B;
+    const int64_t* row_offset;
+    const int32_t* row_valid;
+    int64_t n_events;
+    const uint64_t* ts;
+    const uint8_t* action;
+    const uint8_t* surface;
+    const uint64_t* item;
+    int n_actions, n_surfaces, max_len, pos_learned;
+};
+
+struct Tile {  // one attention work item: <= BM query rows of one unique
+    int q0, nq;     // first query row, number of query rows
+    int kv0, nkv;   // first context K/V row, number of keys visible to the tile
+    int qloc;       // causal: local position of the first query within its unique
+    int u;          // unique id
+    int pad0, pad1;
+};
+
+struct DedupOut {  // device buffers, sized for B rows
+    uint64_t* hash;
+    uint64_t* tab_key;
+    int32_t* tab_val;
+    int64_t tab_cap;
+    int32_t* slot;
+    int32_t* head;
+    int32_t* collided;
+    int32_t* list;       // compacted row list for the collision rounds
+    int32_t* list_n;     // device counter
+    int64_t* scan_tmp;   // B + 1
+    int64_t* scan_blk;   // block sums
+    int64_t* uid;        // B + 1 (exclusive scan of first flags)
+    int32_t* rep;        // B
+    int32_t* first;      // B (b_u used)
+    int32_t* cnt;        // B: candidates per unique
+    int32_t* cursor;     // B
+    int64_t* goff;       // B + 1: candidate group offsets
+    int32_t* perm;       // B: permuted position -> original row
+    int64_t* tok_off;    // B + 1: context token offsets per unique
+    int64_t* ctx_toff;   // B + 1: context tile offsets
+    int64_t* cross_toff; // B + 1: cross tile offsets
+    Status* st;
+};
+
+// Stage 1: hash / verify / first-appearance ids / groups / token offsets.
+// Leaves counts in st (host reads after a sync).
+void dedup_plan(const DedupIn& in, const DedupOut& o, uint64_t hash_mask, int tile_m_ctx, int tile_m_cross,
+                cudaStream_t s);
+// Collision repair rounds (only when st->collisions > 0): returns when fixed.
+void dedup_repair(const DedupIn& in, const DedupOut& o, int n_collided, int tile_m_ctx, int tile_m_cross,
+                  uint64_t hash_mask, cudaStream_t s);
+// Stage 2 (after the host knows b_u / tile counts): tile lists + token map.
+void build_tiles(const DedupIn& in, const DedupOut& o, int b_u, int tile_m_ctx, int tile_m_cross, Tile* ctx_tiles,
+                 Tile* cross_tiles, int32_t* tok_unique, cudaStream_t s);
+// Exclusive scan of n int64 values; out[n] = total; optionally copies total to *total_dst.
+void scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* blk, cudaStream_t s);
+
+// ---------------------------------------------------------------- gather.cu
+struct EmbParams {
+    const float* table;       // J x R x d_sub
+    const uint64_t* seed_mix; // J: mix64(seed_j)
+    int J, R, d_sub;
+    const float* action_emb;  // n_actions x d_emb
+    const float* surface_emb; // n_surfaces x d_emb
+    const float* pos_emb;     // max_len x d_emb or null
+    int d_emb;
+};
+template <typename T>
+void gather_context(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const int32_t* tok_unique,
+                    int64_t T_ctx, T* E, int ldE, cudaStream_t s);
+struct CandParams {
+    const uint64_t* candidate;
+    const double* age;
+    const float* aux;       // B x d_aux or null
+    const float* aux_proj;  // d_aux x d_emb
+    int d_aux;
+    int variant_aux;
+    int max_events;
+    double fresh_days, mid_days;
+    int d_model;            // feat column offset of cand_emb
+    int feat_ld;            // feat leading dimension (0 = no feat)
+};
+template <typename T>
+void gather_candidates(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const CandParams& cp, int64_t B,
+                       T* E, int ldE, T* feat, cudaStream_t s);
+
+// ---------------------------------------------------------------- gemm
+enum EpiMode : int {
+    EPI_BIAS = 0,       // out = act(acc + bias), split across up to 3 column segments
+    EPI_RESID_LN = 1,   // x = acc + bias + resid; x_out fp32; ln_out = LN(x) (or copy of x)
+    EPI_L2NORM = 2,     // y = l2norm(acc + bias); x_out fp32; ln_out = LN(y) or copy; mlogits
+    EPI_HEAD = 3,       // z = gelu(acc + bias); logits = z . w2 + b2
+};
+
+struct Epi {
+    int mode;
+    int act;                 // EPI_BIAS: 0 none, 1 gelu
+    const float* bias;       // [N]
+    void* out[3];            // EPI_BIAS: activation outputs per segment
+    int out_ld[3];
+    int seg_cols;            // columns per output segment
+    const float* resid;      // EPI_RESID_LN: fp32 residual [M x ld_x]
+    float* x_out;            // fp32 [M x ld_x]
+    int ld_x;
+    const float* ln_g;       // LN gain (null: ln_out = plain copy)
+    const float* ln_b;
+    void* ln_out;            // activation type
+    int ln_ld;
+    void* out2;              // EPI_L2NORM: second activation copy (feat), may be null
+    int out2_ld;
+    const float* mod_w;      // EPI_L2NORM: N x 3 module head (null = none)
+    const float* mod_b;
+    float* mlogits;          // [M x 3]
+    const float* w2;         // EPI_HEAD: hidden x 3
+    const float* b2;
+    float* logits;           // [M x 3]
+    Status* st;
+    int layer_idx;           // for non-finite reporting (-1: no check)
+};
+
+// bf16 tensor-core GEMM (tcgen05 + TMEM + TMA): C[M x N] = A[M x K] . W^T,
+// A bf16 row-major (lda), W bf16 [N x K] row-major, fused epilogue.
+void gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K, const Epi& e, cudaStream_t s);
+// fp32 parity path: SIMT GEMM (W in reference in x out layout, ldw) + row epilogue.
+void gemm_f32(const float* A, int lda, const float* W, int ldw, int M, int N, int K, const Epi& e, float* tmp,
+              cudaStream_t s);
+
+// ---------------------------------------------------------------- attention.cu
+struct AttnArgs {
+    const void* q; int ldq;        // query rows (head h at cols h*dh)
+    const void* k; const void* v; int ldkv;  // context K/V (cache)
+    const void* kself; const void* vself; int ldself;  // crossing: per-row own key/value
+    void* out; int ldo;
+    const Tile* tiles; int n_tiles;
+    int n_heads, dh;
+    float scale;
+    int causal;                     // 1: context pass, 0: crossing (with self term)
+    int max_keys;                   // fp32 path: upper bound on keys per query
+};
+void attention_bf16(const AttnArgs& a, cudaStream_t s);
+void attention_f32(const AttnArgs& a, cudaStream_t s);
+
+// ---------------------------------------------------------------- head / scatter
+void scatter_outputs(const int32_t* perm, int64_t B, const float* logits_p, const float* mlog_p, const float* h_p,
+                     int d, float* logits, float* mlogits, float* h_cand, cudaStream_t s);
+
+}  // namespace dcat

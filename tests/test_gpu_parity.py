@@ -1,0 +1,238 @@
+"""Parity of the B200 path (C ABI) against the CPU oracle and the reference goldens.
+
+Tolerances (written next to each check):
+  * dedup plans: bit-exact (integer work).
+  * fp32 parity mode (DCAT_PRECISION_FP32): the reference's own DCAT-vs-naive
+    bound, max-abs 1e-4 on unit-norm H (test_dcat.cpp:227), rel 1e-4 on logits
+    (test_finetune.cpp:359-361).
+  * bf16 production mode (bf16 storage, fp32 accumulate): max-abs 3e-2 on H
+    (unit-norm rows), logits within 3e-2 of the logit scale, cosine(H) >= 0.999.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import golden_util as G
+from oracle import pyoracle
+from paper_2507_12704_b200.abi import FinetuneSpec, ModelSpec
+from paper_2507_12704_b200.synth import make_batch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return pyoracle.oracle()
+
+
+@pytest.fixture(scope="module")
+def api():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2507_12704_b200 import api as a
+    return a
+
+
+def rel_err(got, ref):
+    scale = max(1e-3, float(np.abs(ref).max()))
+    return float(np.abs(np.asarray(got, np.float64) - ref).max()) / scale
+
+
+def cos_min(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    num = (a * b).sum(1)
+    den = np.linalg.norm(a, axis=1) * np.linalg.norm(b, axis=1) + 1e-30
+    return float((num / den).min())
+
+
+# ------------------------------------------------------------------ dedup (K1)
+
+def test_dedup_golden_bit_exact(api, orc):
+    z = G.load("dedup")
+    w = orc.init_weights(ModelSpec(16, 1, 2, 2, 40, 16), 1, table=(4, 64, 4, 3, 0.05))
+    m = api.DcatModel(w)
+    for n in G.names(z):
+        b = G.batch_from(z, n + ".")
+        rep, first, b_u = m.dedup_segments(b)
+        assert b_u == int(z[n + ".b_u"][0]), n
+        np.testing.assert_array_equal(rep, z[n + ".rep"], err_msg=n)
+        np.testing.assert_array_equal(first, z[n + ".first"], err_msg=n)
+
+
+@pytest.mark.parametrize("layout,shared", [("interleaved", False), ("grouped", True), ("interleaved", True)])
+def test_dedup_large_vs_oracle(api, orc, layout, shared):
+    w = orc.init_weights(ModelSpec(16, 1, 2, 2, 300, 16), 1, table=(4, 64, 4, 3, 0.05))
+    m = api.DcatModel(w)
+    b = make_batch(3000, 9, 40, seed=5, layout=layout, shared_storage=shared, ragged=True, empty_users=4)
+    rep, first, b_u = m.dedup_segments(b)
+    rr, rf, rb = orc.dedup(b)
+    assert b_u == rb
+    np.testing.assert_array_equal(rep, rr)
+    np.testing.assert_array_equal(first, rf)
+
+
+def test_dedup_forced_hash_collisions(api, orc, monkeypatch):
+    """A 3-bit content hash makes almost every row collide: the verify / re-key /
+    exact-pass repair must still give the reference plan bit-exactly."""
+    w = orc.init_weights(ModelSpec(16, 1, 2, 2, 40, 16), 1, table=(4, 64, 4, 3, 0.05))
+    m = api.DcatModel(w)
+    b = make_batch(200, 5, 12, seed=9, ragged=True, shared_storage=False)
+    monkeypatch.setenv("DCAT_DEBUG_HASH_BITS", "3")
+    rep, first, b_u = m.dedup_segments(b)
+    monkeypatch.delenv("DCAT_DEBUG_HASH_BITS")
+    rr, rf, rb = orc.dedup(b)
+    assert b_u == rb
+    np.testing.assert_array_equal(rep, rr)
+    np.testing.assert_array_equal(first, rf)
+
+
+# ------------------------------------------------------------------ fp32 parity mode
+
+def test_fp32_cross_goldens(api, orc):
+    """cross vs naive sweep of test_dcat.cpp:215-229 plus the empty prefix case."""
+    z = G.load("cross")
+    for n in G.names(z):
+        spec, w = G.weights_from(z, orc, n + ".")
+        b = G.batch_from(z, n + ".")
+        m = api.DcatModel(w)
+        ft = FinetuneSpec(max_events=spec.max_len - 2)
+        _, _, h = m.rank_forward_batch(b, ft, precision="fp32", want_h=True)
+        err = float(np.abs(h - z[n + ".dcat"]).max())
+        assert err <= 1e-4, (n, err)  # test_dcat.cpp:227
+        assert float(np.abs(h - z[n + ".naive"]).max()) <= 1e-4, n
+
+
+def test_fp32_context_kv(api, orc):
+    z = G.load("kv")
+    spec, w = G.weights_from(z, orc)
+    b = G.batch_from(z)
+    m = api.DcatModel(w)
+    m.rank_forward_batch(b, FinetuneSpec(max_events=spec.max_len - 2), precision="fp32")
+    for u in range(2):
+        for l in range(2):
+            k, v = m.debug_kv(l, u, 64)
+            assert np.abs(k - z[f"k.{u}.{l}"]).max() <= 1e-5
+            assert np.abs(v - z[f"v.{u}.{l}"]).max() <= 1e-5
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_rank_goldens(api, orc, precision):
+    z = G.load("rank")
+    for n in G.names(z):
+        spec, w = G.weights_from(z, orc, n + ".")
+        G.apply_overrides(z, w, n + ".")
+        b = G.batch_from(z, n + ".")
+        ft = G.ft_from(z, n + ".")
+        m = api.DcatModel(w)
+        logits, mlog, h = m.rank_forward_batch(b, ft, precision=precision, want_h=ft.use_seq_module)
+        if precision == "fp32":
+            tol = 1e-4  # test_finetune.cpp:359-361
+            assert rel_err(logits, z[n + ".logits"]) <= tol, n
+            assert rel_err(mlog, z[n + ".module_logits"]) <= tol, n
+            if (n + ".h_cand") in z.files:
+                assert float(np.abs(h - z[n + ".h_cand"]).max()) <= 1e-4, n
+        else:
+            assert rel_err(logits, z[n + ".logits"]) <= 3e-2, (n, rel_err(logits, z[n + ".logits"]))
+            assert rel_err(mlog, z[n + ".module_logits"]) <= 3e-2, n
+            if (n + ".h_cand") in z.files:
+                assert float(np.abs(h - z[n + ".h_cand"]).max()) <= 3e-2, n
+                assert cos_min(h, z[n + ".h_cand"]) >= 0.999, n
+
+
+# ------------------------------------------------------------------ bf16 at BASELINE dims
+
+def _base_setup(orc, U, C, L, **kw):
+    spec = ModelSpec(d_model=256, n_layers=4, n_heads=8, mlp_ratio=4, max_len=L + 2, d_emb=256)
+    w = orc.init_weights(spec, 42, table=(8, 4096, 32, 7, 0.05), head_seed=11)
+    b = make_batch(U, C, L, **kw)
+    return spec, w, b
+
+
+def test_bf16_pinfm_base_sample_vs_oracle(api, orc):
+    spec, w, b = _base_setup(orc, 3, 16, 256, seed=4, ragged=True, layout="grouped")
+    ft = FinetuneSpec(max_events=256)
+    m = api.DcatModel(w)
+    logits, mlog, h = m.rank_forward_batch(b, ft, want_h=True)
+    rl, rm, _, rh = orc.rank_forward_batch(w, ft, b)
+    assert float(np.abs(h - rh).max()) <= 3e-2
+    assert cos_min(h, rh) >= 0.999
+    assert rel_err(logits, rl) <= 3e-2
+    assert rel_err(mlog, rm) <= 3e-2
+    lf, mf, hf = m.rank_forward_batch(b, ft, precision="fp32", want_h=True)
+    assert float(np.abs(hf - rh).max()) <= 1e-4
+    assert rel_err(lf, rl) <= 1e-4
+
+
+def test_bf16_full_size_properties(api, orc):
+    """PinFM-base at full size (1000 users x 128): properties that hold at any
+    size — batch permutation invariance and bit-identical duplicate rows
+    (test_dcat.cpp:243-276) — plus oracle parity on a user sample."""
+    spec, w, b = _base_setup(orc, 1000, 128, 256, seed=1)
+    ft = FinetuneSpec(max_events=256)
+    m = api.DcatModel(w)
+    logits, mlog, _ = m.rank_forward_batch(b, ft)
+    assert np.isfinite(logits).all()
+    rng = np.random.default_rng(0)
+    perm = rng.permutation(b.n_rows)
+    lp, mp, _ = m.rank_forward_batch(b.take(perm), ft)
+    np.testing.assert_array_equal(lp, logits[perm])
+    np.testing.assert_array_equal(mp, mlog[perm])
+    # duplicate (sequence, candidate) rows -> identical outputs
+    b2 = b.take(np.arange(b.n_rows))
+    b2.candidate[1000] = b2.candidate[0]  # rows 0 and 1000 share unique 0 (interleaved)
+    l2, _, _ = m.rank_forward_batch(b2, ft)
+    np.testing.assert_array_equal(l2[0], l2[1000])
+    # oracle parity on 3 users with all their candidates
+    rows = np.nonzero(np.isin(np.arange(b.n_rows) % 1000, [0, 511, 999]))[0]
+    sub = b.take(rows)
+    rl, rm, _, _ = orc.rank_forward_batch(w, ft, sub)
+    assert rel_err(logits[rows], rl) <= 3e-2
+    assert rel_err(mlog[rows], rm) <= 3e-2
+
+
+def test_device_resident_io_matches_host(api, orc):
+    import torch
+    spec, w, b = _base_setup(orc, 20, 8, 64, seed=2, ragged=True)
+    ft = FinetuneSpec(max_events=64)
+    m = api.DcatModel(w)
+    lh, mh, hh = m.rank_forward_batch(b, ft, want_h=True)
+    bd = b.to(lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64) if a.dtype == np.uint64 else a).cuda())
+    ld, md, hd = m.rank_forward_batch(bd, ft, want_h=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(ld.cpu().numpy(), lh)
+    np.testing.assert_array_equal(md.cpu().numpy(), mh)
+    np.testing.assert_array_equal(hd.cpu().numpy(), hh)
+
+
+# ------------------------------------------------------------------ errors (reference SEQFM_CHECKs)
+
+def test_errors(api, orc):
+    spec = ModelSpec(d_model=64, n_layers=2, n_heads=4, mlp_ratio=4, max_len=20, d_emb=64)
+    w = orc.init_weights(spec, 3, table=(8, 128, 8, 7, 0.05))
+    m = api.DcatModel(w)
+    ft = FinetuneSpec(max_events=16)
+    b = make_batch(4, 3, 16, seed=1)
+    m.rank_forward_batch(b, ft)
+    bad = make_batch(4, 3, 16, seed=1)
+    bad.ev_action[5] = 9
+    with pytest.raises(RuntimeError, match="unknown action"):
+        m.rank_forward_batch(bad, ft)
+    bad = make_batch(4, 3, 16, seed=1)
+    bad.ev_surface[3] = 4
+    with pytest.raises(RuntimeError, match="unknown surface"):
+        m.rank_forward_batch(bad, ft)
+    long = make_batch(2, 2, 20, seed=1)  # valid 20 == max_len: the candidate position is out of range
+    with pytest.raises(RuntimeError, match="position"):
+        m.rank_forward_batch(long, ft)
+    neg = make_batch(4, 3, 16, seed=1)
+    neg.age_seconds[2] = -5.0
+    with pytest.raises(RuntimeError, match="non-negative"):
+        m.rank_forward_batch(neg, ft)
+    with pytest.raises(RuntimeError, match="auxiliary"):
+        m.rank_forward_batch(b, FinetuneSpec(variant="aux", max_events=16))
+    with pytest.raises(RuntimeError, match="variant"):
+        m.rank_forward_batch(b, FinetuneSpec(variant="aux-lt", max_events=16))
+    with pytest.raises(RuntimeError, match="max_len"):
+        m.rank_forward_batch(b, FinetuneSpec(max_events=19))
