@@ -266,29 +266,32 @@ __global__ void __launch_bounds__(128) k_flash(AttnArgs p) {
     }
 }
 
-// ---- fp32 parity kernel: one warp per (query row, head), reference loop order
-__global__ void k_attn_f32(AttnArgs p, int max_keys) {
+// ---- SIMT kernel: one warp per (query row, head), the reference's exact loop
+// order (logits, max, exp-sum, axpy over keys in order). fp32 parity path for
+// every head dim, and the bf16 path for head dims below the mma k-step (< 16).
+template <typename T>
+__global__ void k_attn_simt(AttnArgs p, int max_keys) {
     extern __shared__ float logits_all[];
     const Tile tile = p.tiles[blockIdx.x];
     const int h = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     float* logits = logits_all + warp * (max_keys + 1);
-    const float* Q = static_cast<const float*>(p.q);
-    const float* K = static_cast<const float*>(p.k);
-    const float* V = static_cast<const float*>(p.v);
+    const T* Q = static_cast<const T*>(p.q);
+    const T* K = static_cast<const T*>(p.k);
+    const T* V = static_cast<const T*>(p.v);
     const int dh = p.dh, hc = h * dh;
     for (int r = warp; r < tile.nq; r += nw) {
-        const float* q = Q + static_cast<size_t>(tile.q0 + r) * p.ldq + hc;
+        const T* q = Q + static_cast<size_t>(tile.q0 + r) * p.ldq + hc;
         int nkeys = p.causal ? tile.qloc + r + 1 : tile.nkv + 1;  // crossing: context + self (last)
         float mx = -INFINITY;
         for (int j = 0; j < nkeys; j++) {
-            const float* kr;
+            const T* kr;
             if (!p.causal && j == tile.nkv)
-                kr = static_cast<const float*>(p.kself) + static_cast<size_t>(tile.q0 + r) * p.ldself + hc;
+                kr = static_cast<const T*>(p.kself) + static_cast<size_t>(tile.q0 + r) * p.ldself + hc;
             else
                 kr = K + static_cast<size_t>(tile.kv0 + j) * p.ldkv + hc;
             float part = 0.f;
-            for (int d = lane; d < dh; d += 32) part += q[d] * kr[d];
+            for (int d = lane; d < dh; d += 32) part += ActIO<T>::load(q + d) * ActIO<T>::load(kr + d);
             float sdot = warp_sum(part) * p.scale;
             if (lane == 0) logits[j] = sdot;
             mx = fmaxf(mx, sdot);
@@ -300,17 +303,29 @@ __global__ void k_attn_f32(AttnArgs p, int max_keys) {
         for (int d = lane; d < dh; d += 32) {
             float acc = 0.f;
             for (int j = 0; j < nkeys; j++) {
-                const float* vr;
+                const T* vr;
                 if (!p.causal && j == tile.nkv)
-                    vr = static_cast<const float*>(p.vself) + static_cast<size_t>(tile.q0 + r) * p.ldself + hc;
+                    vr = static_cast<const T*>(p.vself) + static_cast<size_t>(tile.q0 + r) * p.ldself + hc;
                 else
                     vr = V + static_cast<size_t>(tile.kv0 + j) * p.ldkv + hc;
-                acc += (expf(logits[j] - mx) * inv) * vr[d];
+                acc += (expf(logits[j] - mx) * inv) * ActIO<T>::load(vr + d);
             }
-            static_cast<float*>(p.out)[static_cast<size_t>(tile.q0 + r) * p.ldo + hc + d] = acc;
+            ActIO<T>::store(static_cast<T*>(p.out) + static_cast<size_t>(tile.q0 + r) * p.ldo + hc + d, acc);
         }
         __syncwarp();
     }
+}
+
+template <typename T>
+void launch_simt(const AttnArgs& a, cudaStream_t s) {
+    const int warps = 4;
+    size_t smem = static_cast<size_t>(warps) * (a.max_keys + 2) * sizeof(float);
+    dim3 grid(a.n_tiles, a.n_heads);
+    if (smem > 48 * 1024)
+        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_attn_simt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem)));
+    k_attn_simt<T><<<grid, warps * 32, smem, s>>>(a, a.max_keys + 1);
+    DCAT_LAUNCH_CHECK();
 }
 
 template <int DH>
@@ -329,20 +344,15 @@ void attention_bf16(const AttnArgs& a, cudaStream_t s) {
         case 16: launch_flash<16>(a, s); break;
         case 32: launch_flash<32>(a, s); break;
         case 64: launch_flash<64>(a, s); break;
-        default: throw InvalidArg("attention: head dim " + std::to_string(a.dh) + " not supported (16/32/64)");
+        default:
+            if (a.dh % 16 == 0) throw InvalidArg("attention: head dim " + std::to_string(a.dh) + " not supported");
+            launch_simt<bf16>(a, s);  // tiny head dims (< one mma k-step)
     }
 }
 
 void attention_f32(const AttnArgs& a, cudaStream_t s) {
     if (a.n_tiles <= 0) return;
-    const int warps = 4;
-    size_t smem = static_cast<size_t>(warps) * (a.max_keys + 2) * sizeof(float);
-    dim3 grid(a.n_tiles, a.n_heads);
-    if (smem > 48 * 1024)
-        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_attn_f32, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(smem)));
-    k_attn_f32<<<grid, warps * 32, smem, s>>>(a, a.max_keys + 1);
-    DCAT_LAUNCH_CHECK();
+    launch_simt<float>(a, s);
 }
 
 }  // namespace dcat

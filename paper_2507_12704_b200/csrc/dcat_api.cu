@@ -68,6 +68,7 @@ struct Lin {
     float* w32 = nullptr; // [in x out] fp32 (parity path, reference layout)
     float* bias = nullptr;
     int in = 0, out = 0;
+    int in32 = 0;  // fp32 path K (in, before bf16 zero padding)
 };
 
 struct LayerW {
@@ -157,6 +158,7 @@ void span(dcat_model* m, const char* name, int a, int b) {
 Lin make_lin(DevAlloc& mem, const float* w, const float* b, int in, int out, int k_pad = 0) {
     Lin L;
     L.in = in;
+    L.in32 = in;
     L.out = out;
     int kp = std::max(in, k_pad);
     std::vector<bf16> wt(static_cast<size_t>(out) * kp, __float2bfloat16(0.0f));
@@ -329,11 +331,11 @@ void gemm(dcat_model* m, const T* A, int lda, const Lin& L, int w_off, int N, in
         gemm_tc(A, lda, L.wt + static_cast<size_t>(w_off) * L.in, L.in, M, N, L.in, e, s);
         m->stats.kernel_launches += 1;
     } else {
-        gemm_f32(A, lda, L.w32 + w_off, L.out, M, N, L.in, e, tmp, s);
+        gemm_f32(A, lda, L.w32 + w_off, L.out, M, N, L.in32, e, tmp, s);
         m->stats.kernel_launches += 2;
     }
     m->stats.gemm_launches += 1;
-    m->stats.gemm_flops += 2.0 * M * N * L.in;
+    m->stats.gemm_flops += 2.0 * M * N * L.in32;
 }
 
 Epi base_epi(dcat_model* m, int mode, int layer_idx = -1) {
@@ -682,8 +684,8 @@ int dcat_model_create(const dcat_model_config* cfg, const dcat_params* params, c
         if (table->num_subtables * table->d_sub != c.d_emb)
             return set_err(DCAT_EINVAL, "segment_inputs: id source dim mismatch");
         int dh = c.d_model / c.n_heads;
-        if (dh != 16 && dh != 32 && dh != 64)
-            return set_err(DCAT_EUNSUPPORTED, "head dim " + std::to_string(dh) + " not supported (16/32/64)");
+        if (!(dh < 16 || dh == 16 || dh == 32 || dh == 64))
+            return set_err(DCAT_EUNSUPPORTED, "head dim " + std::to_string(dh) + " not supported (<16, 16, 32, 64)");
         if (c.d_model % 16 || c.d_emb % 8)
             return set_err(DCAT_EUNSUPPORTED, "d_model must be a multiple of 16 and d_emb of 8");
         m->device = device;
