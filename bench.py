@@ -1,0 +1,401 @@
+"""DCAT scoring benchmark (BASELINE.json metric: candidates scored / s).
+
+One step = one rank_forward_batch over one request batch of synthetic input:
+dedup -> context pass -> crossing pass -> ranking head, per GPU the PinFM-base
+workload (BASELINE.json configs[1]: 4 layers, d=256, 8 heads, L=256, 1000 unique
+users x 128 candidates). Multi-GPU (torchrun): every rank scores its own
+user-disjoint batch (weak scaling), scores are gathered to rank 0 over NCCL
+inside the timed region, time = max over ranks.
+
+  value : device-resident inputs (CUDA events around each step; L2 flushed
+          between steps), candidates/s summed over ranks.
+  e2e   : the same call through the public API with pinned HOST buffers:
+          H2D of the batch and D2H of the logits inside the timed region.
+  --impl reference : the reference's own CPU implementation (oracle/_ref, the
+          unmodified reference sources; rank_forward_batch fanned out over all
+          host threads) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2507_12704_b200.abi import Batch, FinetuneSpec  # noqa: E402
+from paper_2507_12704_b200.synth import CONFIGS, init_weights, make_batch  # noqa: E402
+
+METRIC = "candidates scored/sec (seq len L, C cands/user) at 1/2/4/8 B200; vs CPU ref"
+UNIT = "candidates/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def gemm_flops(cfg, U, C, L):
+    """Algorithmic GEMM flops per batch: per unique user
+    L*(2*de*d + 2*d^2) + (l-1)*L*24d^2 + L*4d^2, per candidate
+    (2*de*d + 2d^2) + l*24d^2 + 4d^2 + 2(2d+8)*64 (head; the 64x3 tail is epilogue FFMA)."""
+    s = cfg["spec"]
+    d, de, nl = s.d_model, s.d_emb, s.n_layers
+    per_user = L * (2 * de * d + 2 * d * d) + (nl - 1) * L * 24 * d * d + L * 4 * d * d
+    per_cand = (2 * de * d + 2 * d * d) + nl * 24 * d * d + 4 * d * d + 2 * (d + de + 8) * 64
+    return U * per_user + U * C * per_cand
+
+
+def attn_flops(cfg, U, C, L):
+    s = cfg["spec"]
+    d, nl = s.d_model, s.n_layers
+    ctx = (nl - 1) * 2 * d * L * (L + 1) * U
+    cross = nl * 4 * d * (L + 1) * U * C
+    return ctx, cross
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            try:
+                a, b, r = [x.strip() for x in line.split(",")]
+                self.samples.append((float(a), float(b), int(r, 16) if r.startswith("0x") else int(r)))
+            except Exception:
+                pass
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        busy = [s for s in self.samples if not (s[2] & 0x1)] or self.samples
+        reasons = set()
+        for s in busy:
+            for bit, name in self.REASONS.items():
+                if s[2] & bit and bit != 0x1:
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median([s[0] for s in busy])), "sm_max_mhz": float(max(s[1] for s in busy)),
+                "reasons": sorted(reasons), "samples": len(busy)}
+
+
+def to_torch(a, device):
+    import torch
+    if a.dtype == np.uint64:
+        a = a.view(np.int64)
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.to(device) if device != "pinned" else t.pin_memory()
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2507_12704_b200 import api
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = CONFIGS[args.config]
+    U, C, L = cfg["U"], cfg["C"], cfg["L"]
+    if args.users:
+        U = args.users
+    spec = cfg["spec"]
+    w = init_weights(spec, seed=42)
+    ft = FinetuneSpec(max_events=L)
+    host = make_batch(U, C, L, seed=1 + 1000 * rank, layout="interleaved", shared_storage=not args.private_rows)
+    B = host.n_rows
+    model = api.DcatModel(w, device=local_rank)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    dbatch = host.to(lambda a: to_torch(a, dev))
+    out_dev = (torch.empty((B, 3), device=dev), torch.empty((B, 3), device=dev), None)
+    gathered = [torch.empty((B, 6), device=dev) for _ in range(world)] if (world > 1 and rank == 0) else None
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def gather_scores(lg, ml):
+        if world == 1:
+            return
+        packed = torch.cat([lg, ml], dim=1)
+        dist.gather(packed, gathered if rank == 0 else None, dst=0)
+
+    def step_device(profile=False):
+        lg, ml, _ = model.rank_forward_batch(dbatch, ft, stream=sp, out=out_dev, profile=profile)
+        gather_scores(lg, ml)
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+
+    clocks = Clocks(local_rank)
+    clocks.start()
+    stage_tot = {}
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()  # L2 flush (256 MB > 126 MB L2), outside the timed span
+        ev[k][0].record(stream)
+        step_device(profile=True)
+        ev[k][1].record(stream)
+        for n, v in model.stage_times().items():
+            stage_tot[n] = stage_tot.get(n, 0.0) + v
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_dev = sum(a.elapsed_time(b) for a, b in ev)
+    stats = model.last_stats()
+
+    # ---- e2e through the public API with pinned host buffers
+    pinned = host.to(lambda a: to_torch(a, "pinned"))
+    hbatch = pinned.to(lambda t: t.numpy())
+    hbatch.ev_ts = hbatch.ev_ts.view(np.uint64)
+    hbatch.ev_item = hbatch.ev_item.view(np.uint64)
+    hbatch.candidate = hbatch.candidate.view(np.uint64)
+    h_out = tuple(torch.empty((B, 3), dtype=torch.float32).pin_memory().numpy() for _ in range(2)) + (None,)
+    h2d = sum(int(getattr(host, f).nbytes) for f in ("row_offset", "row_valid", "ev_ts", "ev_action", "ev_surface",
+                                                     "ev_item", "candidate", "age_seconds"))
+    d2h = 2 * B * 3 * 4
+
+    def step_host():
+        lg, ml, _ = model.rank_forward_batch(hbatch, ft, stream=sp, out=h_out)
+        if world > 1:
+            gather_scores(torch.from_numpy(lg).to(dev), torch.from_numpy(ml).to(dev))
+
+    for _ in range(max(1, args.warmup)):
+        step_host()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_ms = 0.0
+    for k in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ev[k][0].record(stream)
+        step_host()
+        ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        e2e_ms += ev[k][0].elapsed_time(ev[k][1])
+
+    # ---- private-rows variant (every row its own event copy, like std::vector<RankingExample>)
+    priv = None
+    if not args.private_rows and not args.no_private:
+        pb = make_batch(U, C, L, seed=1 + 1000 * rank, layout="interleaved", shared_storage=False)
+        pbd = pb.to(lambda a: to_torch(a, dev))
+        model.rank_forward_batch(pbd, ft, stream=sp, out=out_dev)
+        torch.cuda.synchronize()
+        pms = 0.0
+        for k in range(max(1, args.steps // 2)):
+            flush.zero_()
+            ev[k][0].record(stream)
+            model.rank_forward_batch(pbd, ft, stream=sp, out=out_dev)
+            ev[k][1].record(stream)
+            torch.cuda.synchronize()
+            pms += ev[k][0].elapsed_time(ev[k][1])
+        priv = pms / max(1, args.steps // 2)
+        del pbd
+
+    t = torch.tensor([ms_dev, e2e_ms, priv or 0.0], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_dev, e2e_ms, priv = float(t[0]), float(t[1]), (float(t[2]) if priv is not None else None)
+    if rank != 0:
+        return None
+
+    K = args.steps
+    ms_step = ms_dev / K
+    value = world * B / (ms_step / 1e3)
+    hbm, tf_burst, tf_sus, peak_kind = peaks()
+    # dominant kernel class: the tcgen05 GEMMs (all launches of k_gemm_tc)
+    gemm_ms = sum(v for n, v in stage_tot.items() if n.startswith("gemm.")) / K
+    gf = gemm_flops(cfg, U, C, L)
+    achieved = gf / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    ctx_f, cross_f = attn_flops(cfg, U, C, L)
+    attn_ctx_ms = stage_tot.get("attn.ctx", 0.0) / K
+    attn_cross_ms = stage_tot.get("attn.cross", 0.0) / K
+    s = spec
+    kv_bytes = s.n_layers * 4 * U * L * s.d_model + B * s.n_layers * 8 * s.d_model
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("dram_bytes_per_flop_weighted")
+        except Exception:
+            traffic = None
+    stages = {n: round(v / K, 4) for n, v in sorted(stage_tot.items())}
+    line = {
+        "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 4), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded run_bench recipe, dcat.cpp:493-521; random-init weights)",
+        "config": {"workload": f"{args.config}: {s.n_layers} layers, d={s.d_model}, {s.n_heads} heads, L={L}, "
+                               f"{U} unique users x {C} candidates per GPU",
+                   "unique_users_per_gpu": U, "cands_per_user": C, "seq_len": L, "rows_per_gpu": B,
+                   "input": "private per-row event copies" if args.private_rows else
+                            "CSR event pool, rows of one user share one span (dedup still hashes + verifies every row)",
+                   "l2": "256 MB buffer written between timed steps; per-step working set ~3 GB > 126 MB L2",
+                   "parallelism": f"user-sharded x{world}, NCCL score gather"},
+        "e2e": {"value": round(world * B / (e2e_ms / K / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms / K, 4)},
+        "gpu_launches": int(stats["kernel_launches"]) * K,
+        "roofline": {"bound": "tensor", "kernel": "k_gemm_tc (all tcgen05 GEMM launches of a step)",
+                     "achieved": round(achieved, 1) if achieved else None, "peak": tf_sus, "unit": "TFLOP/s",
+                     "frac": round(achieved / tf_sus, 4) if achieved else None, "peak_kind": f"{peak_kind} sustained",
+                     "traffic": traffic, "gemm_ms_per_step": round(gemm_ms, 4),
+                     "gemm_flops_per_step": gf, "gemm_share_of_step": round(gemm_ms / ms_step, 3)},
+        "kernels": {
+            "attn.ctx": {"ms": round(attn_ctx_ms, 4), "tflops": round(ctx_f / (attn_ctx_ms / 1e3) / 1e12, 1)
+                         if attn_ctx_ms else None},
+            "attn.cross": {"ms": round(attn_cross_ms, 4),
+                           "tflops": round(cross_f / (attn_cross_ms / 1e3) / 1e12, 1) if attn_cross_ms else None,
+                           "hbm_gbs": round(kv_bytes / (attn_cross_ms / 1e3) / 1e9, 1) if attn_cross_ms else None,
+                           "hbm_frac": round(kv_bytes / (attn_cross_ms / 1e3) / 1e9 / hbm, 4) if attn_cross_ms else None},
+        },
+        "stages_ms": stages,
+        "clocks": clk,
+    }
+    if priv:
+        line["value_private_rows"] = round(world * B / (priv / 1e3), 1)
+    if world == 1 and not args.no_cpu:
+        line["cpu_baseline"], line["parity"] = cpu_baseline(args, w, host, ft, model)
+    return line
+
+
+def cpu_baseline(args, w, host: Batch, ft, model):
+    """The reference's CPU path (oracle/_ref) on a bounded sample of the same
+    workload: S users with all their candidates, on all host threads."""
+    from oracle import pyoracle
+    kind = "reference" if pyoracle.have_reference() else "port"
+    impl = pyoracle.reference() if kind == "reference" else pyoracle.oracle()
+    threads = os.cpu_count() or 1
+    U = CONFIGS[args.config]["U"] if not args.users else args.users
+    S = min(U, max(2, args.cpu_users or 2 * threads) if kind == "reference" else 2)
+    users = np.arange(S)
+    rows = np.nonzero(np.isin(np.arange(host.n_rows) % U, users))[0]
+    sub = host.take(rows)
+    t0 = time.perf_counter()
+    if kind == "reference":
+        rl, rm, _, _ = impl.rank_forward_batch(w, ft, sub, n_threads=threads)
+        cores = min(threads, S)
+    else:
+        rl, rm, _, _ = impl.rank_forward_batch(w, ft, sub)
+        cores = 1
+    dt = time.perf_counter() - t0
+    lg, ml, _ = model.rank_forward_batch(sub, ft)
+    scale = max(1e-3, float(np.abs(rl).max()))
+    parity = {"rows": int(len(rows)), "max_rel_err_logits": float(np.abs(lg - rl).max() / scale),
+              "max_rel_err_module_logits": float(np.abs(ml - rm).max() / max(1e-3, float(np.abs(rm).max()))),
+              "tolerance": 3e-2, "vs": kind}
+    return ({"value": round(len(rows) / dt, 2), "unit": UNIT, "cores": cores, "kind": kind,
+             "sample": f"{S} users x {host.n_rows // U} candidates ({len(rows)} rows) of the same batch, "
+                       f"{dt:.1f} s wall on {cores} threads"}, parity)
+
+
+def run_reference(args):
+    from oracle import pyoracle
+    cfg = CONFIGS[args.config]
+    U, C, L = cfg["U"], cfg["C"], cfg["L"]
+    w = init_weights(cfg["spec"], seed=42)
+    ft = FinetuneSpec(max_events=L)
+    if not pyoracle.have_reference():
+        kind, impl, threads = "port", pyoracle.oracle(), 1
+    else:
+        kind, impl, threads = "reference", pyoracle.reference(), os.cpu_count() or 1
+    S = min(U, args.cpu_users or max(2, threads))  # users per step: one user per thread
+    host = make_batch(U, C, L, seed=1, layout="interleaved")
+    rows = np.nonzero(np.isin(np.arange(host.n_rows) % U, np.arange(S)))[0]
+    sub = host.take(rows)
+    run = (lambda: impl.rank_forward_batch(w, ft, sub, n_threads=threads)) if kind == "reference" else \
+        (lambda: impl.rank_forward_batch(w, ft, sub))
+    for _ in range(args.warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    dt = (time.perf_counter() - t0) / args.steps
+    v = round(len(rows) / dt, 2)
+    s = cfg["spec"]
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {s.n_layers} layers, d={s.d_model}, {s.n_heads} heads, L={L}, "
+                                   f"{U} users x {C} candidates (each step: a {S}-user sample)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": min(threads, S), "kind": kind,
+                             "sample": f"{S} users x {C} candidates per step ({len(rows)} rows)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="pinfm-base", choices=sorted(CONFIGS))
+    ap.add_argument("--users", type=int, default=0, help="override unique users per GPU")
+    ap.add_argument("--cpu-users", type=int, default=0)
+    ap.add_argument("--private-rows", action="store_true", help="every row carries its own event copy")
+    ap.add_argument("--no-private", action="store_true", help="skip the private-rows side measurement")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_ours(args, rank, world, local_rank)
+    if rank == 0 and line:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

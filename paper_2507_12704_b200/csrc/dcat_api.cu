@@ -324,9 +324,10 @@ struct Acts {
 };
 
 template <typename T>
-void gemm(dcat_model* m, const T* A, int lda, const Lin& L, int w_off, int N, int M, const Epi& e, float* tmp,
-          cudaStream_t s) {
+void gemm(dcat_model* m, const char* tag, const T* A, int lda, const Lin& L, int w_off, int N, int M, const Epi& e,
+          float* tmp, cudaStream_t s) {
     if (M <= 0) return;
+    int t0 = mark(m, s);
     if constexpr (std::is_same<T, bf16>::value) {
         gemm_tc(A, lda, L.wt + static_cast<size_t>(w_off) * L.in, L.in, M, N, L.in, e, s);
         m->stats.kernel_launches += 1;
@@ -336,6 +337,7 @@ void gemm(dcat_model* m, const T* A, int lda, const Lin& L, int w_off, int N, in
     }
     m->stats.gemm_launches += 1;
     m->stats.gemm_flops += 2.0 * M * N * L.in32;
+    span(m, tag, t0, mark(m, s));
 }
 
 Epi base_epi(dcat_model* m, int mode, int layer_idx = -1) {
@@ -349,9 +351,11 @@ Epi base_epi(dcat_model* m, int mode, int layer_idx = -1) {
 
 template <typename T>
 void attn(dcat_model* m, const AttnArgs& a, cudaStream_t s) {
+    int t0 = mark(m, s);
     if constexpr (std::is_same<T, bf16>::value) attention_bf16(a, s);
     else attention_f32(a, s);
     m->stats.kernel_launches += 1;
+    span(m, a.causal ? "attn.ctx" : "attn.cross", t0, mark(m, s));
 }
 
 // Base / Aux with the sequence module (finetune.cpp:459-492)
@@ -414,7 +418,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         e.out[0] = A.h1;
         e.out_ld[0] = d;
         e.seg_cols = d;
-        gemm<T>(m, A.E, de, m->phi_in1, 0, d, M, e, A.tmp, s);
+        gemm<T>(m, "gemm.ctx.phi_in1", A.E, de, m->phi_in1, 0, d, M, e, A.tmp, s);
         e = base_epi(m, EPI_L2NORM);
         e.bias = m->phi_in2.bias;
         e.x_out = A.x;
@@ -423,7 +427,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         e.ln_b = m->layers[0].ln1_b;
         e.ln_out = A.a;
         e.ln_ld = d;
-        gemm<T>(m, A.h1, d, m->phi_in2, 0, d, M, e, A.tmp, s);
+        gemm<T>(m, "gemm.ctx.phi_in2", A.h1, d, m->phi_in2, 0, d, M, e, A.tmp, s);
         for (int l = 0; l < nl; l++) {
             const LayerW& L = m->layers[l];
             if (l == nl - 1) {  // kv_only (dcat.cpp:60-65): K, V of the final layer
@@ -433,7 +437,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
                 e.out[1] = V_l(l);
                 e.out_ld[0] = e.out_ld[1] = d;
                 e.seg_cols = d;
-                gemm<T>(m, A.a, d, L.qkv, d, 2 * d, M, e, A.tmp, s);
+                gemm<T>(m, "gemm.ctx.kv", A.a, d, L.qkv, d, 2 * d, M, e, A.tmp, s);
                 break;
             }
             // layer_forward (model.cpp:336-398); K, V go straight to the cache
@@ -444,7 +448,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             e.out[2] = V_l(l);
             e.out_ld[0] = e.out_ld[1] = e.out_ld[2] = d;
             e.seg_cols = d;
-            gemm<T>(m, A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
+            gemm<T>(m, "gemm.ctx.qkv", A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
             AttnArgs aa{A.q, d, K_l(l), V_l(l), d, nullptr, nullptr, 0, A.ctx, d, ctx_tiles, st.ctx_tiles,
                         H,   dh, scale, 1, c.max_len + 1};
             attn<T>(m, aa, s);
@@ -458,14 +462,14 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             e.ln_b = L.ln2_b;
             e.ln_out = A.a;
             e.ln_ld = d;
-            gemm<T>(m, A.ctx, d, L.o, 0, d, M, e, A.tmp, s);
+            gemm<T>(m, "gemm.ctx.o", A.ctx, d, L.o, 0, d, M, e, A.tmp, s);
             e = base_epi(m, EPI_BIAS);
             e.act = 1;
             e.bias = L.f1.bias;
             e.out[0] = A.f1;
             e.out_ld[0] = F;
             e.seg_cols = F;
-            gemm<T>(m, A.a, d, L.f1, 0, F, M, e, A.tmp, s);
+            gemm<T>(m, "gemm.ctx.ffn1", A.a, d, L.f1, 0, F, M, e, A.tmp, s);
             e = base_epi(m, EPI_RESID_LN, l);
             e.bias = L.f2.bias;
             e.resid = A.x;
@@ -475,7 +479,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             e.ln_b = m->layers[l + 1].ln1_b;
             e.ln_out = A.a;
             e.ln_ld = d;
-            gemm<T>(m, A.f1, F, L.f2, 0, d, M, e, A.tmp, s);
+            gemm<T>(m, "gemm.ctx.ffn2", A.f1, F, L.f2, 0, d, M, e, A.tmp, s);
         }
     }
     int t_ctx1 = mark(m, s);
@@ -492,7 +496,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     e.out[0] = A.h1;
     e.out_ld[0] = d;
     e.seg_cols = d;
-    gemm<T>(m, A.E, de, m->phi_in1, 0, d, M, e, A.tmp, s);
+    gemm<T>(m, "gemm.cross.phi_in1", A.E, de, m->phi_in1, 0, d, M, e, A.tmp, s);
     e = base_epi(m, EPI_L2NORM);
     e.bias = m->phi_in2.bias;
     e.x_out = A.x;
@@ -501,7 +505,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     e.ln_b = m->layers[0].ln1_b;
     e.ln_out = A.a;
     e.ln_ld = d;
-    gemm<T>(m, A.h1, d, m->phi_in2, 0, d, M, e, A.tmp, s);
+    gemm<T>(m, "gemm.cross.phi_in2", A.h1, d, m->phi_in2, 0, d, M, e, A.tmp, s);
     for (int l = 0; l < nl; l++) {
         const LayerW& L = m->layers[l];
         e = base_epi(m, EPI_BIAS);
@@ -511,7 +515,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         e.out[2] = A.vself;
         e.out_ld[0] = e.out_ld[1] = e.out_ld[2] = d;
         e.seg_cols = d;
-        gemm<T>(m, A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
+        gemm<T>(m, "gemm.cross.qkv", A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
         AttnArgs aa{A.q, d, K_l(l), V_l(l), d, A.kself, A.vself, d, A.ctx, d, cross_tiles, st.cross_tiles,
                     H,   dh, scale, 0, c.max_len + 1};
         attn<T>(m, aa, s);
@@ -524,14 +528,14 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         e.ln_b = L.ln2_b;
         e.ln_out = A.a;
         e.ln_ld = d;
-        gemm<T>(m, A.ctx, d, L.o, 0, d, M, e, A.tmp, s);
+        gemm<T>(m, "gemm.cross.o", A.ctx, d, L.o, 0, d, M, e, A.tmp, s);
         e = base_epi(m, EPI_BIAS);
         e.act = 1;
         e.bias = L.f1.bias;
         e.out[0] = A.f1;
         e.out_ld[0] = F;
         e.seg_cols = F;
-        gemm<T>(m, A.a, d, L.f1, 0, F, M, e, A.tmp, s);
+        gemm<T>(m, "gemm.cross.ffn1", A.a, d, L.f1, 0, F, M, e, A.tmp, s);
         e = base_epi(m, EPI_RESID_LN, l);  // cross_tail's finite check (dcat.cpp:85-86)
         e.bias = L.f2.bias;
         e.resid = A.x;
@@ -541,7 +545,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         e.ln_b = l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr;
         e.ln_out = A.a;
         e.ln_ld = d;
-        gemm<T>(m, A.f1, F, L.f2, 0, d, M, e, A.tmp, s);
+        gemm<T>(m, "gemm.cross.ffn2", A.f1, F, L.f2, 0, d, M, e, A.tmp, s);
     }
     // phi_out (dcat.cpp:266) + module head (finetune.cpp:317-323)
     e = base_epi(m, EPI_BIAS);
@@ -550,7 +554,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     e.out[0] = A.h1;
     e.out_ld[0] = d;
     e.seg_cols = d;
-    gemm<T>(m, A.a, d, m->phi_out1, 0, d, M, e, A.tmp, s);
+    gemm<T>(m, "gemm.cross.phi_out1", A.a, d, m->phi_out1, 0, d, M, e, A.tmp, s);
     e = base_epi(m, EPI_L2NORM);
     e.bias = m->phi_out2.bias;
     e.x_out = h_cand ? A.hc : nullptr;
@@ -560,7 +564,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     e.mod_w = m->mod_w;
     e.mod_b = m->mod_b;
     e.mlogits = A.mlog_p;
-    gemm<T>(m, A.h1, d, m->phi_out2, 0, d, M, e, A.tmp, s);
+    gemm<T>(m, "gemm.cross.phi_out2", A.h1, d, m->phi_out2, 0, d, M, e, A.tmp, s);
     int t_cross1 = mark(m, s);
     // ranking head: crossing MLP on [H_cand | cand_emb | ctx] (finetune.cpp:301-316)
     e = base_epi(m, EPI_HEAD);
@@ -568,7 +572,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     e.w2 = m->hw2;
     e.b2 = m->hb2;
     e.logits = A.logits_p;
-    gemm<T>(m, A.feat, kh, m->head1, 0, m->hidden, M, e, A.tmp, s);
+    gemm<T>(m, "gemm.head", A.feat, kh, m->head1, 0, m->hidden, M, e, A.tmp, s);
     scatter_outputs(o.perm, B, A.logits_p, A.mlog_p, h_cand ? A.hc : nullptr, d, logits, mlogits, h_cand, s);
     m->stats.kernel_launches += 1;
     int t_end = mark(m, s);
@@ -601,7 +605,7 @@ void run_head_only(dcat_model* m, const Staged& sb, const DedupOut& o, const dca
     e.w2 = m->hw2;
     e.b2 = m->hb2;
     e.logits = logits_p;
-    gemm<T>(m, feat, kh, m->head1, 0, m->hidden, static_cast<int>(B), e, tmp, s);
+    gemm<T>(m, "gemm.head", feat, kh, m->head1, 0, m->hidden, static_cast<int>(B), e, tmp, s);
     std::vector<float> mb(static_cast<size_t>(Bp) * 3);
     float hb[3];
     DCAT_CUDA_CHECK(cudaMemcpy(hb, m->mod_b, sizeof hb, cudaMemcpyDeviceToHost));

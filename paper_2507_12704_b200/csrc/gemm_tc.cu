@@ -9,23 +9,30 @@
 // (dcat.cpp:226-229, 77-87), and the ranking head's crossing MLP
 // (finetune.cpp:310-315).
 //
-// One CTA computes one 128 x BN tile:
-//   warp 0     TMA producer (A 128x64 and B BNx64 boxes, 128B swizzle)
-//   warp 1     single-thread tcgen05.mma issuer, fp32 accumulator in TMEM
-//   warp 2     TMEM allocator
-//   warps 4-7  epilogue: tcgen05.ld 32x32b -> registers, one row per thread
-// STAGES-deep smem ring with full/empty mbarriers; 2 CTAs per SM (BN <= 256)
-// so one CTA's epilogue overlaps the other's main loop.
-//
-// Epilogues (launch.h EpiMode), all row-local so one thread owns a row:
+// Persistent, warp-specialized, one CTA per SM:
+//   warp 0        TMA producer: A 128x64 and B BNx64 boxes (128B swizzle) into
+//                 a STAGES-deep smem ring (full/empty mbarriers)
+//   warp 1        single-thread tcgen05.mma issuer (M=128, N<=256 per MMA,
+//                 K=16), fp32 accumulators in TMEM, double-buffered across
+//                 tiles (tmem_full/tmem_empty mbarriers) so tile i+1's main
+//                 loop overlaps tile i's epilogue
+//   warp 2        TMEM allocator
+//   warps 4..     epilogue: CG warps per TMEM lane quadrant, each owning
+//                 BN/CG columns of 32 rows; tcgen05.ld 32x32b, math in
+//                 registers (one row per thread), global I/O transposed through
+//                 per-warp smem so every load/store is row-contiguous
+// Epilogues (launch.h EpiMode):
 //   EPI_BIAS     act(acc + b) -> bf16, split into up to 3 column segments
 //                (QKV -> q, K cache, V cache; FFN1 with GELU)
-//   EPI_RESID_LN x = acc + b + resid -> fp32 residual stream, then LayerNorm
-//                (eps 1e-5, model.cpp:54-81) of x -> bf16 for the next GEMM
+//   EPI_RESID_LN x = acc + b + resid -> fp32 residual stream; LayerNorm
+//                (eps 1e-5, model.cpp:54-81) of x -> bf16 operand of the next GEMM
 //   EPI_L2NORM   y = (acc + b) / max(||acc + b||, 1e-12) (model.cpp:107-117)
 //                -> fp32, optional LN, optional bf16 copy, optional module
 //                logits y . mod_w + mod_b (finetune.cpp:317-323)
 //   EPI_HEAD     z = gelu(acc + b1); logits = z . w2 + b2 (finetune.cpp:310-315)
+// Row statistics (LN mean/var, l2 norm, head dots) are reduced across the CG
+// warps of a quadrant through smem with a per-quadrant named barrier, in a
+// fixed order (deterministic).
 #include <cuda.h>
 
 #include <mutex>
@@ -40,17 +47,63 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int A_BYTES = BM * BK * 2;
+constexpr int SROW = 36;  // staging row pitch (floats): 16B-aligned rows, conflict-free v4 transposes
 
 template <int BN>
 struct Cfg {
-    static constexpr int STAGES = BN == 64 ? 4 : BN == 128 ? 3 : 2;
-    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int CG = BN == 64 ? 2 : BN == 512 ? 2 : 4;  // epilogue warps per lane quadrant
+    static constexpr int EPI_WARPS = 4 * CG;
+    static constexpr int EPI_THREADS = 32 * EPI_WARPS;
+    static constexpr int THREADS = 128 + EPI_THREADS;
+    static constexpr int CPW = BN / CG;  // columns per epilogue warp
+    static constexpr int CHUNKS = CPW / 32;
     static constexpr int MMA_N = BN > 256 ? 256 : BN;
-    static constexpr int N_HALVES = BN > 256 ? 2 : 1;
-    static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
-    static constexpr int SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 + 256;
-    static constexpr int MIN_BLOCKS = BN <= 256 ? 2 : 1;
+    static constexpr int N_HALVES = BN / MMA_N;
+    static constexpr int ACC_BUFS = BN <= 256 ? 2 : 1;
+    static constexpr int TMEM_COLS = BN * ACC_BUFS < 32 ? 32 : BN * ACC_BUFS;
+    static constexpr int STAGES = BN == 64 ? 6 : BN == 128 ? 4 : 2;
+    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int RING = STAGES * (A_BYTES + B_BYTES);
+    static constexpr int STAGING = EPI_WARPS * 32 * SROW * 4;
+    static constexpr int RED = 4 * 3 * CG * 32 * 4;          // [quadrant][value][cg][lane]
+    static constexpr int PARAM_FLOATS = BN == 512 ? 3104 : 1600;  // bias | ln_g | ln_b | mod_w/w2 | mod_b/b2
+    static constexpr int SMEM = RING + STAGING + RED + PARAM_FLOATS * 4 + 1024 + 256;
 };
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ptx::smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void sts4(uint32_t a, float x, float y, float z, float w) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts1(uint32_t a, float x) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory");
+}
+__device__ __forceinline__ float lds1(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// tanh-form GELU (model.hpp:14-18) with the MUFU tanh: its ~2^-11 relative
+// error is below the bf16 rounding of every consumer of this value.
+__device__ __forceinline__ float gelu_fast(float x) {
+    float x3 = x * x * x;
+    return 0.5f * x * (1.0f + tanh_fast(0.7978845608028654f * (x + 0.044715f * x3)));
+}
 
 __device__ __forceinline__ void tmem_load32(uint32_t taddr, float* v) {
     uint32_t r[32];
@@ -67,79 +120,199 @@ __device__ __forceinline__ void tmem_store32(uint32_t taddr, const float* v) {
     ptx::tmem_wait_st();
 }
 
-// store 32 values (columns c0..c0+31 of a segment-local row) as bf16
-__device__ __forceinline__ void store_bf16_32(bf16* dst, const float* v, int ncols) {
-    if (ncols >= 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+// 32 consecutive params starting at smem float index p (broadcast reads)
+__device__ __forceinline__ void lds32(uint32_t sp, int p, float* out) {
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            uint4 p;
-            p.x = pack_bf16(v[8 * j + 0], v[8 * j + 1]);
-            p.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
-            p.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
-            p.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
-            reinterpret_cast<uint4*>(dst)[j] = p;
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 32; i++)
-            if (i < ncols) dst[i] = __float2bfloat16_rn(v[i]);
+    for (int i = 0; i < 32; i += 4) {
+        float4 t = lds4(sp + 4u * (p + i));
+        out[i] = t.x;
+        out[i + 1] = t.y;
+        out[i + 2] = t.z;
+        out[i + 3] = t.w;
     }
 }
 
-__device__ __forceinline__ void load_f32_32(const float* src, float* v, int ncols) {
-    if (ncols >= 32 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+// ---- warp-cooperative, row-contiguous global I/O of a 32 x 32 block through
+// this warp's smem staging tile `st` (shared address). `v` holds this lane's
+// row (row_base + lane), block columns [0, nc).
+
+__device__ __forceinline__ void put_stage(uint32_t st, const float* v, int lane) {
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-            float4 f = __ldg(reinterpret_cast<const float4*>(src) + j);
-            v[4 * j] = f.x;
-            v[4 * j + 1] = f.y;
-            v[4 * j + 2] = f.z;
-            v[4 * j + 3] = f.w;
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 32; i++) v[i] = i < ncols ? __ldg(src + i) : 0.0f;
-    }
+    for (int i = 0; i < 32; i += 4) sts4(st + 4u * (lane * SROW + i), v[i], v[i + 1], v[i + 2], v[i + 3]);
+    __syncwarp();
 }
 
-__device__ __forceinline__ void store_f32_32(float* dst, const float* v, int ncols) {
-    if (ncols >= 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+__device__ __forceinline__ void store_bf16_block(uint32_t st, const float* v, bf16* base, size_t ld, int row_base,
+                                                 int M, int nc, int lane) {
+    put_stage(st, v, lane);
 #pragma unroll
-        for (int j = 0; j < 8; j++)
-            reinterpret_cast<float4*>(dst)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-    } else {
+    for (int k = 0; k < 4; k++) {
+        const int idx = lane + 32 * k, r = idx >> 2, c = (idx & 3) * 8;
+        const int gr = row_base + r;
+        if (gr < M && c < nc) {
+            float4 a = lds4(st + 4u * (r * SROW + c));
+            float4 b = lds4(st + 4u * (r * SROW + c + 4));
+            bf16* dst = base + static_cast<size_t>(gr) * ld + c;
+            if (c + 8 <= nc && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                uint4 p;
+                p.x = pack_bf16(a.x, a.y);
+                p.y = pack_bf16(a.z, a.w);
+                p.z = pack_bf16(b.x, b.y);
+                p.w = pack_bf16(b.z, b.w);
+                *reinterpret_cast<uint4*>(dst) = p;
+            } else {
+                float t[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-        for (int i = 0; i < 32; i++)
-            if (i < ncols) dst[i] = v[i];
+                for (int j = 0; j < 8; j++)
+                    if (c + j < nc) dst[j] = __float2bfloat16_rn(t[j]);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void store_f32_block(uint32_t st, const float* v, float* base, size_t ld, int row_base,
+                                                int M, int nc, int lane) {
+    put_stage(st, v, lane);
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const int idx = lane + 32 * k, r = idx >> 3, c = (idx & 7) * 4;
+        const int gr = row_base + r;
+        if (gr < M && c < nc) {
+            float4 a = lds4(st + 4u * (r * SROW + c));
+            float* dst = base + static_cast<size_t>(gr) * ld + c;
+            if (c + 4 <= nc && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                *reinterpret_cast<float4*>(dst) = a;
+            } else {
+                float t[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (c + j < nc) dst[j] = t[j];
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// rows [row_base, row_base+32) x cols [0, nc) of a fp32 matrix -> out (this lane's row)
+__device__ __forceinline__ void load_f32_block(uint32_t st, const float* base, size_t ld, int row_base, int M, int nc,
+                                               int lane, float* out) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const int idx = lane + 32 * k, r = idx >> 3, c = (idx & 7) * 4;
+        const int gr = row_base + r;
+        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gr < M && c < nc) {
+            const float* src = base + static_cast<size_t>(gr) * ld + c;
+            if (c + 4 <= nc && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                x = *reinterpret_cast<const float4*>(src);  // may alias x_out (in place): coherent load
+            } else {
+                float t[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    if (c + j < nc) t[j] = src[j];
+                x = make_float4(t[0], t[1], t[2], t[3]);
+            }
+        }
+        sts4(st + 4u * (r * SROW + c), x.x, x.y, x.z, x.w);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+        float4 t = lds4(st + 4u * (lane * SROW + i));
+        out[i] = t.x;
+        out[i + 1] = t.y;
+        out[i + 2] = t.z;
+        out[i + 3] = t.w;
+    }
+    __syncwarp();
+}
+
+// sum of NV per-row partials over the CG warps of one lane quadrant (fixed order)
+template <int CG, int NV>
+__device__ __forceinline__ void quad_reduce(uint32_t red, float* vals, int cg, int lane, int q) {
+    const uint32_t r = red + 4u * (q * 3 * CG * 32);
+#pragma unroll
+    for (int k = 0; k < NV; k++) sts1(r + 4u * ((k * CG + cg) * 32 + lane), vals[k]);
+    named_bar(1 + q, CG * 32);
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        float s = 0.f;
+#pragma unroll
+        for (int c = 0; c < CG; c++) s += lds1(r + 4u * ((k * CG + c) * 32 + lane));
+        vals[k] = s;
+    }
+    named_bar(1 + q, CG * 32);
+}
+
+// smem parameter layout (floats): [0, N) bias; then per mode
+//   RESID_LN / L2NORM: [P_G, +N) ln_g, [P_B, +N) ln_b; L2NORM: [P_W, +3N) mod_w, [P_W + 3N, +3) mod_b
+//   HEAD: [P_W, +3N) w2, [P_W + 3N, +3) b2
+struct ParamLayout {
+    int npad, P_G, P_B, P_W;
+};
+__device__ __forceinline__ ParamLayout param_layout(int N) {
+    ParamLayout L;
+    L.npad = (N + 31) & ~31;
+    L.P_G = L.npad;
+    L.P_B = 2 * L.npad;
+    L.P_W = 3 * L.npad;
+    return L;
+}
+
+template <int BN, int MODE>
+__device__ void load_params(const Epi& e, uint32_t sp, int N, int tid, int nthreads) {
+    const ParamLayout L = param_layout(N);
+    for (int i = tid; i < L.npad; i += nthreads) sts1(sp + 4u * i, i < N ? e.bias[i] : 0.f);
+    if constexpr (MODE == EPI_RESID_LN || MODE == EPI_L2NORM) {
+        for (int i = tid; i < L.npad; i += nthreads) {
+            sts1(sp + 4u * (L.P_G + i), (e.ln_g && i < N) ? e.ln_g[i] : 0.f);
+            sts1(sp + 4u * (L.P_B + i), (e.ln_b && i < N) ? e.ln_b[i] : 0.f);
+        }
+    }
+    if constexpr (MODE == EPI_L2NORM || MODE == EPI_HEAD) {
+        const float* w = MODE == EPI_HEAD ? e.w2 : e.mod_w;
+        const float* b = MODE == EPI_HEAD ? e.b2 : e.mod_b;
+        for (int i = tid; i < 3 * L.npad + 3; i += nthreads) {
+            float x = 0.f;
+            if (w && i < 3 * N) x = w[i];
+            if (b && i >= 3 * L.npad) x = b[i - 3 * L.npad];
+            sts1(sp + 4u * (L.P_W + i), x);
+        }
     }
 }
 
 template <int BN, int MODE>
-__device__ __forceinline__ void epilogue(const Epi& e, uint32_t tbase, int row, bool live, int n0, int nvalid) {
-    constexpr int CH = (BN + 31) / 32;
-    float v[32];
+__device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, uint32_t st, uint32_t red, uint32_t sp,
+                                              int q, int cg, int lane, int m0, int n0, int M, int N, int nvalid) {
+    using C = Cfg<BN>;
+    const ParamLayout PL = param_layout(N);
+    const int row_base = m0 + q * 32;
+    const int row = row_base + lane;
+    const bool live = row < M;
+    const int col_lo = cg * C::CPW;
+    float v[32], p[32];
     if constexpr (MODE == EPI_BIAS) {
 #pragma unroll 1
-        for (int ch = 0; ch < CH; ch++) {
-            int c0 = ch * 32;
-            if (c0 >= nvalid) break;
-            tmem_load32(tbase + c0, v);
-            int nc = min(32, nvalid - c0);
-            float b[32];
-            load_f32_32(e.bias + n0 + c0, b, nc);
+        for (int ch = 0; ch < C::CHUNKS; ch++) {
+            const int c = col_lo + ch * 32;
+            if (c >= nvalid) break;
+            const int nc = min(32, nvalid - c);
+            tmem_load32(tacc + c, v);
+            lds32(sp, n0 + c, p);
+            if (e.act) {
 #pragma unroll
-            for (int i = 0; i < 32; i++) {
-                float x = v[i] + b[i];
-                v[i] = e.act ? gelu_tanh(x) : x;
-            }
-            if (!live) continue;
-            int g0 = n0 + c0;
-            int seg = g0 / e.seg_cols;
-            int lc = g0 - seg * e.seg_cols;
-            if (lc + nc <= e.seg_cols) {
-                bf16* dst = static_cast<bf16*>(e.out[seg]) + static_cast<size_t>(row) * e.out_ld[seg] + lc;
-                store_bf16_32(dst, v, nc);
+                for (int i = 0; i < 32; i++) v[i] = gelu_fast(v[i] + p[i]);
             } else {
+#pragma unroll
+                for (int i = 0; i < 32; i++) v[i] += p[i];
+            }
+            const int g0 = n0 + c;
+            const int seg = g0 / e.seg_cols;
+            const int lc = g0 - seg * e.seg_cols;
+            if (lc + nc <= e.seg_cols) {
+                store_bf16_block(st, v, static_cast<bf16*>(e.out[seg]) + lc, e.out_ld[seg], row_base, M, nc, lane);
+            } else if (live) {
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
                     if (i >= nc) continue;
@@ -150,151 +323,153 @@ __device__ __forceinline__ void epilogue(const Epi& e, uint32_t tbase, int row, 
             }
         }
     } else if constexpr (MODE == EPI_HEAD) {
-        float lg0 = 0.f, lg1 = 0.f, lg2 = 0.f;
+        float lg[3] = {0.f, 0.f, 0.f};
 #pragma unroll 1
-        for (int ch = 0; ch < CH; ch++) {
-            int c0 = ch * 32;
-            if (c0 >= nvalid) break;
-            tmem_load32(tbase + c0, v);
-            int nc = min(32, nvalid - c0);
+        for (int ch = 0; ch < C::CHUNKS; ch++) {
+            const int c = col_lo + ch * 32;
+            if (c >= nvalid) break;
+            tmem_load32(tacc + c, v);
+            lds32(sp, c, p);
 #pragma unroll
             for (int i = 0; i < 32; i++) {
-                if (i >= nc) continue;
-                float z = gelu_tanh(v[i] + __ldg(e.bias + c0 + i));
-                const float* w = e.w2 + (c0 + i) * 3;
-                lg0 += z * __ldg(w);
-                lg1 += z * __ldg(w + 1);
-                lg2 += z * __ldg(w + 2);
+                float z = gelu_fast(v[i] + p[i]);  // padded columns: acc 0, bias 0 -> z = 0
+                const uint32_t w = sp + 4u * (PL.P_W + (c + i) * 3);
+                lg[0] += z * lds1(w);
+                lg[1] += z * lds1(w + 4);
+                lg[2] += z * lds1(w + 8);
             }
         }
-        if (live) {
-            e.logits[static_cast<size_t>(row) * 3 + 0] = lg0 + e.b2[0];
-            e.logits[static_cast<size_t>(row) * 3 + 1] = lg1 + e.b2[1];
-            e.logits[static_cast<size_t>(row) * 3 + 2] = lg2 + e.b2[2];
+        quad_reduce<C::CG, 3>(red, lg, cg, lane, q);
+        if (live && cg == 0) {
+            const uint32_t b = sp + 4u * (PL.P_W + 3 * PL.npad);
+            float* o = e.logits + static_cast<size_t>(row) * 3;
+            o[0] = lg[0] + lds1(b);
+            o[1] = lg[1] + lds1(b + 4);
+            o[2] = lg[2] + lds1(b + 8);
         }
     } else {
-        // full-row modes: nvalid == N == d, n0 == 0
-        const float d = static_cast<float>(nvalid);
-        float s1 = 0.f;
-        bool bad = false;
+        // full-row modes: n0 == 0, nvalid == N == d. Padded columns carry zeros
+        // (TMA zero-fill of W, zero params, zero residual) and are masked out of
+        // the centred variance.
+        const float dn = static_cast<float>(nvalid);
+        float s1[1] = {0.f};
         if constexpr (MODE == EPI_RESID_LN) {
+            bool bad = false;
 #pragma unroll 1
-            for (int ch = 0; ch < CH; ch++) {
-                int c0 = ch * 32;
-                if (c0 >= nvalid) break;
-                int nc = min(32, nvalid - c0);
-                tmem_load32(tbase + c0, v);
-                float b[32], r[32];
-                load_f32_32(e.bias + c0, b, nc);
-                if (live) {
-                    load_f32_32(e.resid + static_cast<size_t>(row) * e.ld_x + c0, r, nc);
-                } else {
-                    for (int i = 0; i < 32; i++) r[i] = 0.f;
-                }
+            for (int ch = 0; ch < C::CHUNKS; ch++) {
+                const int c = col_lo + ch * 32;
+                if (c >= nvalid) break;
+                const int nc = min(32, nvalid - c);
+                load_f32_block(st, e.resid + c, e.ld_x, row_base, M, nc, lane, p);
+                tmem_load32(tacc + c, v);
+#pragma unroll
+                for (int i = 0; i < 32; i++) p[i] += v[i];
+                lds32(sp, c, v);
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
-                    v[i] = v[i] + b[i] + r[i];
-                    if (i < nc) {
-                        bad |= !isfinite(v[i]);
-                        s1 += v[i];
-                    }
+                    v[i] = p[i] + v[i];  // (acc + resid) + bias == x2 + o (fp32 add, commutative)
+                    bad |= !isfinite(v[i]);
+                    s1[0] += v[i];
                 }
-                if (live) store_f32_32(e.x_out + static_cast<size_t>(row) * e.ld_x + c0, v, nc);
-                tmem_store32(tbase + c0, v);
+                store_f32_block(st, v, e.x_out + c, e.ld_x, row_base, M, nc, lane);
+                if (e.ln_g == nullptr && e.ln_out)
+                    store_bf16_block(st, v, static_cast<bf16*>(e.ln_out) + c, e.ln_ld, row_base, M, nc, lane);
+                tmem_store32(tacc + c, v);
             }
             if (live && bad && e.layer_idx >= 0) atomicMax(&e.st->nonfinite_layer, e.layer_idx + 1);
         } else {  // EPI_L2NORM
-            float ss = 0.f;
+            float ss[1] = {0.f};
 #pragma unroll 1
-            for (int ch = 0; ch < CH; ch++) {
-                int c0 = ch * 32;
-                if (c0 >= nvalid) break;
-                int nc = min(32, nvalid - c0);
-                tmem_load32(tbase + c0, v);
-                float b[32];
-                load_f32_32(e.bias + c0, b, nc);
+            for (int ch = 0; ch < C::CHUNKS; ch++) {
+                const int c = col_lo + ch * 32;
+                if (c >= nvalid) break;
+                tmem_load32(tacc + c, v);
+                lds32(sp, c, p);
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
-                    v[i] += b[i];
-                    if (i < nc) ss += v[i] * v[i];
+                    v[i] += p[i];
+                    ss[0] += v[i] * v[i];
                 }
-                tmem_store32(tbase + c0, v);
+                tmem_store32(tacc + c, v);
             }
-            float nrm = sqrtf(ss);
-            float inv = 1.0f / (nrm < 1e-12f ? 1e-12f : nrm);
-            float ml0 = 0.f, ml1 = 0.f, ml2 = 0.f;
+            quad_reduce<C::CG, 1>(red, ss, cg, lane, q);
+            const float nrm = sqrtf(ss[0]);
+            const float inv = 1.0f / (nrm < 1e-12f ? 1e-12f : nrm);
+            float ml[3] = {0.f, 0.f, 0.f};
 #pragma unroll 1
-            for (int ch = 0; ch < CH; ch++) {
-                int c0 = ch * 32;
-                if (c0 >= nvalid) break;
-                int nc = min(32, nvalid - c0);
-                tmem_load32(tbase + c0, v);
+            for (int ch = 0; ch < C::CHUNKS; ch++) {
+                const int c = col_lo + ch * 32;
+                if (c >= nvalid) break;
+                const int nc = min(32, nvalid - c);
+                tmem_load32(tacc + c, v);
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
                     v[i] *= inv;
-                    if (i < nc) s1 += v[i];
+                    s1[0] += v[i];
                 }
                 if (e.mod_w) {
 #pragma unroll
                     for (int i = 0; i < 32; i++) {
-                        if (i >= nc) continue;
-                        const float* w = e.mod_w + (c0 + i) * 3;
-                        ml0 += v[i] * __ldg(w);
-                        ml1 += v[i] * __ldg(w + 1);
-                        ml2 += v[i] * __ldg(w + 2);
+                        const uint32_t w = sp + 4u * (PL.P_W + (c + i) * 3);
+                        ml[0] += v[i] * lds1(w);
+                        ml[1] += v[i] * lds1(w + 4);
+                        ml[2] += v[i] * lds1(w + 8);
                     }
                 }
-                if (live) {
-                    if (e.x_out) store_f32_32(e.x_out + static_cast<size_t>(row) * e.ld_x + c0, v, nc);
-                    if (e.out2)
-                        store_bf16_32(static_cast<bf16*>(e.out2) + static_cast<size_t>(row) * e.out2_ld + c0, v, nc);
-                }
-                tmem_store32(tbase + c0, v);
+                if (e.x_out) store_f32_block(st, v, e.x_out + c, e.ld_x, row_base, M, nc, lane);
+                if (e.out2) store_bf16_block(st, v, static_cast<bf16*>(e.out2) + c, e.out2_ld, row_base, M, nc, lane);
+                if (e.ln_g == nullptr && e.ln_out)
+                    store_bf16_block(st, v, static_cast<bf16*>(e.ln_out) + c, e.ln_ld, row_base, M, nc, lane);
+                tmem_store32(tacc + c, v);
             }
-            if (live && e.mod_w) {
-                e.mlogits[static_cast<size_t>(row) * 3 + 0] = ml0 + e.mod_b[0];
-                e.mlogits[static_cast<size_t>(row) * 3 + 1] = ml1 + e.mod_b[1];
-                e.mlogits[static_cast<size_t>(row) * 3 + 2] = ml2 + e.mod_b[2];
-            }
-        }
-        if (e.ln_out == nullptr) return;
-        float mu = s1 / d;
-        float var = 0.f;
-        if (e.ln_g) {
-#pragma unroll 1
-            for (int ch = 0; ch < CH; ch++) {
-                int c0 = ch * 32;
-                if (c0 >= nvalid) break;
-                int nc = min(32, nvalid - c0);
-                tmem_load32(tbase + c0, v);
-#pragma unroll
-                for (int i = 0; i < 32; i++) {
-                    float c = v[i] - mu;
-                    if (i < nc) var += c * c;
+            if (e.mod_w) {
+                quad_reduce<C::CG, 3>(red, ml, cg, lane, q);
+                if (live && cg == 0) {
+                    const uint32_t b = sp + 4u * (PL.P_W + 3 * PL.npad);
+                    float* o = e.mlogits + static_cast<size_t>(row) * 3;
+                    o[0] = ml[0] + lds1(b);
+                    o[1] = ml[1] + lds1(b + 4);
+                    o[2] = ml[2] + lds1(b + 8);
                 }
             }
         }
-        float rs = 1.0f / sqrtf(var / d + 1e-5f);
+        if (e.ln_out == nullptr || e.ln_g == nullptr) return;
+        quad_reduce<C::CG, 1>(red, s1, cg, lane, q);
+        const float mu = s1[0] / dn;
+        float var[1] = {0.f};
 #pragma unroll 1
-        for (int ch = 0; ch < CH; ch++) {
-            int c0 = ch * 32;
-            if (c0 >= nvalid) break;
-            int nc = min(32, nvalid - c0);
-            tmem_load32(tbase + c0, v);
-            if (e.ln_g) {
-                float g[32], bb[32];
-                load_f32_32(e.ln_g + c0, g, nc);
-                load_f32_32(e.ln_b + c0, bb, nc);
+        for (int ch = 0; ch < C::CHUNKS; ch++) {
+            const int c = col_lo + ch * 32;
+            if (c >= nvalid) break;
+            const int nc = min(32, nvalid - c);
+            tmem_load32(tacc + c, v);
 #pragma unroll
-                for (int i = 0; i < 32; i++) v[i] = g[i] * ((v[i] - mu) * rs) + bb[i];
+            for (int i = 0; i < 32; i++) {
+                float t = v[i] - mu;
+                var[0] += (i < nc) ? t * t : 0.f;
             }
-            if (live) store_bf16_32(static_cast<bf16*>(e.ln_out) + static_cast<size_t>(row) * e.ln_ld + c0, v, nc);
+        }
+        quad_reduce<C::CG, 1>(red, var, cg, lane, q);
+        const float rs = 1.0f / sqrtf(var[0] / dn + 1e-5f);
+#pragma unroll 1
+        for (int ch = 0; ch < C::CHUNKS; ch++) {
+            const int c = col_lo + ch * 32;
+            if (c >= nvalid) break;
+            const int nc = min(32, nvalid - c);
+            tmem_load32(tacc + c, v);
+            lds32(sp, PL.P_G + c, p);
+#pragma unroll
+            for (int i = 0; i < 32; i++) v[i] = p[i] * ((v[i] - mu) * rs);
+            lds32(sp, PL.P_B + c, p);
+#pragma unroll
+            for (int i = 0; i < 32; i++) v[i] += p[i];
+            store_bf16_block(st, v, static_cast<bf16*>(e.ln_out) + c, e.ln_ld, row_base, M, nc, lane);
         }
     }
 }
 
 template <int BN, int MODE>
-__global__ void __launch_bounds__(256, Cfg<BN>::MIN_BLOCKS)
+__global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
               const __grid_constant__ Epi e) {
     using C = Cfg<BN>;
@@ -302,14 +477,19 @@ __global__ void __launch_bounds__(256, Cfg<BN>::MIN_BLOCKS)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + C::STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + C::STAGES * C::B_BYTES);
+    const uint32_t s_staging = ptx::smem_u32(smem + C::RING);
+    const uint32_t s_red = s_staging + C::STAGING;
+    const uint32_t s_par = s_red + C::RED;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::RING + C::STAGING + C::RED + C::PARAM_FLOATS * 4);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
     const int nk = (K + BK - 1) / BK;
+    const int num_n = (N + BN - 1) / BN;
+    const int tiles = ((M + BM - 1) / BM) * num_n;
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&tmA);
@@ -318,10 +498,14 @@ __global__ void __launch_bounds__(256, Cfg<BN>::MIN_BLOCKS)
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
         }
-        ptx::mbar_init(tfull, 1);
+        for (int b = 0; b < 2; b++) {
+            ptx::mbar_init(&tfull[b], 1);
+            ptx::mbar_init(&tempty[b], C::EPI_WARPS);
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc(tslot, C::TMEM_COLS);
+    if (warp >= 4) load_params<BN, MODE>(e, s_par, N, threadIdx.x - 128, C::EPI_THREADS);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -329,46 +513,66 @@ __global__ void __launch_bounds__(256, Cfg<BN>::MIN_BLOCKS)
 
     if (warp == 0) {
         if (lane == 0) {
-            for (int kb = 0; kb < nk; kb++) {
-                int s = kb % C::STAGES;
-                if (kb >= C::STAGES) ptx::mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
-                ptx::mbar_expect_tx(&full[s], A_BYTES + C::B_BYTES);
-                ptx::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
+            uint32_t it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+                for (int kb = 0; kb < nk; kb++, it++) {
+                    const int s = it % C::STAGES;
+                    ptx::mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+                    ptx::mbar_expect_tx(&full[s], A_BYTES + C::B_BYTES);
+                    ptx::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
 #pragma unroll
-                for (int h = 0; h < C::N_HALVES; h++)
-                    ptx::tma_load_2d(sB + s * C::B_BYTES + h * C::MMA_N * 128, &tmB, &full[s], kb * BK,
-                                     n0 + h * C::MMA_N);
+                    for (int h = 0; h < C::N_HALVES; h++)
+                        ptx::tma_load_2d(sB + s * C::B_BYTES + h * C::MMA_N * 128, &tmB, &full[s], kb * BK,
+                                         n0 + h * C::MMA_N);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16(BM, C::MMA_N);
-            for (int kb = 0; kb < nk; kb++) {
-                int s = kb % C::STAGES;
-                ptx::mbar_wait(&full[s], (kb / C::STAGES) & 1);
+            uint32_t it = 0, i = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
+                const int buf = i % C::ACC_BUFS;
+                ptx::mbar_wait(&tempty[buf], ((i / C::ACC_BUFS) & 1) ^ 1);
                 ptx::tc_fence_after();
-                uint32_t a_base = ptx::smem_u32(sA + s * A_BYTES);
-                uint32_t b_base = ptx::smem_u32(sB + s * C::B_BYTES);
+                const uint32_t tacc = tmem + buf * BN;
+                for (int kb = 0; kb < nk; kb++, it++) {
+                    const int s = it % C::STAGES;
+                    ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+                    ptx::tc_fence_after();
+                    const uint32_t a_base = ptx::smem_u32(sA + s * A_BYTES);
+                    const uint32_t b_base = ptx::smem_u32(sB + s * C::B_BYTES);
 #pragma unroll
-                for (int k = 0; k < BK / 16; k++) {
-                    uint64_t ad = ptx::sdesc_sw128(a_base + k * 32);
+                    for (int k = 0; k < BK / 16; k++) {
+                        const uint64_t ad = ptx::sdesc_sw128(a_base + k * 32);
 #pragma unroll
-                    for (int h = 0; h < C::N_HALVES; h++) {
-                        uint64_t bd = ptx::sdesc_sw128(b_base + h * C::MMA_N * 128 + k * 32);
-                        ptx::mma_bf16(tmem + h * C::MMA_N, ad, bd, idesc, (kb | k) != 0);
+                        for (int h = 0; h < C::N_HALVES; h++) {
+                            const uint64_t bd = ptx::sdesc_sw128(b_base + h * C::MMA_N * 128 + k * 32);
+                            ptx::mma_bf16(tacc + h * C::MMA_N, ad, bd, idesc, (kb | k) != 0);
+                        }
                     }
+                    ptx::mma_commit(&empty[s]);
                 }
-                ptx::mma_commit(&empty[s]);
+                ptx::mma_commit(&tfull[buf]);
             }
-            ptx::mma_commit(tfull);
         }
     } else if (warp >= 4) {
-        ptx::mbar_wait(tfull, 0);
-        ptx::tc_fence_after();
-        const int q = warp & 3;
-        const int row = m0 + q * 32 + lane;
-        const int nvalid = min(BN, N - n0);
-        epilogue<BN, MODE>(e, tmem + (static_cast<uint32_t>(q * 32) << 16), row, row < M, n0, nvalid);
+        const int ew = warp - 4;
+        const int q = warp & 3, cg = ew >> 2;
+        const uint32_t st = s_staging + 4u * (ew * 32 * SROW);
+        uint32_t i = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
+            const int buf = i % C::ACC_BUFS;
+            ptx::mbar_wait(&tfull[buf], (i / C::ACC_BUFS) & 1);
+            ptx::tc_fence_after();
+            const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+            const uint32_t tacc = tmem + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
+            epilogue_tile<BN, MODE>(e, tacc, st, s_red, s_par, q, cg, lane, m0, n0, M, N, min(BN, N - n0));
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[buf]);
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -413,16 +617,30 @@ CUtensorMap tmap_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t
     return m;
 }
 
+int num_sms() {
+    static int n = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    });
+    return n;
+}
+
 template <int BN, int MODE>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e, cudaStream_t s) {
     using C = Cfg<BN>;
+    static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
     static std::once_flag once;
     std::call_once(once, [] {
         DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tc<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM));
     });
-    dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
-    k_gemm_tc<BN, MODE><<<grid, 256, C::SMEM, s>>>(ta, tb, M, N, K, e);
+    int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    int grid = tiles < num_sms() ? tiles : num_sms();
+    k_gemm_tc<BN, MODE><<<grid, C::THREADS, C::SMEM, s>>>(ta, tb, M, N, K, e);
     DCAT_LAUNCH_CHECK();
 }
 
