@@ -35,6 +35,7 @@
 // fixed order (deterministic).
 #include <cuda.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "launch.h"
@@ -47,11 +48,22 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int SROW = 36;  // staging row pitch (floats): 16B-aligned rows, conflict-free v4 transposes
+// Epilogue tiles are 32 rows x 32 columns per warp-chunk, moved by TMA:
+//   fp32 blocks (residual in, x out): 32 x 128 B rows, 128-byte swizzle (1 KB atoms)
+//   bf16 blocks (activations out):    32 x  64 B rows,  64-byte swizzle
+// One row per lane; the swizzles make every lane's 16-byte shared access
+// bank-conflict free within a quarter warp.
+constexpr int F_BYTES = 32 * 32 * 4;
+constexpr int H_BYTES = 32 * 32 * 2;
 
-template <int BN>
+struct EpiMaps {
+    CUtensorMap resid, xout, ln, o[3], out2;
+};
+
+template <int BN, int MODE>
 struct Cfg {
-    static constexpr int CG = BN == 64 ? 2 : BN == 512 ? 2 : 4;  // epilogue warps per lane quadrant
+    static constexpr bool FULL = MODE == EPI_RESID_LN || MODE == EPI_L2NORM;
+    static constexpr int CG = BN == 64 ? 2 : (FULL ? (BN == 512 ? 1 : 2) : 4);  // epilogue warps per lane quadrant
     static constexpr int EPI_WARPS = 4 * CG;
     static constexpr int EPI_THREADS = 32 * EPI_WARPS;
     static constexpr int THREADS = 128 + EPI_THREADS;
@@ -61,13 +73,14 @@ struct Cfg {
     static constexpr int N_HALVES = BN / MMA_N;
     static constexpr int ACC_BUFS = BN <= 256 ? 2 : 1;
     static constexpr int TMEM_COLS = BN * ACC_BUFS < 32 ? 32 : BN * ACC_BUFS;
-    static constexpr int STAGES = BN == 64 ? 6 : BN == 128 ? 4 : 2;
+    static constexpr int STAGES = BN == 64 ? (FULL ? 4 : 6) : BN == 128 ? (FULL ? 3 : 4) : BN == 256 ? (FULL ? 2 : 3) : 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int RING = STAGES * (A_BYTES + B_BYTES);
-    static constexpr int STAGING = EPI_WARPS * 32 * SROW * 4;
-    static constexpr int RED = 4 * 3 * CG * 32 * 4;          // [quadrant][value][cg][lane]
-    static constexpr int PARAM_FLOATS = BN == 512 ? 3104 : 1600;  // bias | ln_g | ln_b | mod_w/w2 | mod_b/b2
-    static constexpr int SMEM = RING + STAGING + RED + PARAM_FLOATS * 4 + 1024 + 256;
+    static constexpr int EW = FULL ? 2 * F_BYTES + 2 * H_BYTES : (MODE == EPI_BIAS ? 2 * H_BYTES : 0);  // per warp
+    static constexpr int EPI_SMEM = EW * EPI_WARPS;
+    static constexpr int RED = 4 * 3 * CG * 32 * 4;  // [quadrant][value][cg][lane]
+    static constexpr int PARAM_FLOATS = BN == 512 ? 3088 : 1600;  // bias | ln_g | ln_b | mod_w/w2 | mod_b/b2
+    static constexpr int SMEM = RING + EPI_SMEM + RED + PARAM_FLOATS * 4 + 1024 + 512;
 };
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -78,6 +91,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void sts4(uint32_t a, float x, float y, float z, float w) {
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(x), "f"(y), "f"(z), "f"(w) : "memory");
+}
+__device__ __forceinline__ void sts4u(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
 }
 __device__ __forceinline__ float4 lds4(uint32_t a) {
     float4 v;
@@ -93,6 +109,35 @@ __device__ __forceinline__ float lds1(uint32_t a) {
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
     return v;
 }
+// ---- TMA store / bulk groups (per issuing thread)
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, uint32_t src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(src), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_s(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+            "r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_s(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+    while (!ptx::mbar_try_wait(bar, parity)) {
+    }
+}
+
 __device__ __forceinline__ float tanh_fast(float x) {
     float y;
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -132,105 +177,50 @@ __device__ __forceinline__ void lds32(uint32_t sp, int p, float* out) {
     }
 }
 
-// ---- warp-cooperative, row-contiguous global I/O of a 32 x 32 block through
-// this warp's smem staging tile `st` (shared address). `v` holds this lane's
-// row (row_base + lane), block columns [0, nc).
-
-__device__ __forceinline__ void put_stage(uint32_t st, const float* v, int lane) {
+// this lane's row of a swizzled fp32 block <-> registers
+__device__ __forceinline__ void read_f32_row(uint32_t buf, int lane, float* v) {
 #pragma unroll
-    for (int i = 0; i < 32; i += 4) sts4(st + 4u * (lane * SROW + i), v[i], v[i + 1], v[i + 2], v[i + 3]);
-    __syncwarp();
+    for (int j = 0; j < 8; j++) {
+        float4 t = lds4(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
+        v[4 * j] = t.x;
+        v[4 * j + 1] = t.y;
+        v[4 * j + 2] = t.z;
+        v[4 * j + 3] = t.w;
+    }
+}
+__device__ __forceinline__ void write_f32_row(uint32_t buf, int lane, const float* v) {
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+        sts4(buf + lane * 128 + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+}
+__device__ __forceinline__ void write_bf16_row(uint32_t buf, int lane, const float* v) {
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+        sts4u(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4), pack_bf16(v[8 * j], v[8 * j + 1]),
+              pack_bf16(v[8 * j + 2], v[8 * j + 3]), pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+              pack_bf16(v[8 * j + 6], v[8 * j + 7]));
 }
 
-__device__ __forceinline__ void store_bf16_block(uint32_t st, const float* v, bf16* base, size_t ld, int row_base,
-                                                 int M, int nc, int lane) {
-    put_stage(st, v, lane);
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const int idx = lane + 32 * k, r = idx >> 2, c = (idx & 3) * 8;
-        const int gr = row_base + r;
-        if (gr < M && c < nc) {
-            float4 a = lds4(st + 4u * (r * SROW + c));
-            float4 b = lds4(st + 4u * (r * SROW + c + 4));
-            bf16* dst = base + static_cast<size_t>(gr) * ld + c;
-            if (c + 8 <= nc && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-                uint4 p;
-                p.x = pack_bf16(a.x, a.y);
-                p.y = pack_bf16(a.z, a.w);
-                p.z = pack_bf16(b.x, b.y);
-                p.w = pack_bf16(b.z, b.w);
-                *reinterpret_cast<uint4*>(dst) = p;
-            } else {
-                float t[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-                for (int j = 0; j < 8; j++)
-                    if (c + j < nc) dst[j] = __float2bfloat16_rn(t[j]);
-            }
-        }
-    }
+// publish this warp's staged block to the async proxy and TMA-store it (lane 0)
+__device__ __forceinline__ void store_block(const CUtensorMap* m, uint32_t buf, int col, int row, int lane) {
+    fence_async_smem();
     __syncwarp();
+    if (lane == 0) {
+        tma_store_2d(m, buf, col, row);
+        bulk_commit();
+    }
 }
-
-__device__ __forceinline__ void store_f32_block(uint32_t st, const float* v, float* base, size_t ld, int row_base,
-                                                int M, int nc, int lane) {
-    put_stage(st, v, lane);
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        const int idx = lane + 32 * k, r = idx >> 3, c = (idx & 7) * 4;
-        const int gr = row_base + r;
-        if (gr < M && c < nc) {
-            float4 a = lds4(st + 4u * (r * SROW + c));
-            float* dst = base + static_cast<size_t>(gr) * ld + c;
-            if (c + 4 <= nc && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-                *reinterpret_cast<float4*>(dst) = a;
-            } else {
-                float t[4] = {a.x, a.y, a.z, a.w};
-#pragma unroll
-                for (int j = 0; j < 4; j++)
-                    if (c + j < nc) dst[j] = t[j];
-            }
-        }
-    }
-    __syncwarp();
-}
-
-// rows [row_base, row_base+32) x cols [0, nc) of a fp32 matrix -> out (this lane's row)
-__device__ __forceinline__ void load_f32_block(uint32_t st, const float* base, size_t ld, int row_base, int M, int nc,
-                                               int lane, float* out) {
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-        const int idx = lane + 32 * k, r = idx >> 3, c = (idx & 7) * 4;
-        const int gr = row_base + r;
-        float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gr < M && c < nc) {
-            const float* src = base + static_cast<size_t>(gr) * ld + c;
-            if (c + 4 <= nc && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-                x = *reinterpret_cast<const float4*>(src);  // may alias x_out (in place): coherent load
-            } else {
-                float t[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-                for (int j = 0; j < 4; j++)
-                    if (c + j < nc) t[j] = src[j];
-                x = make_float4(t[0], t[1], t[2], t[3]);
-            }
-        }
-        sts4(st + 4u * (r * SROW + c), x.x, x.y, x.z, x.w);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-        float4 t = lds4(st + 4u * (lane * SROW + i));
-        out[i] = t.x;
-        out[i + 1] = t.y;
-        out[i + 2] = t.z;
-        out[i + 3] = t.w;
-    }
+// before re-filling a staging buffer: wait until at most N of this lane-0's stores still read smem
+template <int N>
+__device__ __forceinline__ void staging_free(int lane) {
+    if (lane == 0) bulk_wait_read<N>();
     __syncwarp();
 }
 
 // sum of NV per-row partials over the CG warps of one lane quadrant (fixed order)
 template <int CG, int NV>
 __device__ __forceinline__ void quad_reduce(uint32_t red, float* vals, int cg, int lane, int q) {
+    if constexpr (CG == 1) return;
     const uint32_t r = red + 4u * (q * 3 * CG * 32);
 #pragma unroll
     for (int k = 0; k < NV; k++) sts1(r + 4u * ((k * CG + cg) * 32 + lane), vals[k]);
@@ -260,7 +250,7 @@ __device__ __forceinline__ ParamLayout param_layout(int N) {
     return L;
 }
 
-template <int BN, int MODE>
+template <int MODE>
 __device__ void load_params(const Epi& e, uint32_t sp, int N, int tid, int nthreads) {
     const ParamLayout L = param_layout(N);
     for (int i = tid; i < L.npad; i += nthreads) sts1(sp + 4u * i, i < N ? e.bias[i] : 0.f);
@@ -282,10 +272,20 @@ __device__ void load_params(const Epi& e, uint32_t sp, int N, int tid, int nthre
     }
 }
 
+// Per-warp epilogue state kept across tiles (prefetch pipeline of residual blocks).
+struct EpiWarp {
+    uint32_t ew;       // staging region of this warp
+    uint32_t rbar;     // 2 mbarriers for residual blocks
+    uint32_t rph;      // phase bits of the two residual barriers
+    uint32_t gc;       // residual blocks consumed so far (slot = gc & 1)
+    uint32_t hb;       // next bf16 staging buffer (alternates on every bf16 store)
+};
+
 template <int BN, int MODE>
-__device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, uint32_t st, uint32_t red, uint32_t sp,
-                                              int q, int cg, int lane, int m0, int n0, int M, int N, int nvalid) {
-    using C = Cfg<BN>;
+__device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, uint32_t tacc, EpiWarp& W,
+                                              uint32_t red, uint32_t sp, int q, int cg, int lane, int m0, int n0,
+                                              int M, int N, int nvalid, int t, int tiles) {
+    using C = Cfg<BN, MODE>;
     const ParamLayout PL = param_layout(N);
     const int row_base = m0 + q * 32;
     const int row = row_base + lane;
@@ -293,6 +293,7 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, uint3
     const int col_lo = cg * C::CPW;
     float v[32], p[32];
     if constexpr (MODE == EPI_BIAS) {
+        const bool tma_ok = (e.seg_cols % 32) == 0;
 #pragma unroll 1
         for (int ch = 0; ch < C::CHUNKS; ch++) {
             const int c = col_lo + ch * 32;
@@ -309,9 +310,12 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, uint3
             }
             const int g0 = n0 + c;
             const int seg = g0 / e.seg_cols;
-            const int lc = g0 - seg * e.seg_cols;
-            if (lc + nc <= e.seg_cols) {
-                store_bf16_block(st, v, static_cast<bf16*>(e.out[seg]) + lc, e.out_ld[seg], row_base, M, nc, lane);
+            if (tma_ok) {
+                const uint32_t buf = W.ew + W.hb * H_BYTES;
+                W.hb ^= 1;
+                staging_free<1>(lane);
+                write_bf16_row(buf, lane, v);
+                store_block(&mp.o[seg], buf, g0 - seg * e.seg_cols, row_base, lane);
             } else if (live) {
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
@@ -348,41 +352,65 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, uint3
             o[2] = lg[2] + lds1(b + 8);
         }
     } else {
-        // full-row modes: n0 == 0, nvalid == N == d. Padded columns carry zeros
-        // (TMA zero-fill of W, zero params, zero residual) and are masked out of
-        // the centred variance.
+        // full-row modes: n0 == 0, nvalid == N == d. Columns past d carry zeros
+        // (TMA zero fill of W and of the residual, zero params) and are masked
+        // out of the centred variance.
+        const uint32_t F0 = W.ew, H0 = W.ew + 2 * F_BYTES;
         const float dn = static_cast<float>(nvalid);
+        int nchunks = 0;
+#pragma unroll 1
+        for (int ch = 0; ch < C::CHUNKS; ch++)
+            if (col_lo + ch * 32 < nvalid) nchunks++;
         float s1[1] = {0.f};
         if constexpr (MODE == EPI_RESID_LN) {
             bool bad = false;
 #pragma unroll 1
-            for (int ch = 0; ch < C::CHUNKS; ch++) {
+            for (int ch = 0; ch < nchunks; ch++) {
                 const int c = col_lo + ch * 32;
-                if (c >= nvalid) break;
-                const int nc = min(32, nvalid - c);
-                load_f32_block(st, e.resid + c, e.ld_x, row_base, M, nc, lane, p);
+                const int b = W.gc & 1;
+                const uint32_t F = F0 + b * F_BYTES;
+                mbar_wait_s(W.rbar + 8 * b, (W.rph >> b) & 1);  // residual block (prefetched)
+                W.rph ^= 1u << b;
+                read_f32_row(F, lane, p);
                 tmem_load32(tacc + c, v);
 #pragma unroll
                 for (int i = 0; i < 32; i++) p[i] += v[i];
                 lds32(sp, c, v);
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
-                    v[i] = p[i] + v[i];  // (acc + resid) + bias == x2 + o (fp32 add, commutative)
+                    v[i] = p[i] + v[i];  // (acc + resid) + bias
                     bad |= !isfinite(v[i]);
                     s1[0] += v[i];
                 }
-                store_f32_block(st, v, e.x_out + c, e.ld_x, row_base, M, nc, lane);
-                if (e.ln_g == nullptr && e.ln_out)
-                    store_bf16_block(st, v, static_cast<bf16*>(e.ln_out) + c, e.ln_ld, row_base, M, nc, lane);
+                __syncwarp();
+                write_f32_row(F, lane, v);  // the residual slot becomes the x_out slot
+                store_block(&mp.xout, F, c, row_base, lane);
+                if (e.ln_g == nullptr && e.ln_out) {
+                    const uint32_t H = H0 + W.hb * H_BYTES;
+                    W.hb ^= 1;
+                    staging_free<1>(lane);
+                    write_bf16_row(H, lane, v);
+                    store_block(&mp.ln, H, c, row_base, lane);
+                }
                 tmem_store32(tacc + c, v);
+                // refill this slot with the residual block two chunks ahead (maybe in a later tile;
+                // full-row GEMMs have one N tile, so tile index -> m0 = tile * BM)
+                const int ahead = (ch + 2) / nchunks;
+                const int ta = t + ahead * static_cast<int>(gridDim.x);
+                if (lane == 0 && ta < tiles) {
+                    bulk_wait_read<0>();  // the x_out store must have read the slot
+                    mbar_expect_tx_s(W.rbar + 8 * b, F_BYTES);
+                    tma_load_s(F, &mp.resid, W.rbar + 8 * b, col_lo + ((ch + 2) % nchunks) * 32, ta * BM + q * 32);
+                }
+                W.gc++;
+                __syncwarp();
             }
             if (live && bad && e.layer_idx >= 0) atomicMax(&e.st->nonfinite_layer, e.layer_idx + 1);
         } else {  // EPI_L2NORM
             float ss[1] = {0.f};
 #pragma unroll 1
-            for (int ch = 0; ch < C::CHUNKS; ch++) {
+            for (int ch = 0; ch < nchunks; ch++) {
                 const int c = col_lo + ch * 32;
-                if (c >= nvalid) break;
                 tmem_load32(tacc + c, v);
                 lds32(sp, c, p);
 #pragma unroll
@@ -397,10 +425,8 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, uint3
             const float inv = 1.0f / (nrm < 1e-12f ? 1e-12f : nrm);
             float ml[3] = {0.f, 0.f, 0.f};
 #pragma unroll 1
-            for (int ch = 0; ch < C::CHUNKS; ch++) {
+            for (int ch = 0; ch < nchunks; ch++) {
                 const int c = col_lo + ch * 32;
-                if (c >= nvalid) break;
-                const int nc = min(32, nvalid - c);
                 tmem_load32(tacc + c, v);
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
@@ -416,10 +442,24 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, uint3
                         ml[2] += v[i] * lds1(w + 8);
                     }
                 }
-                if (e.x_out) store_f32_block(st, v, e.x_out + c, e.ld_x, row_base, M, nc, lane);
-                if (e.out2) store_bf16_block(st, v, static_cast<bf16*>(e.out2) + c, e.out2_ld, row_base, M, nc, lane);
-                if (e.ln_g == nullptr && e.ln_out)
-                    store_bf16_block(st, v, static_cast<bf16*>(e.ln_out) + c, e.ln_ld, row_base, M, nc, lane);
+                if (e.x_out) {
+                    const uint32_t F = F0;
+                    staging_free<0>(lane);
+                    write_f32_row(F, lane, v);
+                    store_block(&mp.xout, F, c, row_base, lane);
+                }
+                if (e.out2) {
+                    const uint32_t H = H0;
+                    staging_free<0>(lane);
+                    write_bf16_row(H, lane, v);
+                    store_block(&mp.out2, H, c, row_base, lane);
+                }
+                if (e.ln_g == nullptr && e.ln_out) {
+                    const uint32_t H = H0 + H_BYTES;
+                    staging_free<0>(lane);
+                    write_bf16_row(H, lane, v);
+                    store_block(&mp.ln, H, c, row_base, lane);
+                }
                 tmem_store32(tacc + c, v);
             }
             if (e.mod_w) {
@@ -438,9 +478,8 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, uint3
         const float mu = s1[0] / dn;
         float var[1] = {0.f};
 #pragma unroll 1
-        for (int ch = 0; ch < C::CHUNKS; ch++) {
+        for (int ch = 0; ch < nchunks; ch++) {
             const int c = col_lo + ch * 32;
-            if (c >= nvalid) break;
             const int nc = min(32, nvalid - c);
             tmem_load32(tacc + c, v);
 #pragma unroll
@@ -452,10 +491,8 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, uint3
         quad_reduce<C::CG, 1>(red, var, cg, lane, q);
         const float rs = 1.0f / sqrtf(var[0] / dn + 1e-5f);
 #pragma unroll 1
-        for (int ch = 0; ch < C::CHUNKS; ch++) {
+        for (int ch = 0; ch < nchunks; ch++) {
             const int c = col_lo + ch * 32;
-            if (c >= nvalid) break;
-            const int nc = min(32, nvalid - c);
             tmem_load32(tacc + c, v);
             lds32(sp, PL.P_G + c, p);
 #pragma unroll
@@ -463,28 +500,33 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, uint32_t tacc, uint3
             lds32(sp, PL.P_B + c, p);
 #pragma unroll
             for (int i = 0; i < 32; i++) v[i] += p[i];
-            store_bf16_block(st, v, static_cast<bf16*>(e.ln_out) + c, e.ln_ld, row_base, M, nc, lane);
+            const uint32_t H = H0 + W.hb * H_BYTES;
+            W.hb ^= 1;
+            staging_free<1>(lane);
+            write_bf16_row(H, lane, v);
+            store_block(&mp.ln, H, c, row_base, lane);
         }
     }
 }
 
 template <int BN, int MODE>
-__global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-              const __grid_constant__ Epi e) {
-    using C = Cfg<BN>;
+              const __grid_constant__ Epi e, const __grid_constant__ EpiMaps mp) {
+    using C = Cfg<BN, MODE>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + C::STAGES * A_BYTES;
-    const uint32_t s_staging = ptx::smem_u32(smem + C::RING);
-    const uint32_t s_red = s_staging + C::STAGING;
+    const uint32_t s_epi = ptx::smem_u32(smem + C::RING);  // 1 KB aligned (RING is a multiple of 1 KB)
+    const uint32_t s_red = s_epi + C::EPI_SMEM;
     const uint32_t s_par = s_red + C::RED;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::RING + C::STAGING + C::RED + C::PARAM_FLOATS * 4);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::RING + C::EPI_SMEM + C::RED + C::PARAM_FLOATS * 4);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* rbars = tempty + 2;  // 2 per epilogue warp
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(rbars + 2 * C::EPI_WARPS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (K + BK - 1) / BK;
@@ -502,10 +544,11 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
             ptx::mbar_init(&tfull[b], 1);
             ptx::mbar_init(&tempty[b], C::EPI_WARPS);
         }
+        for (int b = 0; b < 2 * C::EPI_WARPS; b++) ptx::mbar_init(&rbars[b], 1);
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc(tslot, C::TMEM_COLS);
-    if (warp >= 4) load_params<BN, MODE>(e, s_par, N, threadIdx.x - 128, C::EPI_THREADS);
+    if (warp >= 4) load_params<MODE>(e, s_par, N, threadIdx.x - 128, C::EPI_THREADS);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -560,19 +603,44 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     } else if (warp >= 4) {
         const int ew = warp - 4;
         const int q = warp & 3, cg = ew >> 2;
-        const uint32_t st = s_staging + 4u * (ew * 32 * SROW);
+        EpiWarp W;
+        W.ew = s_epi + ew * C::EW;
+        W.rbar = ptx::smem_u32(&rbars[2 * ew]);
+        W.rph = 0;
+        W.gc = 0;
+        W.hb = 0;
+        if constexpr (MODE == EPI_RESID_LN) {
+            // prime the residual pipeline: global blocks 0 and 1 of this warp
+            int nck = 0;
+            for (int ch = 0; ch < C::CHUNKS; ch++)
+                if (cg * C::CPW + ch * 32 < N) nck++;
+            if (lane == 0 && nck > 0) {
+                for (int g = 0; g < 2; g++) {
+                    const int ta = blockIdx.x + (g / nck) * gridDim.x;
+                    if (ta < tiles) {
+                        mbar_expect_tx_s(W.rbar + 8 * g, F_BYTES);
+                        tma_load_s(W.ew + g * F_BYTES, &mp.resid, W.rbar + 8 * g, cg * C::CPW + (g % nck) * 32,
+                                   ta * BM + q * 32);
+                    }
+                }
+            }
+            __syncwarp();
+        }
         uint32_t i = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
             const int buf = i % C::ACC_BUFS;
+            const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
             ptx::mbar_wait(&tfull[buf], (i / C::ACC_BUFS) & 1);
             ptx::tc_fence_after();
-            const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
             const uint32_t tacc = tmem + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
-            epilogue_tile<BN, MODE>(e, tacc, st, s_red, s_par, q, cg, lane, m0, n0, M, N, min(BN, N - n0));
+            epilogue_tile<BN, MODE>(e, mp, tacc, W, s_red, s_par, q, cg, lane, m0, n0, M, N, min(BN, N - n0), t,
+                                    tiles);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
         }
+        if (lane == 0) bulk_wait_all();  // smem must stay valid until every store has been read
+        __syncwarp();
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -617,6 +685,43 @@ CUtensorMap tmap_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t
     return m;
 }
 
+// epilogue I/O map: rows x cols matrix (ld elements), 32 x 32 boxes; fp32 -> 128B swizzle, bf16 -> 64B
+CUtensorMap tmap_epi(const void* base, bool f32, uint64_t cols, uint64_t rows, uint64_t ld) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof m);
+    if (!base) return m;
+    const uint64_t es = f32 ? 4 : 2;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {ld * es};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t el[2] = {1, 1};
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * es) & 15))
+        throw CudaError("epilogue tensor map: base / row stride must be 16-byte aligned");
+    CUresult r = encode_fn()(&m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                             const_cast<void*>(base), dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             f32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (epilogue) failed: " + std::to_string(static_cast<int>(r)));
+    return m;
+}
+
+EpiMaps make_maps(const Epi& e, int M, int N) {
+    EpiMaps mp;
+    std::memset(&mp, 0, sizeof mp);
+    const uint64_t rows = static_cast<uint64_t>(M);
+    if (e.mode == EPI_BIAS) {
+        if (e.seg_cols % 32 == 0)
+            for (int s = 0; s < 3 && s * e.seg_cols < N; s++)
+                mp.o[s] = tmap_epi(e.out[s], false, static_cast<uint64_t>(e.seg_cols), rows, e.out_ld[s]);
+    } else if (e.mode == EPI_RESID_LN || e.mode == EPI_L2NORM) {
+        mp.resid = tmap_epi(e.resid, true, static_cast<uint64_t>(N), rows, e.ld_x);
+        mp.xout = tmap_epi(e.x_out, true, static_cast<uint64_t>(N), rows, e.ld_x);
+        mp.ln = tmap_epi(e.ln_out, false, static_cast<uint64_t>(N), rows, e.ln_ld);
+        mp.out2 = tmap_epi(e.out2, false, static_cast<uint64_t>(N), rows, e.out2_ld);
+    }
+    return mp;
+}
+
 int num_sms() {
     static int n = 0;
     static std::once_flag once;
@@ -631,16 +736,17 @@ int num_sms() {
 
 template <int BN, int MODE>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e, cudaStream_t s) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, MODE>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
     static std::once_flag once;
     std::call_once(once, [] {
         DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tc<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM));
     });
+    const EpiMaps mp = make_maps(e, M, N);
     int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
     int grid = tiles < num_sms() ? tiles : num_sms();
-    k_gemm_tc<BN, MODE><<<grid, C::THREADS, C::SMEM, s>>>(ta, tb, M, N, K, e);
+    k_gemm_tc<BN, MODE><<<grid, C::THREADS, C::SMEM, s>>>(ta, tb, M, N, K, e, mp);
     DCAT_LAUNCH_CHECK();
 }
 
