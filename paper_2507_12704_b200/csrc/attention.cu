@@ -8,14 +8,20 @@
 //    here the candidates of one unique are packed as the M dimension of a
 //    query tile (Tile in launch.h), the unique's K/V blocks are staged once per
 //    tile in shared memory and the self key/value enters the online softmax as
-//    a per-row initial state.
+//    a per-row initial state (m = q.k_self, l = 1, o = v_self).
 //
-// bf16 path: flash-style kernel, 4 warps x 16 query rows, 64-key blocks
+// bf16 path: flash-style kernel, WARPS x 16 query rows per CTA, 64-key blocks
 // double-buffered with cp.async, QK^T and PV on mma.sync m16n8k16 (bf16 in,
-// fp32 accumulate), quad-shuffle row max/sum, online rescaling.
-// fp32 path (parity): one warp per (query, head) restating the reference's
-// exact loop order: logits, max, exp-sum, axpy over keys in order.
+// fp32 accumulate). With head dim 32 the kernel is bound by the softmax, not
+// the tensor pipe, so the per-score work is cut to one FFMA + one MUFU.EX2:
+// masks only on partial blocks, row max on raw scores, and the row sums are
+// accumulated by the tensor core (P times a ones column) in the same rescaled
+// accumulators as O.
+// fp32 path (parity) and tiny head dims: one warp per (query, head) restating
+// the reference's exact loop order: logits, max, exp-sum, axpy over keys.
 #include <math.h>
+
+#include <mutex>
 
 #include "launch.h"
 
@@ -23,11 +29,9 @@ namespace dcat {
 
 namespace {
 
-constexpr int BQ = 64;  // queries per CTA (4 warps x 16)
-constexpr int BKV = 64; // keys per block
+constexpr int BKV = 64;  // keys per block
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
-    uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+__device__ __forceinline__ void cp_async16(uint32_t s, const void* gmem, bool pred) {
     int n = pred ? 16 : 0;
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
 }
@@ -36,28 +40,16 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-
-__device__ __forceinline__ void ldsm_x4(uint32_t* r, const void* p) {
-    uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+__device__ __forceinline__ void ldsm_x4(uint32_t* r, uint32_t s) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                  : "r"(s));
 }
-__device__ __forceinline__ void ldsm_x4_t(uint32_t* r, const void* p) {
-    uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+__device__ __forceinline__ void ldsm_x4_t(uint32_t* r, uint32_t s) {
     asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                  : "r"(s));
 }
-__device__ __forceinline__ void ldsm_x2_t(uint32_t* r, const void* p) {
-    uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(p));
-    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(s));
-}
-__device__ __forceinline__ void ldsm_x2(uint32_t* r, const void* p) {
-    uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(p));
-    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(s));
-}
-
 __device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
     asm volatile(
         "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -65,15 +57,32 @@ __device__ __forceinline__ void mma16816(float* d, const uint32_t* a, uint32_t b
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
-template <int DH, bool CAUSAL>
-__global__ void __launch_bounds__(128) k_flash(AttnArgs p) {
-    constexpr int LD = DH + 8;          // padded smem row (bf16), conflict-free ldmatrix
-    constexpr int CHUNKS = DH / 8;      // 16-byte chunks per row
-    constexpr int NT = DH / 8;          // n-tiles of the output
-    __shared__ __align__(16) bf16 sQ[BQ * LD];
-    __shared__ __align__(16) bf16 sK[2][BKV * LD];
-    __shared__ __align__(16) bf16 sV[2][BKV * LD];
+template <int DH, int WARPS>
+struct FlashCfg {
+    static constexpr int BQ = WARPS * 16;
+    static constexpr int LD = DH + 8;  // padded smem row (bf16): conflict-free ldmatrix
+    static constexpr int Q_ELEMS = BQ * LD;
+    static constexpr int KV_ELEMS = BKV * LD;
+    static constexpr int SMEM = (Q_ELEMS + 4 * KV_ELEMS) * 2;
+};
+
+template <int DH, bool CAUSAL, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_flash(AttnArgs p) {
+    using C = FlashCfg<DH, WARPS>;
+    constexpr int LD = C::LD;
+    constexpr int CHUNKS = DH / 8;  // 16-byte chunks per row
+    constexpr int NT = DH / 8;      // n-tiles of the output
+    constexpr int NTHR = WARPS * 32;
+    extern __shared__ __align__(16) bf16 smem_attn[];
+    const uint32_t sQ = static_cast<uint32_t>(__cvta_generic_to_shared(smem_attn));
+    const uint32_t sK0 = sQ + C::Q_ELEMS * 2;
+    const uint32_t sV0 = sK0 + 2 * C::KV_ELEMS * 2;
 
     const Tile tile = p.tiles[blockIdx.x];
     const int h = blockIdx.y;
@@ -84,22 +93,22 @@ __global__ void __launch_bounds__(128) k_flash(AttnArgs p) {
     const bf16* V = static_cast<const bf16*>(p.v);
     const int hc = h * DH;
 
-    // ---- stage Q and the first K/V block
-    for (int i = threadIdx.x; i < BQ * CHUNKS; i += 128) {
+    for (int i = threadIdx.x; i < C::BQ * CHUNKS; i += NTHR) {
         int r = i / CHUNKS, c = i % CHUNKS;
         bool ok = r < tile.nq;
         const bf16* src = Q + static_cast<size_t>(tile.q0 + (ok ? r : 0)) * p.ldq + hc + c * 8;
-        cp_async16(sQ + r * LD + c * 8, src, ok);
+        cp_async16(sQ + 2 * (r * LD + c * 8), src, ok);
     }
     const int nblk = (tile.nkv + BKV - 1) / BKV;
     auto load_kv = [&](int blk, int buf) {
-        for (int i = threadIdx.x; i < BKV * CHUNKS; i += 128) {
+        for (int i = threadIdx.x; i < BKV * CHUNKS; i += NTHR) {
             int r = i / CHUNKS, c = i % CHUNKS;
             int key = blk * BKV + r;
             bool ok = key < tile.nkv;
             size_t off = static_cast<size_t>(tile.kv0 + (ok ? key : 0)) * p.ldkv + hc + c * 8;
-            cp_async16(sK[buf] + r * LD + c * 8, K + off, ok);
-            cp_async16(sV[buf] + r * LD + c * 8, V + off, ok);
+            uint32_t so = 2 * (buf * C::KV_ELEMS + r * LD + c * 8);
+            cp_async16(sK0 + so, K + off, ok);
+            cp_async16(sV0 + so, V + off, ok);
         }
     };
     if (nblk > 0) load_kv(0, 0);
@@ -107,33 +116,36 @@ __global__ void __launch_bounds__(128) k_flash(AttnArgs p) {
 
     const float sl2 = p.scale * 1.4426950408889634f;  // scale * log2(e)
     const int r0 = warp * 16 + g, r1 = r0 + 8;          // tile-local rows of this thread
+    const uint32_t ONES = 0x3F803F80u;                  // bf16x2 (1, 1)
     float o[NT][4];
-    float m0, m1, l0, l1;
+    float lacc[4];  // row sums (every column equal), rescaled with o
+    float m0, m1;   // running row max of the RAW scores
 #pragma unroll
     for (int j = 0; j < NT; j++) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+    lacc[0] = lacc[1] = lacc[2] = lacc[3] = 0.f;
     m0 = m1 = -INFINITY;
-    l0 = l1 = 0.f;
 
     cp_async_wait<0>();
     __syncthreads();
 
     if constexpr (!CAUSAL) {
-        // self term: s = q . k_self, initial state m = s, l = 1, o = v_self
+        // self term: initial state m = q . k_self, l = 1, o = v_self
         const bf16* KS = static_cast<const bf16*>(p.kself);
         const bf16* VS = static_cast<const bf16*>(p.vself);
+        const bf16* sq = smem_attn;
         int q0r = tile.q0 + (r0 < tile.nq ? r0 : 0), q1r = tile.q0 + (r1 < tile.nq ? r1 : 0);
         float d0 = 0.f, d1 = 0.f;
 #pragma unroll
         for (int j = 0; j < NT; j++) {
             int c = j * 8 + 2 * t4;
-            __nv_bfloat162 qa = *reinterpret_cast<const __nv_bfloat162*>(sQ + r0 * LD + c);
-            __nv_bfloat162 qb = *reinterpret_cast<const __nv_bfloat162*>(sQ + r1 * LD + c);
-            __nv_bfloat162 ka = *reinterpret_cast<const __nv_bfloat162*>(KS + static_cast<size_t>(q0r) * p.ldself + hc + c);
-            __nv_bfloat162 kb = *reinterpret_cast<const __nv_bfloat162*>(KS + static_cast<size_t>(q1r) * p.ldself + hc + c);
-            float2 qa2 = __bfloat1622float2(qa), qb2 = __bfloat1622float2(qb);
-            float2 ka2 = __bfloat1622float2(ka), kb2 = __bfloat1622float2(kb);
-            d0 += qa2.x * ka2.x + qa2.y * ka2.y;
-            d1 += qb2.x * kb2.x + qb2.y * kb2.y;
+            float2 qa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sq + r0 * LD + c));
+            float2 qb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(sq + r1 * LD + c));
+            float2 ka = __bfloat1622float2(
+                *reinterpret_cast<const __nv_bfloat162*>(KS + static_cast<size_t>(q0r) * p.ldself + hc + c));
+            float2 kb = __bfloat1622float2(
+                *reinterpret_cast<const __nv_bfloat162*>(KS + static_cast<size_t>(q1r) * p.ldself + hc + c));
+            d0 += qa.x * ka.x + qa.y * ka.y;
+            d1 += qb.x * kb.x + qb.y * kb.y;
             float2 va = __bfloat1622float2(
                 *reinterpret_cast<const __nv_bfloat162*>(VS + static_cast<size_t>(q0r) * p.ldself + hc + c));
             float2 vb = __bfloat1622float2(
@@ -147,9 +159,9 @@ __global__ void __launch_bounds__(128) k_flash(AttnArgs p) {
         d0 += __shfl_xor_sync(0xffffffffu, d0, 2);
         d1 += __shfl_xor_sync(0xffffffffu, d1, 1);
         d1 += __shfl_xor_sync(0xffffffffu, d1, 2);
-        m0 = d0 * sl2;
-        m1 = d1 * sl2;
-        l0 = l1 = (t4 == 0) ? 1.f : 0.f;
+        m0 = d0;
+        m1 = d1;
+        lacc[0] = lacc[1] = lacc[2] = lacc[3] = 1.f;
     }
 
     // Q fragments (A operand), kept in registers for all key blocks
@@ -158,7 +170,7 @@ __global__ void __launch_bounds__(128) k_flash(AttnArgs p) {
     for (int kk = 0; kk < DH / 16; kk++) {
         int row = warp * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
         int col = kk * 16 + 8 * (lane >> 4);
-        ldsm_x4(qf[kk], sQ + row * LD + col);
+        ldsm_x4(qf[kk], sQ + 2 * (row * LD + col));
     }
 
     for (int blk = 0; blk < nblk; blk++) {
@@ -166,11 +178,10 @@ __global__ void __launch_bounds__(128) k_flash(AttnArgs p) {
         if (blk + 1 < nblk) load_kv(blk + 1, buf ^ 1);
         cp_async_commit();
 
-        // S = Q K^T for 64 keys: 8 n-tiles of 8 keys
         float s[8][4];
 #pragma unroll
         for (int j = 0; j < 8; j++) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
-        const bf16* kb = sK[buf];
+        const uint32_t kb = sK0 + 2 * buf * C::KV_ELEMS;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; kk++) {
 #pragma unroll
@@ -178,39 +189,42 @@ __global__ void __launch_bounds__(128) k_flash(AttnArgs p) {
                 uint32_t b[4];
                 int key = 8 * (j + (lane >> 4)) + (lane & 7);
                 int col = kk * 16 + 8 * ((lane >> 3) & 1);
-                ldsm_x4(b, kb + key * LD + col);
+                ldsm_x4(b, kb + 2 * (key * LD + col));
                 mma16816(s[j], qf[kk], b[0], b[1]);
                 mma16816(s[j + 1], qf[kk], b[2], b[3]);
             }
         }
-        // mask + block row max
         const int kbase = blk * BKV;
-        float bm0 = -INFINITY, bm1 = -INFINITY;
+        const bool full = (kbase + BKV <= tile.nkv) && (!CAUSAL || kbase + BKV - 1 <= tile.qloc + warp * 16);
+        if (!full) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    int key = kbase + 8 * j + 2 * t4 + (e & 1);
+                    int row = (e < 2) ? r0 : r1;
+                    bool ok = key < tile.nkv;
+                    if (CAUSAL) ok = ok && key <= tile.qloc + row;
+                    if (!ok) s[j][e] = -INFINITY;
+                }
+            }
+        }
+        float bm0 = s[0][0], bm1 = s[0][2];
 #pragma unroll
         for (int j = 0; j < 8; j++) {
-#pragma unroll
-            for (int e = 0; e < 4; e++) {
-                int key = kbase + 8 * j + 2 * t4 + (e & 1);
-                int row = (e < 2) ? r0 : r1;
-                bool ok = key < tile.nkv;
-                if (CAUSAL) ok = ok && key <= tile.qloc + row;
-                float x = ok ? s[j][e] * sl2 : -INFINITY;
-                s[j][e] = x;
-                if (e < 2) bm0 = fmaxf(bm0, x);
-                else bm1 = fmaxf(bm1, x);
-            }
+            bm0 = fmaxf(bm0, fmaxf(s[j][0], s[j][1]));
+            bm1 = fmaxf(bm1, fmaxf(s[j][2], s[j][3]));
         }
         bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
         bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
         bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
         bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
-        float nm0 = fmaxf(m0, bm0), nm1 = fmaxf(m1, bm1);
-        float u0 = nm0 == -INFINITY ? 0.f : nm0, u1 = nm1 == -INFINITY ? 0.f : nm1;
-        float a0 = exp2f(m0 - u0), a1 = exp2f(m1 - u1);
+        const float nm0 = fmaxf(m0, bm0), nm1 = fmaxf(m1, bm1);
+        const float u0 = nm0 == -INFINITY ? 0.f : -nm0 * sl2;  // exponent offset (scaled)
+        const float u1 = nm1 == -INFINITY ? 0.f : -nm1 * sl2;
+        const float a0 = ex2(fmaf(m0, sl2, u0)), a1 = ex2(fmaf(m1, sl2, u1));  // m = -inf -> 0
         m0 = nm0;
         m1 = nm1;
-        l0 *= a0;
-        l1 *= a1;
 #pragma unroll
         for (int j = 0; j < NT; j++) {
             o[j][0] *= a0;
@@ -218,41 +232,38 @@ __global__ void __launch_bounds__(128) k_flash(AttnArgs p) {
             o[j][2] *= a1;
             o[j][3] *= a1;
         }
+        lacc[0] *= a0;
+        lacc[1] *= a0;
+        lacc[2] *= a1;
+        lacc[3] *= a1;
         uint32_t pf[4][4];
 #pragma unroll
         for (int j = 0; j < 8; j++) {
-            float p0 = exp2f(s[j][0] - u0), p1 = exp2f(s[j][1] - u0);
-            float p2 = exp2f(s[j][2] - u1), p3 = exp2f(s[j][3] - u1);
-            l0 += p0 + p1;
-            l1 += p2 + p3;
+            float p0 = ex2(fmaf(s[j][0], sl2, u0)), p1 = ex2(fmaf(s[j][1], sl2, u0));
+            float p2 = ex2(fmaf(s[j][2], sl2, u1)), p3 = ex2(fmaf(s[j][3], sl2, u1));
             pf[j >> 1][(j & 1) * 2 + 0] = pack_bf16(p0, p1);
             pf[j >> 1][(j & 1) * 2 + 1] = pack_bf16(p2, p3);
         }
-        // O += P V
-        const bf16* vb = sV[buf];
+        // O += P V, l += P 1
+        const uint32_t vb = sV0 + 2 * buf * C::KV_ELEMS;
 #pragma unroll
         for (int kk = 0; kk < 4; kk++) {
-            uint32_t a[4] = {pf[kk][0], pf[kk][1], pf[kk][2], pf[kk][3]};
+            const uint32_t* a = pf[kk];
             int key = kk * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
-            if constexpr (NT >= 2) {
 #pragma unroll
-                for (int j = 0; j < NT; j += 2) {
-                    uint32_t b[4];
-                    ldsm_x4_t(b, vb + key * LD + 8 * (j + (lane >> 4)));
-                    mma16816(o[j], a, b[0], b[1]);
-                    mma16816(o[j + 1], a, b[2], b[3]);
-                }
+            for (int j = 0; j < NT; j += 2) {
+                uint32_t b[4];
+                ldsm_x4_t(b, vb + 2 * (key * LD + 8 * (j + (lane >> 4))));
+                mma16816(o[j], a, b[0], b[1]);
+                mma16816(o[j + 1], a, b[2], b[3]);
             }
+            mma16816(lacc, a, ONES, ONES);
         }
         cp_async_wait<0>();
         __syncthreads();
     }
 
-    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
-    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
-    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
-    float i0 = 1.f / l0, i1 = 1.f / l1;
+    const float i0 = 1.f / lacc[0], i1 = 1.f / lacc[2];
     bf16* O = static_cast<bf16*>(p.out);
 #pragma unroll
     for (int j = 0; j < NT; j++) {
@@ -328,12 +339,24 @@ void launch_simt(const AttnArgs& a, cudaStream_t s) {
     DCAT_LAUNCH_CHECK();
 }
 
+template <int DH, bool CAUSAL, int WARPS>
+void launch_flash_t(const AttnArgs& a, cudaStream_t s) {
+    using C = FlashCfg<DH, WARPS>;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_flash<DH, CAUSAL, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::SMEM));
+    });
+    dim3 grid(a.n_tiles, a.n_heads);
+    k_flash<DH, CAUSAL, WARPS><<<grid, WARPS * 32, C::SMEM, s>>>(a);
+    DCAT_LAUNCH_CHECK();
+}
+
+// context tiles hold 64 queries (causal, 4 warps); crossing tiles 128 (8 warps)
 template <int DH>
 void launch_flash(const AttnArgs& a, cudaStream_t s) {
-    dim3 grid(a.n_tiles, a.n_heads);
-    if (a.causal) k_flash<DH, true><<<grid, 128, 0, s>>>(a);
-    else k_flash<DH, false><<<grid, 128, 0, s>>>(a);
-    DCAT_LAUNCH_CHECK();
+    if (a.causal) launch_flash_t<DH, true, 4>(a, s);
+    else launch_flash_t<DH, false, 8>(a, s);
 }
 
 }  // namespace

@@ -297,7 +297,7 @@ uint64_t debug_hash_mask() {
 }
 
 constexpr int kTileCtx = 64;
-constexpr int kTileCross = 64;
+constexpr int kTileCross = 128;  // crossing tiles: 128 candidate queries of one unique (8 warps)
 
 // dedup + validation; leaves the plan on the device and the counts in m->st_host
 void run_dedup(dcat_model* m, const Staged& sb, const DedupOut& o, cudaStream_t s) {

@@ -1,0 +1,72 @@
+"""World-size-2 gloo test of the multi-GPU host path (paper_2507_12704_b200.sharding):
+user-disjoint sharding of a request batch + the single score gather to rank 0.
+The per-rank scorer here is the CPU oracle (this runs without a GPU); on the B200
+box the same code path runs with the CUDA scorer and NCCL (bench.py --gpus N)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2507_12704_b200.abi import FinetuneSpec, ModelSpec
+from paper_2507_12704_b200.sharding import row_content_hash, shard_rows
+from paper_2507_12704_b200.synth import make_batch
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_path):
+    import torch
+    import torch.distributed as dist
+    from oracle import pyoracle
+    from paper_2507_12704_b200.sharding import gather_scores
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    orc = pyoracle.oracle()
+    spec = ModelSpec(d_model=32, n_layers=2, n_heads=2, mlp_ratio=2, max_len=14, d_emb=16)
+    w = orc.init_weights(spec, 5, table=(2, 64, 8, 3, 0.05), hidden=8)
+    b = make_batch(13, 3, 12, seed=7, ragged=True, shared_storage=False)
+    rows = shard_rows(b, world)
+    ft = FinetuneSpec(max_events=12)
+    logits, mlog, _, _ = orc.rank_forward_batch(w, ft, b.take(rows[rank]))
+    local = torch.from_numpy(np.concatenate([logits, mlog], 1))
+    full = gather_scores(local, rows, b.n_rows)
+    if rank == 0:
+        np.save(out_path, full.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_sharding_is_user_disjoint_and_covers_every_row():
+    b = make_batch(40, 5, 10, seed=3, ragged=True, shared_storage=False, layout="interleaved")
+    h = row_content_hash(b)
+    shards = shard_rows(b, 4)
+    assert sorted(np.concatenate(shards).tolist()) == list(range(b.n_rows))
+    owner = np.empty(b.n_rows, np.int64)
+    for r, s in enumerate(shards):
+        owner[s] = r
+    for v in np.unique(h):
+        assert len(set(owner[h == v])) == 1  # one content -> one rank
+    # equal content hashes equal whatever the storage layout
+    bs = make_batch(40, 5, 10, seed=3, ragged=True, shared_storage=True, layout="interleaved")
+    np.testing.assert_array_equal(row_content_hash(bs), h)
+
+
+def test_world2_gloo_gather_matches_single_process(tmp_path):
+    from oracle import pyoracle
+    out = str(tmp_path / "scores.npy")
+    port = _free_port()
+    mp.start_processes(_worker, args=(2, port, out), nprocs=2, join=True, start_method="spawn")
+    got = np.load(out)
+    orc = pyoracle.oracle()
+    spec = ModelSpec(d_model=32, n_layers=2, n_heads=2, mlp_ratio=2, max_len=14, d_emb=16)
+    w = orc.init_weights(spec, 5, table=(2, 64, 8, 3, 0.05), hidden=8)
+    b = make_batch(13, 3, 12, seed=7, ragged=True, shared_storage=False)
+    logits, mlog, _, _ = orc.rank_forward_batch(w, FinetuneSpec(max_events=12), b)
+    np.testing.assert_array_equal(got, np.concatenate([logits, mlog], 1))
