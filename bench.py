@@ -57,6 +57,24 @@ def gemm_flops(cfg, U, C, L):
     return U * per_user + U * C * per_cand
 
 
+def gemm_bytes(cfg, U, C, L):
+    """Algorithmic HBM bytes of all GEMM launches of one step (bf16 activations,
+    fp32 residual stream): per context token phi_in 1K+2K, per full layer
+    qkv 2K + o 3K + ffn1 2.5K + ffn2 4.5K (d=256 units scale with d), last-layer
+    kv 1.5K; per candidate phi_in 3K, 4 layers x 12K, phi_out 2K, head 1.2K.
+    Written generally: A read + outputs written + residual read/written."""
+    s = cfg["spec"]
+    d, de, nl, F = s.d_model, s.d_emb, s.n_layers, s.d_ff
+    b2, b4 = 2, 4
+    phi_in = (de * b2 + d * b2) + (d * b2 + d * b4 + d * b2)
+    layer = (d * b2 + 3 * d * b2) + (d * b2 + 2 * d * b4 + d * b2) + (d * b2 + F * b2) + (F * b2 + 2 * d * b4 + d * b2)
+    kv = d * b2 + 2 * d * b2
+    kh = (d + de + 8 + 63) // 64 * 64
+    per_user = L * (phi_in + (nl - 1) * layer + kv)
+    per_cand = phi_in + nl * layer + (d * b2 + d * b2) + (d * b2 + d * b2 + 12) + (kh * b2 + 12)
+    return U * per_user + U * C * per_cand
+
+
 def attn_flops(cfg, U, C, L):
     s = cfg["spec"]
     d, nl = s.d_model, s.n_layers
@@ -254,18 +272,22 @@ def run_ours(args, rank, world, local_rank):
     hbm, tf_burst, tf_sus, peak_kind = peaks()
     # dominant kernel class: the tcgen05 GEMMs (all launches of k_gemm_tc)
     gemm_ms = sum(v for n, v in stage_tot.items() if n.startswith("gemm.")) / K
-    gf = gemm_flops(cfg, U, C, L)
+    U_loc = B // C  # unique users of this rank (rank 0 reports)
+    gf = gemm_flops(cfg, U_loc, C, L)
+    gb = gemm_bytes(cfg, U_loc, C, L)
     achieved = gf / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     ctx_f, cross_f = attn_flops(cfg, U, C, L)
     attn_ctx_ms = stage_tot.get("attn.ctx", 0.0) / K
     attn_cross_ms = stage_tot.get("attn.cross", 0.0) / K
     s = spec
     kv_bytes = s.n_layers * 4 * U * L * s.d_model + B * s.n_layers * 8 * s.d_model
+    # measured DRAM bytes (dram__bytes_read + write) of the same GEMM launches from the
+    # committed ncu --set full capture (profiles/), per step of this workload
     traffic = None
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and args.config == "pinfm-base" and U_loc == CONFIGS["pinfm-base"]["U"]:
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_flop_weighted")
+            traffic = json.load(open(tp)).get("dram_bytes_per_step")
         except Exception:
             traffic = None
     stages = {n: round(v / K, 4) for n, v in sorted(stage_tot.items())}
@@ -283,11 +305,18 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": round(B_total / (e2e_ms / K / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms / K, 4)},
         "gpu_launches": int(stats["kernel_launches"]) * K,
-        "roofline": {"bound": "tensor", "kernel": "k_gemm_tc (all tcgen05 GEMM launches of a step)",
-                     "achieved": round(achieved, 1) if achieved else None, "peak": tf_sus, "unit": "TFLOP/s",
-                     "frac": round(achieved / tf_sus, 4) if achieved else None, "peak_kind": f"{peak_kind} sustained",
-                     "traffic": traffic, "gemm_ms_per_step": round(gemm_ms, 4),
-                     "gemm_flops_per_step": gf, "gemm_share_of_step": round(gemm_ms / ms_step, 3)},
+        # dominant kernel class: the tcgen05 GEMMs with fused epilogues. At d=256 their
+        # arithmetic intensity (gf / gb ~ 130 flop/B) is below the B200 ridge
+        # (1348.6 TF/s / 6545.6 GB/s ~ 206 flop/B), so the bound is HBM.
+        "roofline": {"bound": "hbm", "kernel": "k_gemm_tc (all tcgen05 GEMM launches of a step, fused epilogues)",
+                     "achieved": round(gb / (gemm_ms / 1e3) / 1e9, 1) if gemm_ms else None, "peak": hbm,
+                     "unit": "GB/s", "frac": round(gb / (gemm_ms / 1e3) / 1e9 / hbm, 4) if gemm_ms else None,
+                     "peak_kind": f"{peak_kind} copy bandwidth", "traffic": traffic,
+                     "algorithmic_bytes_per_step": gb, "gemm_ms_per_step": round(gemm_ms, 4),
+                     "gemm_share_of_step": round(gemm_ms / ms_step, 3),
+                     "tensor": {"achieved_tflops": round(achieved, 1) if achieved else None, "peak": tf_sus,
+                                "frac": round(achieved / tf_sus, 4) if achieved else None,
+                                "flops_per_step": gf, "intensity_flop_per_byte": round(gf / gb, 1)}},
         "kernels": {
             "attn.ctx": {"ms": round(attn_ctx_ms, 4), "tflops": round(ctx_f / (attn_ctx_ms / 1e3) / 1e12, 1)
                          if attn_ctx_ms else None},

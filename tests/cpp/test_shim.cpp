@@ -1,0 +1,204 @@
+// test_shim.cpp — the drop-in shim against the UNMODIFIED reference, in one binary.
+//
+// Links the reference library (oracle/_ref/libseqfm_ref.so, built from
+// /root/reference/proj/src) and the B200 shim (seqfm::b200, over
+// libdcat_b200.so). Mirrors the reference's own parity tests:
+//   test_finetune.cpp:327-364  rank_forward_batch vs the single scorer (rel 1e-4)
+//   test_dcat.cpp:84-137       dedup plans exact
+//   test_dcat.cpp:215-229      DCAT rows vs naive (1e-4)
+// Exit code 0 = all checks pass. Run by tests/test_gpu_shim.py on the GPU box.
+#include <cmath>
+#include <cstdio>
+#include <stdexcept>
+#include <vector>
+
+#include "seqfm/dcat.hpp"
+#include "seqfm/finetune.hpp"
+#include "../../paper_2507_12704_b200/shim/seqfm_b200.hpp"
+
+using namespace seqfm;
+
+static int failures = 0;
+#define EXPECT(c, ...)                                  \
+    do {                                                \
+        if (!(c)) {                                     \
+            failures++;                                 \
+            std::printf("FAIL %s:%d: ", __FILE__, __LINE__); \
+            std::printf(__VA_ARGS__);                   \
+            std::printf("\n");                          \
+        }                                               \
+    } while (0)
+
+static Segment random_segment(u64 user, int valid, int L, Rng& rng) {
+    Segment s;
+    s.user_id = user;
+    s.valid = valid;
+    s.events.resize(static_cast<size_t>(L));
+    u64 ts = 10000 + rng.uniform_u64(100);
+    for (int i = 0; i < valid; i++) {
+        ts += 1 + rng.uniform_u64(20);
+        Event& e = s.events[static_cast<size_t>(i)];
+        e.timestamp = ts;
+        e.action = static_cast<Action>(rng.uniform_u64(kActionCount));
+        e.surface = static_cast<Surface>(rng.uniform_u64(kSurfaceCount));
+        e.item_id = rng.next_u64() % 100000;
+    }
+    return s;
+}
+
+static std::vector<RankingExample> make_batch(int users, int cands, int L, int d_aux, Rng& rng, bool with_empty) {
+    std::vector<Segment> uniq;
+    for (int u = 0; u < users; u++) {
+        int v = with_empty && u == 0 ? 0 : 1 + static_cast<int>(rng.uniform_u64(static_cast<u64>(L)));
+        uniq.push_back(random_segment(static_cast<u64>(u), v, L, rng));
+    }
+    std::vector<RankingExample> b;
+    for (int i = 0; i < users * cands; i++) {
+        RankingExample ex;
+        ex.seq = uniq[static_cast<size_t>(i % users)];
+        ex.seq.user_id = static_cast<u64>(i);
+        ex.candidate = rng.next_u64() % 100000;
+        ex.age_seconds = rng.uniform(0.0, 60 * 86400.0);
+        for (int k = 0; k < d_aux; k++) ex.aux.push_back(static_cast<float>(rng.normal()));
+        b.push_back(ex);
+    }
+    return b;
+}
+
+static double rel(double a, double b, double scale) { return std::fabs(a - b) / std::max(1e-3, scale); }
+
+static void check_rank(const char* name, const ModelConfig& mc, int L, int users, int cands, FusionVariant v,
+                       bool with_empty) {
+    TransformerParams p;
+    p.init(mc, 51, 0.3f);
+    HashedEmbeddingTable table(4, 64, mc.d_emb / 4, 52);
+    FinetuneConfig cfg;
+    cfg.variant = v;
+    cfg.max_events = L;
+    cfg.crossing_hidden = 8;
+    cfg.d_aux = 4;
+    cfg.validate(mc);
+    RankingHeadParams rp;
+    rp.init(mc.d_model, mc.d_emb, cfg.d_aux, cfg.n_ctx(), cfg.crossing_hidden, cfg.sel_per_example(), 53);
+    Rng ar(5);
+    for (auto& x : rp.aux_proj.v.a) x = 0.3f * static_cast<float>(ar.normal());
+    Rng rng(77);
+    auto batch = make_batch(users, cands, L, v == FusionVariant::Aux ? 4 : 0, rng, with_empty);
+    auto ref = seqfm::rank_forward_batch(p, table, rp, batch, cfg);
+    b200::Scorer sc(p, table, rp);
+    for (int fp32 = 1; fp32 >= 0; fp32--) {
+        sc.set_fp32(fp32 != 0);
+        auto got = sc.rank_forward_batch(batch, cfg);
+        double scale = 0, scale_m = 0, err = 0, err_m = 0;
+        for (auto& r : ref)
+            for (int h = 0; h < 3; h++) {
+                scale = std::max(scale, std::fabs(r.logit[h]));
+                scale_m = std::max(scale_m, std::fabs(r.module_logit[h]));
+            }
+        for (size_t i = 0; i < ref.size(); i++)
+            for (int h = 0; h < 3; h++) {
+                err = std::max(err, rel(got[i].logit[h], ref[i].logit[h], scale));
+                err_m = std::max(err_m, rel(got[i].module_logit[h], ref[i].module_logit[h], scale_m));
+                EXPECT(std::fabs(got[i].prob[h] - 1.0 / (1.0 + std::exp(-got[i].logit[h]))) < 1e-12, "prob");
+            }
+        double tol = fp32 ? 1e-4 : 3e-2;  // test_finetune.cpp:359-361 / bf16 storage
+        std::printf("%-28s %s  max rel err logits %.3e  module %.3e  (tol %.0e)\n", name, fp32 ? "fp32" : "bf16", err,
+                    err_m, tol);
+        EXPECT(err <= tol && err_m <= tol, "%s rank_forward_batch parity", name);
+    }
+}
+
+int main() {
+    // 1. rank_forward_batch parity (test_finetune.cpp:327-364 analogue)
+    ModelConfig tiny;
+    tiny.d_model = 16;
+    tiny.n_layers = 1;
+    tiny.n_heads = 2;
+    tiny.mlp_ratio = 2;
+    tiny.max_len = 8;
+    tiny.d_emb = 8;
+    check_rank("tiny base", tiny, 4, 5, 3, FusionVariant::Base, false);
+    check_rank("tiny aux", tiny, 4, 5, 3, FusionVariant::Aux, false);
+    check_rank("tiny base + empty seq", tiny, 4, 5, 3, FusionVariant::Base, true);
+    ModelConfig base;
+    base.d_model = 256;
+    base.n_layers = 4;
+    base.n_heads = 8;
+    base.max_len = 66;
+    base.d_emb = 256;
+    check_rank("PinFM-base dims, L=64", base, 64, 3, 40, FusionVariant::Base, false);
+
+    // 2. dedup plans (test_dcat.cpp:84-137)
+    Rng rng(3);
+    std::vector<Segment> segs;
+    for (int i = 0; i < 50; i++) segs.push_back(random_segment(static_cast<u64>(i), static_cast<int>(rng.uniform_u64(9)), 8, rng));
+    for (int i = 0; i < 200; i++) {
+        Segment s = segs[static_cast<size_t>(rng.uniform_u64(50))];
+        s.user_id = 1000 + static_cast<u64>(i);
+        if (s.valid < 8) s.events[static_cast<size_t>(s.valid)].item_id = 999999;  // padding is ignored
+        segs.push_back(s);
+    }
+    std::vector<Segment> ur, ub;
+    DedupPlan pr = seqfm::dedup_segments(segs, &ur);
+    DedupPlan pb = b200::dedup_segments(segs, &ub);
+    EXPECT(pr.b_u == pb.b_u && pr.rep == pb.rep && pr.first == pb.first, "dedup plan differs");
+    std::printf("dedup: b=%d b_u=%d (reference %d) %s\n", pb.b, pb.b_u, pr.b_u, pr.rep == pb.rep ? "exact" : "DIFF");
+
+    // 3. DCAT candidate rows vs the reference naive forward (test_dcat.cpp:215-229)
+    for (int layers : {1, 2})
+        for (int heads : {1, 4}) {
+            ModelConfig c;
+            c.d_model = 16;
+            c.n_layers = layers;
+            c.n_heads = heads;
+            c.d_emb = 16;
+            c.max_len = 16;
+            TransformerParams p;
+            p.init(c, static_cast<u64>(100 + layers * 10 + heads));
+            HashedEmbeddingTable table(4, 64, 4, 21);
+            RankingHeadParams rp;
+            rp.init(16, 16, 16, 8, 64, 1, 11);
+            Rng r2(7);
+            auto batch = make_batch(4, 4, 10, 0, r2, false);
+            std::vector<Segment> bs;
+            std::vector<u64> items;
+            for (auto& ex : batch) {
+                bs.push_back(ex.seq);
+                items.push_back(ex.candidate);
+            }
+            Mat naive = naive_candidate_outputs(p, table, bs, items);
+            b200::Scorer sc(p, table, rp);
+            sc.set_fp32(true);
+            FinetuneConfig cfg;
+            cfg.max_events = 10;
+            Mat h = sc.candidate_outputs(batch, cfg);
+            double m = 0;
+            for (size_t i = 0; i < h.a.size(); i++) m = std::max(m, static_cast<double>(std::fabs(h.a[i] - naive.a[i])));
+            std::printf("cross vs naive l%d h%d: max abs %.3e\n", layers, heads, m);
+            EXPECT(m <= 1e-4, "cross vs naive");
+        }
+
+    // 4. errors surface as std::runtime_error (SEQFM_CHECK)
+    {
+        TransformerParams p;
+        p.init(tiny, 1);
+        HashedEmbeddingTable table(4, 64, 2, 2);
+        RankingHeadParams rp;
+        FinetuneConfig cfg;
+        cfg.max_events = 4;
+        cfg.crossing_hidden = 8;
+        rp.init(16, 8, cfg.d_aux, cfg.n_ctx(), 8, 1, 3);
+        Rng r3(9);
+        auto batch = make_batch(2, 2, 4, 0, r3, false);
+        batch[1].seq.events[0].action = static_cast<Action>(9);
+        bool threw = false;
+        try {
+            b200::rank_forward_batch(p, table, rp, batch, cfg);
+        } catch (const std::runtime_error& e) {
+            threw = std::string(e.what()).find("unknown action") != std::string::npos;
+        }
+        EXPECT(threw, "unknown action must throw std::runtime_error");
+    }
+    std::printf(failures ? "FAILED (%d)\n" : "ALL OK\n", failures);
+    return failures ? 1 : 0;
+}
