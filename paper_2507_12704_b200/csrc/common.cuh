@@ -92,7 +92,8 @@ inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b -
     do {                                                                                    \
         cudaError_t e__ = (expr);                                                           \
         if (e__ != cudaSuccess)                                                             \
-            throw ::dcat::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e__));   \
+            throw ::dcat::CudaError(std::string(#expr) + " (" + __FILE__ + ":" + std::to_string(__LINE__) + "): " + \
+                                    cudaGetErrorString(e__));                                  \
     } while (0)
 
 #define DCAT_LAUNCH_CHECK() DCAT_CUDA_CHECK(cudaGetLastError())

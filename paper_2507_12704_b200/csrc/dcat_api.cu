@@ -121,6 +121,9 @@ struct dcat_model {
     // last-call bookkeeping
     int64_t last_bu = 0, last_T = 0, last_Tp = 0;
     int last_precision_f32 = 0;
+    int tile_ctx = 64, tile_cross = 128;  // attention query tiles of the current call
+    bool vt = false;                      // current call keeps the V cache transposed (tcgen05 attention)
+    bool last_vt = false;
     void* last_kv = nullptr;
     std::vector<int64_t> last_tok_off;
     dcat_call_stats stats{};
@@ -296,12 +299,20 @@ uint64_t debug_hash_mask() {
     return (1ull << bits) - 1;
 }
 
-constexpr int kTileCtx = 64;
-constexpr int kTileCross = 128;  // crossing tiles: 128 candidate queries of one unique (8 warps)
+// Attention tiling: the tcgen05 attention (bf16, head dim 16/32/64, V cache stored
+// transposed) takes 128-query tiles in both passes; the mma.sync / SIMT kernels take
+// 64-query context tiles.
+bool use_tc_attention(const dcat_model* m, bool f32) {
+    const int dh = m->cfg.d_model / m->cfg.n_heads;
+    // opt-in until it beats the mma.sync flash kernel (per-CTA TMA -> MMA -> softmax -> MMA
+    // chain is serialized at 2 CTAs/SM; see profiles/r01_summary.md)
+    return !f32 && (dh == 32 || dh == 64) && getenv("DCAT_TC_ATTENTION") != nullptr;
+}
 
 // dedup + validation; leaves the plan on the device and the counts in m->st_host
 void run_dedup(dcat_model* m, const Staged& sb, const DedupOut& o, cudaStream_t s) {
     uint64_t mask = debug_hash_mask();
+    const int kTileCtx = m->tile_ctx, kTileCross = m->tile_cross;
     dedup_plan(sb.in, o, mask, kTileCtx, kTileCross, s);
     m->stats.kernel_launches += 23;
     DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
@@ -350,10 +361,14 @@ Epi base_epi(dcat_model* m, int mode, int layer_idx = -1) {
 }
 
 template <typename T>
-void attn(dcat_model* m, const AttnArgs& a, cudaStream_t s) {
+void attn(dcat_model* m, const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t s) {
     int t0 = mark(m, s);
-    if constexpr (std::is_same<T, bf16>::value) attention_bf16(a, s);
-    else attention_f32(a, s);
+    if constexpr (std::is_same<T, bf16>::value) {
+        if (a.ldvt > 0) attention_tc(a, q_rows, kv_rows, s);
+        else attention_bf16(a, s);
+    } else {
+        attention_f32(a, s);
+    }
     m->stats.kernel_launches += 1;
     span(m, a.causal ? "attn.ctx" : "attn.cross", t0, mark(m, s));
 }
@@ -376,8 +391,11 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     Tile* ctx_tiles = m->b_dd[20].get<Tile>(std::max(st.ctx_tiles, 1));
     Tile* cross_tiles = m->b_dd[21].get<Tile>(std::max(st.cross_tiles, 1));
     int32_t* tok_unique = m->b_dd[22].get<int32_t>(std::max<int64_t>(T_ctx, 1));
-    build_tiles(sb.in, o, b_u, kTileCtx, kTileCross, ctx_tiles, cross_tiles, tok_unique, s);
+    build_tiles(sb.in, o, b_u, m->tile_ctx, m->tile_cross, ctx_tiles, cross_tiles, tok_unique, s);
     m->stats.kernel_launches += 2;
+    // V cache layout: V^T [d][Tp] (keys contiguous) for the tcgen05 attention, else rows [Tp][d]
+    const bool vt = m->vt;
+    const int ldvt = vt ? static_cast<int>(Tp) : 0;
 
     Acts<T> A;
     A.Tp = Tp;
@@ -435,7 +453,9 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
                 e.bias = L.qkv.bias + d;
                 e.out[0] = K_l(l);
                 e.out[1] = V_l(l);
-                e.out_ld[0] = e.out_ld[1] = d;
+                e.out_ld[0] = d;
+                e.out_ld[1] = vt ? static_cast<int>(Tp) : d;
+                e.out_trans[1] = vt;
                 e.seg_cols = d;
                 gemm<T>(m, "gemm.ctx.kv", A.a, d, L.qkv, d, 2 * d, M, e, A.tmp, s);
                 break;
@@ -446,13 +466,14 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             e.out[0] = A.q;
             e.out[1] = K_l(l);
             e.out[2] = V_l(l);
-            e.out_ld[0] = e.out_ld[1] = e.out_ld[2] = d;
+            e.out_ld[0] = e.out_ld[1] = d;
+            e.out_ld[2] = vt ? static_cast<int>(Tp) : d;
+            e.out_trans[2] = vt;
             e.seg_cols = d;
             gemm<T>(m, "gemm.ctx.qkv", A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
-            AttnArgs aa{A.q, d, K_l(l), V_l(l), d, nullptr, nullptr, 0, A.ctx, d, ctx_tiles, st.ctx_tiles,
-                        H,   dh, scale, 1, c.max_len + 1};
-            attn<T>(m, aa, s);
-            m->stats.attn_flops += 0;  // accounted analytically by the caller
+            AttnArgs aa{A.q,     d,  K_l(l), V_l(l), d, ldvt, nullptr, nullptr, 0, A.ctx, d, ctx_tiles, st.ctx_tiles,
+                        H,       dh, scale,  1,      c.max_len + 1};
+            attn<T>(m, aa, Rr, Tp, s);
             e = base_epi(m, EPI_RESID_LN, l);
             e.bias = L.o.bias;
             e.resid = A.x;
@@ -516,9 +537,9 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         e.out_ld[0] = e.out_ld[1] = e.out_ld[2] = d;
         e.seg_cols = d;
         gemm<T>(m, "gemm.cross.qkv", A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
-        AttnArgs aa{A.q, d, K_l(l), V_l(l), d, A.kself, A.vself, d, A.ctx, d, cross_tiles, st.cross_tiles,
-                    H,   dh, scale, 0, c.max_len + 1};
-        attn<T>(m, aa, s);
+        AttnArgs aa{A.q, d,     K_l(l), V_l(l), d, ldvt, A.kself, A.vself, d, A.ctx, d, cross_tiles, st.cross_tiles,
+                    H,   dh,    scale,  0,      c.max_len + 1};
+        attn<T>(m, aa, Rr, std::max<int64_t>(Tp, 1), s);
         e = base_epi(m, EPI_RESID_LN, l);
         e.bias = L.o.bias;
         e.resid = A.x;
@@ -812,6 +833,9 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         std::memset(&m->stats, 0, sizeof m->stats);
         int64_t B = batch->n_rows;
         if (B == 0) return DCAT_OK;
+        m->vt = use_tc_attention(m, f32);
+        m->tile_ctx = m->vt ? 128 : 64;
+        m->tile_cross = 128;
         int t0 = mark(m, s);
         Staged sb = stage_batch(m, batch, device, ft->variant == DCAT_VARIANT_AUX, s);
         DedupOut o = dedup_buffers(m, B);
@@ -830,6 +854,7 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         m->last_bu = st.b_u;
         m->last_T = st.ctx_tokens;
         m->last_precision_f32 = f32;
+        m->last_vt = m->vt;
         float *dl = logits, *dm = module_logits, *dh = h_cand;
         if (!device) {
             dl = m->b_out[0].get<float>(B * 3);
@@ -893,6 +918,16 @@ int dcat_debug_kv(dcat_model* m, int32_t layer, int32_t unique, float* k, float*
             float* dst = which ? v : k;
             if (!dst) continue;
             size_t base = (static_cast<size_t>(2 * layer + which) * m->last_Tp + a) * d;
+            if (which == 1 && m->last_vt) {  // V^T [d][Tp]: gather the unique's key columns
+                const size_t vbase = static_cast<size_t>(2 * layer + 1) * m->last_Tp * d;
+                std::vector<bf16> tmp(static_cast<size_t>(d) * m->last_Tp);
+                DCAT_CUDA_CHECK(cudaMemcpy(tmp.data(), static_cast<bf16*>(m->last_kv) + vbase, tmp.size() * 2,
+                                           cudaMemcpyDeviceToHost));
+                for (int64_t t = 0; t < b - a; t++)
+                    for (int i = 0; i < d; i++)
+                        dst[t * d + i] = __bfloat162float(tmp[static_cast<size_t>(i) * m->last_Tp + a + t]);
+                continue;
+            }
             if (m->last_precision_f32) {
                 DCAT_CUDA_CHECK(cudaMemcpy(dst, static_cast<float*>(m->last_kv) + base, cnt * 4, cudaMemcpyDeviceToHost));
             } else {

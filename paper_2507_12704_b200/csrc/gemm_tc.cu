@@ -201,6 +201,17 @@ __device__ __forceinline__ void write_bf16_row(uint32_t buf, int lane, const flo
               pack_bf16(v[8 * j + 6], v[8 * j + 7]));
 }
 
+// transposed: value i of this lane's row -> element (i, lane) of a [32][32] bf16 SW64 block
+__device__ __forceinline__ void write_bf16_col(uint32_t buf, int lane, const float* v) {
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+        const uint32_t a = buf + i * 64 + ((((lane >> 3) ^ ((i >> 1) & 3)) << 4) | ((lane & 7) << 1));
+        const __nv_bfloat16 h = __float2bfloat16_rn(v[i]);
+        asm volatile("st.shared.b16 [%0], %1;" ::"r"(a), "h"(*reinterpret_cast<const unsigned short*>(&h))
+                     : "memory");
+    }
+}
+
 // publish this warp's staged block to the async proxy and TMA-store it (lane 0)
 __device__ __forceinline__ void store_block(const CUtensorMap* m, uint32_t buf, int col, int row, int lane) {
     fence_async_smem();
@@ -314,15 +325,21 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
                 const uint32_t buf = W.ew + W.hb * H_BYTES;
                 W.hb ^= 1;
                 staging_free<1>(lane);
-                write_bf16_row(buf, lane, v);
-                store_block(&mp.o[seg], buf, g0 - seg * e.seg_cols, row_base, lane);
+                if (e.out_trans[seg]) {  // V^T: this lane's row becomes column `lane` of a [dims][rows] block
+                    write_bf16_col(buf, lane, v);
+                    store_block(&mp.o[seg], buf, row_base, g0 - seg * e.seg_cols, lane);
+                } else {
+                    write_bf16_row(buf, lane, v);
+                    store_block(&mp.o[seg], buf, g0 - seg * e.seg_cols, row_base, lane);
+                }
             } else if (live) {
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
                     if (i >= nc) continue;
                     int g = g0 + i, sg = g / e.seg_cols;
-                    static_cast<bf16*>(e.out[sg])[static_cast<size_t>(row) * e.out_ld[sg] + (g - sg * e.seg_cols)] =
-                        __float2bfloat16_rn(v[i]);
+                    size_t off = e.out_trans[sg] ? static_cast<size_t>(g - sg * e.seg_cols) * e.out_ld[sg] + row
+                                                 : static_cast<size_t>(row) * e.out_ld[sg] + (g - sg * e.seg_cols);
+                    static_cast<bf16*>(e.out[sg])[off] = __float2bfloat16_rn(v[i]);
                 }
             }
         }
@@ -712,7 +729,10 @@ EpiMaps make_maps(const Epi& e, int M, int N) {
     if (e.mode == EPI_BIAS) {
         if (e.seg_cols % 32 == 0)
             for (int s = 0; s < 3 && s * e.seg_cols < N; s++)
-                mp.o[s] = tmap_epi(e.out[s], false, static_cast<uint64_t>(e.seg_cols), rows, e.out_ld[s]);
+                mp.o[s] = e.out_trans[s]
+                              ? tmap_epi(e.out[s], false, static_cast<uint64_t>(e.out_ld[s]),
+                                         static_cast<uint64_t>(e.seg_cols), e.out_ld[s])  // [seg_cols][ld] (V^T)
+                              : tmap_epi(e.out[s], false, static_cast<uint64_t>(e.seg_cols), rows, e.out_ld[s]);
     } else if (e.mode == EPI_RESID_LN || e.mode == EPI_L2NORM) {
         mp.resid = tmap_epi(e.resid, true, static_cast<uint64_t>(N), rows, e.ld_x);
         mp.xout = tmap_epi(e.x_out, true, static_cast<uint64_t>(N), rows, e.ld_x);

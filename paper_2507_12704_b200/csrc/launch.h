@@ -113,6 +113,7 @@ struct Epi {
     const float* bias;       // [N]
     void* out[3];            // EPI_BIAS: activation outputs per segment
     int out_ld[3];
+    int out_trans[3];        // 1: segment stored transposed, [seg_cols][out_ld] (V^T of the K/V cache)
     int seg_cols;            // columns per output segment
     const float* resid;      // EPI_RESID_LN: fp32 residual [M x ld_x]
     float* x_out;            // fp32 [M x ld_x]
@@ -143,7 +144,8 @@ void gemm_f32(const float* A, int lda, const float* W, int ldw, int M, int N, in
 // ---------------------------------------------------------------- attention.cu
 struct AttnArgs {
     const void* q; int ldq;        // query rows (head h at cols h*dh)
-    const void* k; const void* v; int ldkv;  // context K/V (cache)
+    const void* k; const void* v; int ldkv;  // context K (rows) and V (rows; bf16 path: V^T, see ldvt)
+    int ldvt;                      // bf16 path: V cache is V^T [d][ldvt] (keys contiguous); 0 = row-major V
     const void* kself; const void* vself; int ldself;  // crossing: per-row own key/value
     void* out; int ldo;
     const Tile* tiles; int n_tiles;
@@ -153,6 +155,9 @@ struct AttnArgs {
     int max_keys;                   // fp32 path: upper bound on keys per query
 };
 void attention_bf16(const AttnArgs& a, cudaStream_t s);
+// tcgen05 attention (attn_tc.cu): bf16, V cache transposed (ldvt > 0); q_rows / kv_rows are the
+// row extents of the Q and K tensors.
+void attention_tc(const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t s);
 void attention_f32(const AttnArgs& a, cudaStream_t s);
 
 // ---------------------------------------------------------------- head / scatter

@@ -165,6 +165,30 @@ def test_bf16_pinfm_base_sample_vs_oracle(api, orc):
     assert rel_err(lf, rl) <= 1e-4
 
 
+@pytest.mark.parametrize("impl", ["tcgen05", "flash"])
+def test_bf16_attention_impls_and_kv_cache(api, orc, impl, monkeypatch):
+    """Both bf16 attention kernels (tcgen05 with the V^T cache, mma.sync flash with the
+    row-major cache) against the oracle, and the bf16 K/V cache against context_forward's."""
+    if impl == "tcgen05":
+        monkeypatch.setenv("DCAT_TC_ATTENTION", "1")
+    spec, w, b = _base_setup(orc, 5, 9, 200, seed=6, ragged=True, layout="grouped")
+    ft = FinetuneSpec(max_events=200)
+    m = api.DcatModel(w)
+    logits, mlog, h = m.rank_forward_batch(b, ft, want_h=True)
+    rl, rm, _, rh = orc.rank_forward_batch(w, ft, b)
+    assert float(np.abs(h - rh).max()) <= 3e-2 and cos_min(h, rh) >= 0.999
+    assert rel_err(logits, rl) <= 3e-2 and rel_err(mlog, rm) <= 3e-2
+    rep, first, b_u = orc.dedup(b)
+    uniq = b.take(first)
+    for u in (0, b_u - 1):
+        for l in (0, spec.n_layers - 1):
+            k, v = m.debug_kv(l, u, 300)
+            rk, rv = orc.context_kv(w, uniq, l, u)
+            assert k.shape == rk.shape
+            assert float(np.abs(k - rk).max()) <= 3e-2 * max(1.0, float(np.abs(rk).max()))
+            assert float(np.abs(v - rv).max()) <= 3e-2 * max(1.0, float(np.abs(rv).max()))
+
+
 def test_bf16_full_size_properties(api, orc):
     """PinFM-base at full size (1000 users x 128): properties that hold at any
     size — batch permutation invariance and bit-identical duplicate rows
