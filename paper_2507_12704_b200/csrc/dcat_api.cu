@@ -349,6 +349,13 @@ void gemm(dcat_model* m, const char* tag, const T* A, int lda, const Lin& L, int
     m->stats.gemm_launches += 1;
     m->stats.gemm_flops += 2.0 * M * N * L.in32;
     span(m, tag, t0, mark(m, s));
+    static const bool debug_sync = getenv("DCAT_DEBUG_SYNC") != nullptr;  // debug: name the faulting GEMM
+    if (debug_sync) {
+        cudaError_t err = cudaStreamSynchronize(s);
+        if (err != cudaSuccess)
+            throw CudaError(std::string(tag) + " M=" + std::to_string(M) + " N=" + std::to_string(N) + " K=" +
+                            std::to_string(L.in) + ": " + cudaGetErrorString(err));
+    }
 }
 
 Epi base_epi(dcat_model* m, int mode, int layer_idx = -1) {

@@ -181,7 +181,8 @@ __global__ void k_row_epi(const float* __restrict__ acc, int ldacc, int M, int N
 void gemm_f32(const float* A, int lda, const float* W, int ldw, int M, int N, int K, const Epi& e, float* tmp,
               cudaStream_t s) {
     if (M <= 0 || N <= 0) return;
-    if (N > 32 * MAXV) throw InvalidArg("gemm_f32: N too large for the row epilogue");
+    if (N > 32 * MAXV && e.mode != EPI_BIAS)  // only the row-statistics modes keep the row in registers
+        throw InvalidArg("gemm_f32: N too large for the row epilogue");
     dim3 grid((N + TN - 1) / TN, (M + TM - 1) / TM);
     k_sgemm<<<grid, 256, 0, s>>>(A, lda, W, ldw, M, N, K, tmp, N);
     unsigned g = static_cast<unsigned>((static_cast<int64_t>(M) * 32 + 255) / 256);

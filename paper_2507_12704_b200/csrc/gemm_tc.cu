@@ -78,8 +78,10 @@ struct Cfg {
     static constexpr int RING = STAGES * (A_BYTES + B_BYTES);
     static constexpr int EW = FULL ? 2 * F_BYTES + 2 * H_BYTES : (MODE == EPI_BIAS ? 2 * H_BYTES : 0);  // per warp
     static constexpr int EPI_SMEM = EW * EPI_WARPS;
-    static constexpr int RED = 4 * 3 * CG * 32 * 4;  // [quadrant][value][cg][lane]
-    static constexpr int PARAM_FLOATS = BN == 512 ? 3088 : 1600;  // bias | ln_g | ln_b | mod_w/w2 | mod_b/b2
+    static constexpr int RED = MODE == EPI_BIAS ? 0 : 4 * 3 * CG * 32 * 4;  // [quadrant][value][cg][lane]
+    // smem params: EPI_BIAS keeps the whole bias (N <= 4096, every N tile of a persistent CTA);
+    // full-row / head modes: bias | ln_g | ln_b | mod_w/w2 | mod_b/b2 of one row (d <= 512)
+    static constexpr int PARAM_FLOATS = MODE == EPI_BIAS ? 4096 : BN == 512 ? 3088 : 1600;
     static constexpr int SMEM = RING + EPI_SMEM + RED + PARAM_FLOATS * 4 + 1024 + 512;
 };
 
@@ -763,6 +765,12 @@ void launch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, c
         DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tc<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM));
     });
+    {
+        const int npad = (N + 31) & ~31;
+        const int need = MODE == EPI_BIAS ? npad : MODE == EPI_HEAD ? 4 * npad + 3 : 6 * npad + 3;
+        if (need > C::PARAM_FLOATS)
+            throw InvalidArg("gemm_tc: epilogue parameters of N=" + std::to_string(N) + " exceed the smem staging");
+    }
     const EpiMaps mp = make_maps(e, M, N);
     int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
     int grid = tiles < num_sms() ? tiles : num_sms();

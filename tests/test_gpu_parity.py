@@ -189,6 +189,22 @@ def test_bf16_attention_impls_and_kv_cache(api, orc, impl, monkeypatch):
             assert float(np.abs(v - rv).max()) <= 3e-2 * max(1.0, float(np.abs(rv).max()))
 
 
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_long_seq_dims_d512(api, orc, precision):
+    """long-seq dims (d=512, 8 heads -> head dim 64, FFN 2048): the 512-wide full-row
+    epilogue, 2048-wide FFN bias staging and head-dim-64 attention."""
+    spec = ModelSpec(d_model=512, n_layers=2, n_heads=8, mlp_ratio=4, max_len=98, d_emb=512)
+    w = orc.init_weights(spec, 42, table=(8, 4096, 64, 7, 0.05), head_seed=11)
+    b = make_batch(3, 5, 96, seed=12, ragged=True, layout="grouped")
+    ft = FinetuneSpec(max_events=96)
+    m = api.DcatModel(w)
+    logits, mlog, h = m.rank_forward_batch(b, ft, precision=precision, want_h=True)
+    rl, rm, _, rh = orc.rank_forward_batch(w, ft, b)
+    tol = 1e-4 if precision == "fp32" else 3e-2
+    assert float(np.abs(h - rh).max()) <= tol
+    assert rel_err(logits, rl) <= tol and rel_err(mlog, rm) <= tol
+
+
 def test_bf16_full_size_properties(api, orc):
     """PinFM-base at full size (1000 users x 128): properties that hold at any
     size — batch permutation invariance and bit-identical duplicate rows
