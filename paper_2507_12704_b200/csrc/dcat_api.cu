@@ -367,6 +367,40 @@ Epi base_epi(dcat_model* m, int mode, int layer_idx = -1) {
     return e;
 }
 
+// FFN of a layer (model.cpp:386-397 / dcat.cpp:80-86): fused tcgen05 kernel when the
+// shape allows (the d_ff-wide intermediate never leaves the SM), else FFN1 + FFN2 GEMMs.
+// `fin` carries the residual / LN fields of the FFN2 epilogue.
+template <typename T>
+void ffn(dcat_model* m, const char* pass, const T* a, const LayerW& L, int M, Epi fin, T* f1, float* tmp,
+         cudaStream_t s) {
+    const int d = m->cfg.d_model, F = d * m->cfg.mlp_ratio;
+    static const bool no_fuse = getenv("DCAT_NO_FUSED_FFN") != nullptr;
+    if constexpr (std::is_same<T, bf16>::value) {
+        if (!no_fuse && ffn_tc_supported(d, F)) {
+            if (M <= 0) return;
+            int t0 = mark(m, s);
+            fin.bias = L.f1.bias;
+            fin.b2 = L.f2.bias;
+            ffn_tc(a, d, L.f1.wt, L.f2.wt, M, d, F, fin, s);
+            m->stats.kernel_launches += 1;
+            m->stats.gemm_launches += 1;
+            m->stats.gemm_flops += 4.0 * M * F * d;
+            span(m, pass[0] == 'c' && pass[1] == 't' ? "gemm.ctx.ffn" : "gemm.cross.ffn", t0, mark(m, s));
+            return;
+        }
+    }
+    Epi e = base_epi(m, EPI_BIAS);
+    e.act = 1;
+    e.bias = L.f1.bias;
+    e.out[0] = f1;
+    e.out_ld[0] = F;
+    e.seg_cols = F;
+    const bool ctx = pass[0] == 'c' && pass[1] == 't';
+    gemm<T>(m, ctx ? "gemm.ctx.ffn1" : "gemm.cross.ffn1", a, d, L.f1, 0, F, M, e, tmp, s);
+    fin.bias = L.f2.bias;
+    gemm<T>(m, ctx ? "gemm.ctx.ffn2" : "gemm.cross.ffn2", f1, F, L.f2, 0, d, M, fin, tmp, s);
+}
+
 template <typename T>
 void attn(dcat_model* m, const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t s) {
     int t0 = mark(m, s);
@@ -491,15 +525,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             e.ln_out = A.a;
             e.ln_ld = d;
             gemm<T>(m, "gemm.ctx.o", A.ctx, d, L.o, 0, d, M, e, A.tmp, s);
-            e = base_epi(m, EPI_BIAS);
-            e.act = 1;
-            e.bias = L.f1.bias;
-            e.out[0] = A.f1;
-            e.out_ld[0] = F;
-            e.seg_cols = F;
-            gemm<T>(m, "gemm.ctx.ffn1", A.a, d, L.f1, 0, F, M, e, A.tmp, s);
             e = base_epi(m, EPI_RESID_LN, l);
-            e.bias = L.f2.bias;
             e.resid = A.x;
             e.x_out = A.x;
             e.ld_x = d;
@@ -507,7 +533,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             e.ln_b = m->layers[l + 1].ln1_b;
             e.ln_out = A.a;
             e.ln_ld = d;
-            gemm<T>(m, "gemm.ctx.ffn2", A.f1, F, L.f2, 0, d, M, e, A.tmp, s);
+            ffn<T>(m, "ctx", A.a, L, M, e, A.f1, A.tmp, s);
         }
     }
     int t_ctx1 = mark(m, s);
@@ -557,15 +583,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         e.ln_out = A.a;
         e.ln_ld = d;
         gemm<T>(m, "gemm.cross.o", A.ctx, d, L.o, 0, d, M, e, A.tmp, s);
-        e = base_epi(m, EPI_BIAS);
-        e.act = 1;
-        e.bias = L.f1.bias;
-        e.out[0] = A.f1;
-        e.out_ld[0] = F;
-        e.seg_cols = F;
-        gemm<T>(m, "gemm.cross.ffn1", A.a, d, L.f1, 0, F, M, e, A.tmp, s);
         e = base_epi(m, EPI_RESID_LN, l);  // cross_tail's finite check (dcat.cpp:85-86)
-        e.bias = L.f2.bias;
         e.resid = A.x;
         e.x_out = A.x;
         e.ld_x = d;
@@ -573,7 +591,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         e.ln_b = l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr;
         e.ln_out = A.a;
         e.ln_ld = d;
-        gemm<T>(m, "gemm.cross.ffn2", A.f1, F, L.f2, 0, d, M, e, A.tmp, s);
+        ffn<T>(m, "cross", A.a, L, M, e, A.f1, A.tmp, s);
     }
     // phi_out (dcat.cpp:266) + module head (finetune.cpp:317-323)
     e = base_epi(m, EPI_BIAS);

@@ -669,6 +669,305 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------- fused FFN
+// The FFN half of layer_forward / cross_tail (model.cpp:386-397, dcat.cpp:80-86):
+//   x_out = x + gelu(a . W1 + b1) . W2 + b2 ;  ln_out = LN(x_out) (next LN1) or a plain copy
+// as ONE persistent kernel per 128-row tile: the d_ff-wide intermediate stays on the
+// SM (TMEM -> GELU -> bf16 smem -> next MMA) instead of a 2 x d_ff x 2 B round trip
+// through HBM per row. The A tile (128 x D) is resident in smem for the tile; the
+// hidden dimension is walked in 128-column chunks: FFN1 chunk j goes to one of two
+// TMEM accumulators (double-buffered), 8 epilogue warps apply bias + GELU and write
+// the chunk as the next MMA's K-major A operand, FFN2 accumulates all chunks into a
+// D-column TMEM accumulator; the residual / LayerNorm epilogue then runs on it.
+template <int D>
+struct FfnCfg {
+    static constexpr int CH = 128;                        // hidden columns per chunk
+    static constexpr int KB1 = D / 64;                    // k-blocks of the A tile
+    static constexpr int SLOT = (D > CH ? D : CH) * 128;  // ring slot: W1 block [CH x 64] | W2 block [D x 64]
+    static constexpr int STAGES = D == 256 ? 2 : 4;
+    static constexpr int A_TILE = KB1 * 16384;
+    static constexpr int H_BUF = 2 * 16384;  // [128 x CH] bf16 = 2 SW128 k-blocks
+    static constexpr int EPI_WARPS = 8;      // 2 per TMEM lane quadrant
+    static constexpr int CG = 2;
+    static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+    static constexpr int FCOLS = D / CG;     // final-epilogue columns per warp
+    static constexpr int PARAM_FLOATS = 1024 + 3 * 256 + 32;  // b1 (d_ff <= 1024) | b2 | ln_g | ln_b
+    static constexpr int RED = 4 * 3 * CG * 32 * 4;
+    static constexpr int SMEM = A_TILE + 2 * H_BUF + STAGES * SLOT + PARAM_FLOATS * 4 + RED + 1024 + 512;
+    static_assert(EPI_WARPS * 8192 <= 2 * H_BUF, "final-epilogue staging lives in the H buffers");
+};
+
+template <int D>
+__global__ void __launch_bounds__(FfnCfg<D>::THREADS, 1)
+    k_ffn_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW1,
+             const __grid_constant__ CUtensorMap tmW2, int M, int F, const __grid_constant__ Epi e,
+             const __grid_constant__ EpiMaps mp) {
+    using C = FfnCfg<D>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sH = sA + C::A_TILE;
+    uint8_t* ring = sH + 2 * C::H_BUF;
+    const uint32_t s_par = ptx::smem_u32(ring + C::STAGES * C::SLOT);
+    const uint32_t s_red = s_par + C::PARAM_FLOATS * 4;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + C::STAGES * C::SLOT + C::PARAM_FLOATS * 4 + C::RED);
+    uint64_t* a_full = bars;
+    uint64_t* a_empty = bars + 1;
+    uint64_t* full = bars + 2;
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* acc1_full = empty + C::STAGES;
+    uint64_t* acc1_empty = acc1_full + 2;
+    uint64_t* h_full = acc1_empty + 2;
+    uint64_t* h_empty = h_full + 2;
+    uint64_t* acc2_full = h_empty + 2;
+    uint64_t* acc2_empty = acc2_full + 1;
+    uint64_t* rbar = acc2_empty + 1;  // one per epilogue warp
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + C::EPI_WARPS);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tiles = (M + 127) / 128;
+    const int nch = F / C::CH;
+    const int P_B2 = 1024, P_G = 1024 + 256, P_BB = 1024 + 512;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch(&tmA);
+        ptx::tma_prefetch(&tmW1);
+        ptx::tma_prefetch(&tmW2);
+        ptx::mbar_init(a_full, 1);
+        ptx::mbar_init(a_empty, 1);
+        for (int s = 0; s < C::STAGES; s++) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            ptx::mbar_init(&acc1_full[b], 1);
+            ptx::mbar_init(&acc1_empty[b], C::EPI_WARPS);
+            ptx::mbar_init(&h_full[b], C::EPI_WARPS);
+            ptx::mbar_init(&h_empty[b], 1);
+        }
+        ptx::mbar_init(acc2_full, 1);
+        ptx::mbar_init(acc2_empty, C::EPI_WARPS);
+        for (int w = 0; w < C::EPI_WARPS; w++) ptx::mbar_init(&rbar[w], 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc(tslot, 512);
+    if (warp >= 4) {
+        const int tid = threadIdx.x - 128;
+        for (int i = tid; i < 1024; i += 32 * C::EPI_WARPS) sts1(s_par + 4u * i, i < F ? e.bias[i] : 0.f);
+        for (int i = tid; i < 256; i += 32 * C::EPI_WARPS) {
+            sts1(s_par + 4u * (P_B2 + i), i < D ? e.b2[i] : 0.f);
+            sts1(s_par + 4u * (P_G + i), (e.ln_g && i < D) ? e.ln_g[i] : 0.f);
+            sts1(s_par + 4u * (P_BB + i), (e.ln_b && i < D) ? e.ln_b[i] : 0.f);
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t T_ACC2 = tmem, T_ACC1 = tmem + 256;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t it = 0, i = 0;
+            auto push = [&](const CUtensorMap* map, int c0, int c1, uint32_t bytes) {
+                const int s = it % C::STAGES;
+                ptx::mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+                ptx::mbar_expect_tx(&full[s], bytes);
+                ptx::tma_load_2d(ring + s * C::SLOT, map, &full[s], c0, c1);
+                it++;
+            };
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
+                ptx::mbar_wait(a_empty, (i & 1) ^ 1);
+                ptx::mbar_expect_tx(a_full, C::A_TILE);
+                for (int kb = 0; kb < C::KB1; kb++) ptx::tma_load_2d(sA + kb * 16384, &tmA, a_full, kb * 64, t * 128);
+                for (int j = 0; j <= nch; j++) {
+                    if (j < nch)
+                        for (int kb = 0; kb < C::KB1; kb++) push(&tmW1, kb * 64, j * C::CH, C::CH * 128);
+                    if (j > 0)
+                        for (int kb2 = 0; kb2 < 2; kb2++) push(&tmW2, (j - 1) * C::CH + kb2 * 64, 0, D * 128);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc1 = ptx::idesc_bf16(128, C::CH);
+            constexpr uint32_t idesc2 = ptx::idesc_bf16(128, D);
+            uint32_t it = 0, c1 = 0, c2 = 0, i = 0;
+            const uint32_t a_base = ptx::smem_u32(sA), h_base = ptx::smem_u32(sH), r_base = ptx::smem_u32(ring);
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
+                ptx::mbar_wait(a_full, i & 1);
+                ptx::tc_fence_after();
+                for (int j = 0; j <= nch; j++) {
+                    if (j < nch) {  // FFN1 chunk j -> acc1[b]
+                        const int b = c1 & 1;
+                        ptx::mbar_wait(&acc1_empty[b], ((c1 >> 1) & 1) ^ 1);
+                        ptx::tc_fence_after();
+                        for (int kb = 0; kb < C::KB1; kb++, it++) {
+                            const int s = it % C::STAGES;
+                            ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+                            ptx::tc_fence_after();
+#pragma unroll
+                            for (int k = 0; k < 4; k++)
+                                ptx::mma_bf16(T_ACC1 + b * C::CH, ptx::sdesc_sw128(a_base + kb * 16384 + k * 32),
+                                              ptx::sdesc_sw128(r_base + s * C::SLOT + k * 32), idesc1, (kb | k) != 0);
+                            ptx::mma_commit(&empty[s]);
+                        }
+                        ptx::mma_commit(&acc1_full[b]);
+                        c1++;
+                        if (j == nch - 1) ptx::mma_commit(a_empty);  // the A tile is free once these complete
+                    }
+                    if (j > 0) {  // FFN2 of chunk j-1: acc2 += H . W2_chunk
+                        const int hb = c2 & 1;
+                        ptx::mbar_wait(&h_full[hb], (c2 >> 1) & 1);
+                        if (j == 1) ptx::mbar_wait(acc2_empty, (i & 1) ^ 1);
+                        ptx::tc_fence_after();
+                        for (int kb2 = 0; kb2 < 2; kb2++, it++) {
+                            const int s = it % C::STAGES;
+                            ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+                            ptx::tc_fence_after();
+#pragma unroll
+                            for (int k = 0; k < 4; k++)
+                                ptx::mma_bf16(T_ACC2, ptx::sdesc_sw128(h_base + hb * C::H_BUF + kb2 * 16384 + k * 32),
+                                              ptx::sdesc_sw128(r_base + s * C::SLOT + k * 32), idesc2,
+                                              (j > 1 || kb2 > 0 || k > 0));
+                            ptx::mma_commit(&empty[s]);
+                        }
+                        ptx::mma_commit(&h_empty[hb]);
+                        c2++;
+                    }
+                }
+                ptx::mma_commit(acc2_full);
+            }
+        }
+    } else if (warp >= 4) {
+        const int ew = warp - 4, q = warp & 3, cg = ew >> 2;
+        const int r = q * 32 + lane;  // tile row of this thread
+        const uint32_t h_base = ptx::smem_u32(sH);
+        const uint32_t F0 = h_base + ew * 8192, H0 = F0 + 4096;  // final-epilogue staging (in the H buffers)
+        const uint32_t rb = ptx::smem_u32(&rbar[ew]);
+        uint32_t c1 = 0, rph = 0, i = 0;
+        float v[32], pp[32];
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
+            const int m0 = t * 128, row_base = m0 + q * 32;
+            // ---- GELU chunks
+            for (int j = 0; j < nch; j++, c1++) {
+                const int b = c1 & 1;
+                ptx::mbar_wait(&acc1_full[b], (c1 >> 1) & 1);
+                ptx::tc_fence_after();
+                float g[64];
+                tmem_load32(T_ACC1 + b * C::CH + cg * 64 + (static_cast<uint32_t>(q * 32) << 16), g);
+                tmem_load32(T_ACC1 + b * C::CH + cg * 64 + 32 + (static_cast<uint32_t>(q * 32) << 16), g + 32);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc1_empty[b]);
+                const int pc = j * C::CH + cg * 64;
+#pragma unroll
+                for (int k = 0; k < 64; k += 4) {
+                    float4 bb = lds4(s_par + 4u * (pc + k));
+                    g[k] = gelu_fast(g[k] + bb.x);
+                    g[k + 1] = gelu_fast(g[k + 1] + bb.y);
+                    g[k + 2] = gelu_fast(g[k + 2] + bb.z);
+                    g[k + 3] = gelu_fast(g[k + 3] + bb.w);
+                }
+                ptx::mbar_wait(&h_empty[b], ((c1 >> 1) & 1) ^ 1);
+                // row r of k-block cg of H buffer b: 8 x 16 B chunks, 128 B swizzle
+                const uint32_t rowa = h_base + b * C::H_BUF + cg * 16384 + r * 128;
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    sts4u(rowa + ((k ^ (r & 7)) << 4), pack_bf16(g[8 * k], g[8 * k + 1]),
+                          pack_bf16(g[8 * k + 2], g[8 * k + 3]), pack_bf16(g[8 * k + 4], g[8 * k + 5]),
+                          pack_bf16(g[8 * k + 6], g[8 * k + 7]));
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&h_full[b]);
+            }
+            // ---- residual + LayerNorm on acc2 (all FFN2 MMAs of the tile are done: H buffers free)
+            ptx::mbar_wait(acc2_full, i & 1);
+            ptx::tc_fence_after();
+            const uint32_t tacc = T_ACC2 + (static_cast<uint32_t>(q * 32) << 16);
+            float s1[1] = {0.f};
+            bool bad = false;
+#pragma unroll 1
+            for (int ch = 0; ch < C::FCOLS / 32; ch++) {
+                const int c = cg * C::FCOLS + ch * 32;
+                if (lane == 0) {
+                    mbar_expect_tx_s(rb, F_BYTES);
+                    tma_load_s(F0, &mp.resid, rb, c, row_base);
+                }
+                mbar_wait_s(rb, rph);
+                rph ^= 1;
+                read_f32_row(F0, lane, pp);
+                tmem_load32(tacc + c, v);
+#pragma unroll
+                for (int k = 0; k < 32; k++) v[k] = v[k] + pp[k];  // (acc + resid) + b2, as RESID_LN
+                lds32(s_par, P_B2 + c, pp);
+#pragma unroll
+                for (int k = 0; k < 32; k++) {
+                    v[k] += pp[k];
+                    bad |= !isfinite(v[k]);
+                    s1[0] += v[k];
+                }
+                __syncwarp();
+                write_f32_row(F0, lane, v);
+                store_block(&mp.xout, F0, c, row_base, lane);
+                if (e.ln_g == nullptr && e.ln_out) {
+                    staging_free<1>(lane);
+                    write_bf16_row(H0, lane, v);
+                    store_block(&mp.ln, H0, c, row_base, lane);
+                }
+                tmem_store32(tacc + c, v);
+                staging_free<0>(lane);
+            }
+            if (bad && row_base + lane < M && e.layer_idx >= 0) atomicMax(&e.st->nonfinite_layer, e.layer_idx + 1);
+            if (e.ln_g && e.ln_out) {
+                quad_reduce<C::CG, 1>(s_red, s1, cg, lane, q);
+                const float dn = static_cast<float>(D);
+                const float mu = s1[0] / dn;
+                float var[1] = {0.f};
+#pragma unroll 1
+                for (int ch = 0; ch < C::FCOLS / 32; ch++) {
+                    tmem_load32(tacc + cg * C::FCOLS + ch * 32, v);
+#pragma unroll
+                    for (int k = 0; k < 32; k++) {
+                        float d0 = v[k] - mu;
+                        var[0] += d0 * d0;
+                    }
+                }
+                quad_reduce<C::CG, 1>(s_red, var, cg, lane, q);
+                const float rs = 1.0f / sqrtf(var[0] / dn + 1e-5f);
+#pragma unroll 1
+                for (int ch = 0; ch < C::FCOLS / 32; ch++) {
+                    const int c = cg * C::FCOLS + ch * 32;
+                    tmem_load32(tacc + c, v);
+                    lds32(s_par, P_G + c, pp);
+#pragma unroll
+                    for (int k = 0; k < 32; k++) v[k] = pp[k] * ((v[k] - mu) * rs);
+                    lds32(s_par, P_BB + c, pp);
+#pragma unroll
+                    for (int k = 0; k < 32; k++) v[k] += pp[k];
+                    staging_free<0>(lane);
+                    write_bf16_row(H0, lane, v);
+                    store_block(&mp.ln, H0, c, row_base, lane);
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc2_empty);
+            // the next tile's GELU writes reuse this staging: all epilogue warps drain first
+            staging_free<0>(lane);
+            named_bar(5, 32 * C::EPI_WARPS);
+        }
+        if (lane == 0) bulk_wait_all();
+        __syncwarp();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 512);
+    }
+}
+
 // ---------------------------------------------------------------- host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -796,6 +1095,45 @@ void launch_mode(int BN, const CUtensorMap& ta, const CUtensorMap& tb, int M, in
 }
 
 }  // namespace
+
+namespace {
+template <int D>
+void launch_ffn(const CUtensorMap& ta, const CUtensorMap& t1, const CUtensorMap& t2, int M, int F, const Epi& e,
+                const EpiMaps& mp, cudaStream_t s) {
+    using C = FfnCfg<D>;
+    static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
+    static std::once_flag once;
+    std::call_once(once, [] {
+        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_ffn_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    });
+    const int tiles = (M + 127) / 128;
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    k_ffn_tc<D><<<grid, C::THREADS, C::SMEM, s>>>(ta, t1, t2, M, F, e, mp);
+    DCAT_LAUNCH_CHECK();
+}
+}  // namespace
+
+bool ffn_tc_supported(int D, int F) { return (D == 64 || D == 128 || D == 256) && F % 128 == 0 && F <= 1024; }
+
+void ffn_tc(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M, int D, int F, const Epi& e,
+            cudaStream_t s) {
+    if (M <= 0) return;
+    if (!ffn_tc_supported(D, F)) throw InvalidArg("ffn_tc: unsupported shape");
+    CUtensorMap ta = tmap_bf16(A, static_cast<uint64_t>(D), static_cast<uint64_t>(M), static_cast<uint64_t>(lda) * 2,
+                               128);
+    CUtensorMap t1 = tmap_bf16(W1t, static_cast<uint64_t>(D), static_cast<uint64_t>(F), static_cast<uint64_t>(D) * 2,
+                               128);
+    CUtensorMap t2 = tmap_bf16(W2t, static_cast<uint64_t>(F), static_cast<uint64_t>(D), static_cast<uint64_t>(F) * 2,
+                               static_cast<uint32_t>(D));
+    Epi em = e;
+    em.mode = EPI_RESID_LN;
+    const EpiMaps mp = make_maps(em, M, D);
+    switch (D) {
+        case 64: launch_ffn<64>(ta, t1, t2, M, F, e, mp, s); break;
+        case 128: launch_ffn<128>(ta, t1, t2, M, F, e, mp, s); break;
+        default: launch_ffn<256>(ta, t1, t2, M, F, e, mp, s); break;
+    }
+}
 
 void gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K, const Epi& e, cudaStream_t s) {
     if (M <= 0 || N <= 0) return;

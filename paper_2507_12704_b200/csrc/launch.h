@@ -137,6 +137,12 @@ struct Epi {
 // bf16 tensor-core GEMM (tcgen05 + TMEM + TMA): C[M x N] = A[M x K] . W^T,
 // A bf16 row-major (lda), W bf16 [N x K] row-major, fused epilogue.
 void gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K, const Epi& e, cudaStream_t s);
+// Fused FFN (tcgen05): x_out = resid + gelu(A . W1t^T + bias) . W2t^T + b2, then LN -> ln_out
+// (e.bias = b1 [F], e.b2 = b2 [D], resid / x_out / ld_x / ln_g / ln_b / ln_out / ln_ld as EPI_RESID_LN).
+// W1t = W1^T [F x D], W2t = W2^T [D x F] (bf16, K-major).
+bool ffn_tc_supported(int D, int F);
+void ffn_tc(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M, int D, int F, const Epi& e,
+            cudaStream_t s);
 // fp32 parity path: SIMT GEMM (W in reference in x out layout, ldw) + row epilogue.
 void gemm_f32(const float* A, int lda, const float* W, int ldw, int M, int N, int K, const Epi& e, float* tmp,
               cudaStream_t s);
