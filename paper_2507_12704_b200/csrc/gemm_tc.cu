@@ -41,6 +41,13 @@
 #include "launch.h"
 #include "ptx.cuh"
 
+#ifndef DCAT_FFN_ABLATE
+#define DCAT_FFN_ABLATE 0  // product build: nothing ablated
+#endif
+#ifndef DCAT_FFN_TRACE
+#define DCAT_FFN_TRACE 0  // kernel micro-bench only: clock64 event trace of CTA 0 of k_ffn_tc
+#endif
+
 namespace dcat {
 
 namespace {
@@ -148,8 +155,9 @@ __device__ __forceinline__ float tanh_fast(float x) {
 // tanh-form GELU (model.hpp:14-18) with the MUFU tanh: its ~2^-11 relative
 // error is below the bf16 rounding of every consumer of this value.
 __device__ __forceinline__ float gelu_fast(float x) {
-    float x3 = x * x * x;
-    return 0.5f * x * (1.0f + tanh_fast(0.7978845608028654f * (x + 0.044715f * x3)));
+    const float u = x * fmaf(x * x, 0.7978845608028654f * 0.044715f, 0.7978845608028654f);
+    const float h = 0.5f * x;
+    return fmaf(h, tanh_fast(u), h);
 }
 
 __device__ __forceinline__ void tmem_load32(uint32_t taddr, float* v) {
@@ -679,30 +687,73 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
 // TMEM accumulators (double-buffered), 8 epilogue warps apply bias + GELU and write
 // the chunk as the next MMA's K-major A operand, FFN2 accumulates all chunks into a
 // D-column TMEM accumulator; the residual / LayerNorm epilogue then runs on it.
-template <int D>
+template <int D, int CL>
 struct FfnCfg {
     static constexpr int CH = 128;                        // hidden columns per chunk
     static constexpr int KB1 = D / 64;                    // k-blocks of the A tile
-    static constexpr int SLOT = (D > CH ? D : CH) * 128;  // ring slot: W1 block [CH x 64] | W2 block [D x 64]
-    static constexpr int STAGES = D == 256 ? 2 : 4;
+    // Weight blocks this CTA loads: CL = 1 the whole block, CL = 2 its half of the N rows
+    // (the pair MMA reads B rows [0, N/2) from the leader and [N/2, N) from the peer).
+    static constexpr int NW2 = CL == 1 && D > 128 ? 128 : D;  // N of one FFN2 MMA (single CTA: <= 128)
+    static constexpr int W1_ROWS = CH / CL;               // W1 rows (hidden units) per block
+    static constexpr int W2_ROWS = CL == 2 ? D / 2 : NW2;  // W2 rows (output dims) per block
+    static constexpr int W1_BLK = W1_ROWS * 128;          // one 64-wide k-block, SW128
+    static constexpr int W2_BLK = W2_ROWS * 128;
+    static constexpr int SLOT = 16384;                    // ring slot
+    static constexpr int W1_PER_SLOT = SLOT / W1_BLK;     // k-blocks per slot
+    static constexpr int W2_PER_SLOT = SLOT / W2_BLK;
+    static constexpr int S1 = KB1 / W1_PER_SLOT;          // slots per FFN1 chunk
+    static constexpr int S2 = 2 / W2_PER_SLOT;            // slots per FFN2 chunk (2 k-blocks of 64)
+    static constexpr int STAGES = D == 256 ? 5 : 7;       // weight blocks in flight (L2 latency)
     static constexpr int A_TILE = KB1 * 16384;
     static constexpr int H_BUF = 2 * 16384;  // [128 x CH] bf16 = 2 SW128 k-blocks
-    static constexpr int EPI_WARPS = 8;      // 2 per TMEM lane quadrant
-    static constexpr int CG = 2;
-    static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-    static constexpr int FCOLS = D / CG;     // final-epilogue columns per warp
+    // warp 0: TMA producer + TMEM allocator, warp 1: MMA issuer (leader CTA), warps 2..17:
+    // epilogue. Epilogue warp w reads TMEM lane quadrant w % 4; the 4 warps of a quadrant
+    // split the columns (GELU: 32 of each 128-column chunk; final: FCOLS of the D outputs).
+    static constexpr int EPI_WARPS = 16;
+    static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+    static constexpr int CGF = D >= 128 ? 4 : 2;  // final-epilogue warps per quadrant
+    static constexpr int FCOLS = D / CGF;         // final-epilogue columns per warp
+    static constexpr int STG = 4096;              // final-epilogue staging per warp (in the H buffers)
     static constexpr int PARAM_FLOATS = 1024 + 3 * 256 + 32;  // b1 (d_ff <= 1024) | b2 | ln_g | ln_b
-    static constexpr int RED = 4 * 3 * CG * 32 * 4;
+    static constexpr int RED = 4 * 3 * CGF * 32 * 4;
     static constexpr int SMEM = A_TILE + 2 * H_BUF + STAGES * SLOT + PARAM_FLOATS * 4 + RED + 1024 + 512;
-    static_assert(EPI_WARPS * 8192 <= 2 * H_BUF, "final-epilogue staging lives in the H buffers");
+    static_assert(EPI_WARPS * STG <= 2 * H_BUF, "final-epilogue staging lives in the H buffers");
+    static_assert(FCOLS == 32 || FCOLS == 64, "final epilogue works on one or two 32-column blocks");
+    static_assert(CL == 1 || D >= 128, "CTA-pair FFN needs D >= 128");
+    static_assert(W1_PER_SLOT * W1_BLK == SLOT && W2_PER_SLOT * W2_BLK == SLOT && S1 >= 1 && S2 >= 1,
+                  "slot holds whole weight blocks");
 };
 
-template <int D>
-__global__ void __launch_bounds__(FfnCfg<D>::THREADS, 1)
+#if DCAT_FFN_TRACE
+__device__ unsigned long long g_ffn_trace[8192];
+__device__ unsigned int g_ffn_trace_n;
+#define FFN_EV(code, j)                                                                       \
+    do {                                                                                      \
+        if (blockIdx.x == 0 && i < 4) {                                                       \
+            unsigned k_ = atomicAdd(&g_ffn_trace_n, 1u);                                      \
+            if (k_ < 8192)                                                                    \
+                g_ffn_trace[k_] = (static_cast<unsigned long long>(clock64()) << 16) |        \
+                                  (static_cast<unsigned>(code) << 8) | static_cast<unsigned>(j); \
+        }                                                                                     \
+    } while (0)
+#else
+#define FFN_EV(code, j) \
+    do {                \
+    } while (0)
+#endif
+
+// CL = 1: one CTA per 128-row tile. CL = 2: a CTA pair (cluster of 2 on one TPC) per
+// 256-row tile; the leader issues M = 256 tcgen05.mma.cta_group::2 reading each CTA's
+// own A / H rows and its half of every weight block, so each SM streams half the
+// weight bytes per row. Every barrier the MMA issuer waits on lives in the leader
+// (peer producers / epilogue warps arrive remotely); MMA completions are multicast to
+// the same barrier in both CTAs.
+template <int D, int CL>
+__global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
     k_ffn_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW1,
              const __grid_constant__ CUtensorMap tmW2, int M, int F, const __grid_constant__ Epi e,
              const __grid_constant__ EpiMaps mp) {
-    using C = FfnCfg<D>;
+    using C = FfnCfg<D, CL>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -721,38 +772,67 @@ __global__ void __launch_bounds__(FfnCfg<D>::THREADS, 1)
     uint64_t* h_empty = h_full + 2;
     uint64_t* acc2_full = h_empty + 2;
     uint64_t* acc2_empty = acc2_full + 1;
-    uint64_t* rbar = acc2_empty + 1;  // one per epilogue warp
+    uint64_t* rbar = acc2_empty + 1;  // residual block loads, one per epilogue warp
     uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + C::EPI_WARPS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tiles = (M + 127) / 128;
+    const uint32_t rank = CL == 2 ? ptx::cluster_rank() : 0;
+    const int units = ((M + 127) / 128 + CL - 1) / CL;  // row tiles of 128 * CL rows
+    const int unit0 = blockIdx.x / CL, ustride = gridDim.x / CL;
     const int nch = F / C::CH;
     const int P_B2 = 1024, P_G = 1024 + 256, P_BB = 1024 + 512;
+    // MMA issue order F1_0 .. F1_{LA-1}, then F1_j, F2_{j-LA}: FFN1 runs LA chunks ahead, so a
+    // chunk's GELU overlaps ~2 LA chunk-MMAs and F1_j only needs GELU_{j-2}'s TMEM read.
+    constexpr int LA = 2;
+    // Hidden chunks in ascending order for every tile: a row's FP32 accumulation order never
+    // depends on which CTA processes it (bit-exact under batch permutation).
+    auto chunk = [](int j) { return j; };
+
+    // barrier plumbing: arrivals that the MMA issuer waits on go to the leader CTA
+    auto lead = [&](uint64_t* b) -> uint32_t {
+        if constexpr (CL == 2) return ptx::mapa(ptx::smem_u32(b), 0);
+        else return ptx::smem_u32(b);
+    };
+    auto arrive_lead = [&](uint64_t* b) {
+        if constexpr (CL == 2) ptx::mbar_arrive_cl(lead(b));
+        else mbar_arrive(b);
+    };
+    auto commit = [&](uint64_t* b) {
+        if constexpr (CL == 2) ptx::mma_commit_pair(b);
+        else ptx::mma_commit(b);
+    };
+    auto wait_lead = [&](uint64_t* b, uint32_t parity) {  // leader-side wait on remote arrivals
+        if constexpr (CL == 2) ptx::mbar_wait_cl(b, parity);
+        else ptx::mbar_wait(b, parity);
+    };
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch(&tmA);
         ptx::tma_prefetch(&tmW1);
         ptx::tma_prefetch(&tmW2);
-        ptx::mbar_init(a_full, 1);
+        ptx::mbar_init(a_full, CL);  // one expect_tx arrival per CTA
         ptx::mbar_init(a_empty, 1);
         for (int s = 0; s < C::STAGES; s++) {
-            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&full[s], CL);
             ptx::mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; b++) {
             ptx::mbar_init(&acc1_full[b], 1);
-            ptx::mbar_init(&acc1_empty[b], C::EPI_WARPS);
-            ptx::mbar_init(&h_full[b], C::EPI_WARPS);
+            ptx::mbar_init(&acc1_empty[b], CL * C::EPI_WARPS);
+            ptx::mbar_init(&h_full[b], CL * C::EPI_WARPS);
             ptx::mbar_init(&h_empty[b], 1);
         }
         ptx::mbar_init(acc2_full, 1);
-        ptx::mbar_init(acc2_empty, C::EPI_WARPS);
+        ptx::mbar_init(acc2_empty, CL * 4 * C::CGF);
         for (int w = 0; w < C::EPI_WARPS; w++) ptx::mbar_init(&rbar[w], 1);
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc(tslot, 512);
-    if (warp >= 4) {
-        const int tid = threadIdx.x - 128;
+    if (warp == 0) {
+        if constexpr (CL == 2) ptx::tmem_alloc_pair(tslot, 512);
+        else ptx::tmem_alloc(tslot, 512);
+    }
+    if (warp >= 2) {
+        const int tid = threadIdx.x - 64;
         for (int i = tid; i < 1024; i += 32 * C::EPI_WARPS) sts1(s_par + 4u * i, i < F ? e.bias[i] : 0.f);
         for (int i = tid; i < 256; i += 32 * C::EPI_WARPS) {
             sts1(s_par + 4u * (P_B2 + i), i < D ? e.b2[i] : 0.f);
@@ -761,7 +841,8 @@ __global__ void __launch_bounds__(FfnCfg<D>::THREADS, 1)
         }
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CL == 2) ptx::cluster_sync();  // peer barriers initialised before any remote arrival
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
     const uint32_t T_ACC2 = tmem, T_ACC1 = tmem + 256;
@@ -769,100 +850,194 @@ __global__ void __launch_bounds__(FfnCfg<D>::THREADS, 1)
     if (warp == 0) {
         if (lane == 0) {
             uint32_t it = 0, i = 0;
-            auto push = [&](const CUtensorMap* map, int c0, int c1, uint32_t bytes) {
+            // one ring slot: `n` weight blocks of `blk` bytes at k offsets k0 + 64 w, rows r0
+            auto push = [&](const CUtensorMap* map, int k0, int r0, int n, int blk) {
                 const int s = it % C::STAGES;
                 ptx::mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
-                ptx::mbar_expect_tx(&full[s], bytes);
-                ptx::tma_load_2d(ring + s * C::SLOT, map, &full[s], c0, c1);
+                FFN_EV(11, it & 255);
+                const uint32_t dst = ptx::smem_u32(ring + s * C::SLOT);
+#if DCAT_FFN_ABLATE & 4  // kernel micro-bench only: weights loaded once, ring recycled without TMA
+                if (it >= static_cast<uint32_t>(C::STAGES)) {
+                    if constexpr (CL == 2) ptx::mbar_arrive_cl(lead(&full[s]));
+                    else mbar_arrive(&full[s]);
+                    it++;
+                    return;
+                }
+#endif
+                if constexpr (CL == 2) {
+                    ptx::mbar_expect_tx_cl(lead(&full[s]), C::SLOT);
+                    for (int w = 0; w < n; w++) ptx::tma_load_2d_pair(dst + w * blk, map, lead(&full[s]), k0 + 64 * w, r0);
+                } else {
+                    ptx::mbar_expect_tx(&full[s], C::SLOT);
+                    for (int w = 0; w < n; w++) ptx::tma_load_2d(ring + s * C::SLOT + w * blk, map, &full[s], k0 + 64 * w, r0);
+                }
                 it++;
             };
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
+            for (int u = unit0; u < units; u += ustride, i++) {
+                const int t = u * CL + static_cast<int>(rank);  // this CTA's 128-row tile
                 ptx::mbar_wait(a_empty, (i & 1) ^ 1);
-                ptx::mbar_expect_tx(a_full, C::A_TILE);
-                for (int kb = 0; kb < C::KB1; kb++) ptx::tma_load_2d(sA + kb * 16384, &tmA, a_full, kb * 64, t * 128);
-                for (int j = 0; j <= nch; j++) {
+                FFN_EV(10, 0);
+                if constexpr (CL == 2) {
+                    ptx::mbar_expect_tx_cl(lead(a_full), C::A_TILE);
+                    for (int kb = 0; kb < C::KB1; kb++)
+                        ptx::tma_load_2d_pair(ptx::smem_u32(sA + kb * 16384), &tmA, lead(a_full), kb * 64, t * 128);
+                } else {
+                    ptx::mbar_expect_tx(a_full, C::A_TILE);
+                    for (int kb = 0; kb < C::KB1; kb++) ptx::tma_load_2d(sA + kb * 16384, &tmA, a_full, kb * 64, t * 128);
+                }
+                // the next tile's A rows and residual rows stream into L2 while this tile's MMAs
+                // run, so its A load and residual slots are L2 hits
+                if (u + ustride < units) {
+                    const int tn = (u + ustride) * CL + static_cast<int>(rank);
+                    for (int kb = 0; kb < C::KB1; kb++) ptx::tma_prefetch_l2(&tmA, kb * 64, tn * 128);
+                    for (int cc = 0; cc < D; cc += 32) ptx::tma_prefetch_l2(&mp.resid, cc, tn * 128);
+                }
+                if (i == 0)
+                    for (int cc = 0; cc < D; cc += 32) ptx::tma_prefetch_l2(&mp.resid, cc, t * 128);
+                for (int j = 0; j < nch + LA; j++) {  // same order as the MMA issuer
                     if (j < nch)
-                        for (int kb = 0; kb < C::KB1; kb++) push(&tmW1, kb * 64, j * C::CH, C::CH * 128);
-                    if (j > 0)
-                        for (int kb2 = 0; kb2 < 2; kb2++) push(&tmW2, (j - 1) * C::CH + kb2 * 64, 0, D * 128);
+                        for (int p = 0; p < C::S1; p++)
+                            push(&tmW1, p * C::W1_PER_SLOT * 64, chunk(j) * C::CH + static_cast<int>(rank) * C::W1_ROWS,
+                                 C::W1_PER_SLOT, C::W1_BLK);
+                    if (j >= LA) {
+                        const int jj = j - LA;
+                        if (jj == 0)  // residual [128 x 32] fp32 blocks: the initial value of acc2
+                            for (int cc = 0; cc < D; cc += 32) push(&mp.resid, cc, t * 128, 1, C::SLOT);
+                        if constexpr (CL == 1 && C::NW2 < D) {  // single CTA, D = 256: N halves per slot
+                            for (int kb2 = 0; kb2 < 2; kb2++)
+                                for (int nh = 0; nh < D / C::NW2; nh++)
+                                    push(&tmW2, chunk(jj) * C::CH + kb2 * 64, nh * C::NW2, 1, C::SLOT);
+                        } else {
+                            for (int p = 0; p < C::S2; p++)
+                                push(&tmW2, chunk(jj) * C::CH + p * C::W2_PER_SLOT * 64,
+                                     static_cast<int>(rank) * C::W2_ROWS, C::W2_PER_SLOT, C::W2_BLK);
+                        }
+                    }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc1 = ptx::idesc_bf16(128, C::CH);
-            constexpr uint32_t idesc2 = ptx::idesc_bf16(128, D);
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t idesc1 = ptx::idesc_bf16(128 * CL, C::CH);
+            constexpr uint32_t idesc2 = ptx::idesc_bf16(128 * CL, C::NW2);
             uint32_t it = 0, c1 = 0, c2 = 0, i = 0;
             const uint32_t a_base = ptx::smem_u32(sA), h_base = ptx::smem_u32(sH), r_base = ptx::smem_u32(ring);
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
-                ptx::mbar_wait(a_full, i & 1);
+            auto mma = [&](uint32_t d, uint32_t a, uint32_t b, uint32_t idesc, uint32_t acc) {
+#if DCAT_FFN_ABLATE & 8  // kernel micro-bench only: no MMAs issued
+                return;
+#endif
+                if constexpr (CL == 2) ptx::mma_bf16_pair(d, ptx::sdesc_sw128(a), ptx::sdesc_sw128(b), idesc, acc);
+                else ptx::mma_bf16(d, ptx::sdesc_sw128(a), ptx::sdesc_sw128(b), idesc, acc);
+            };
+            auto next_slot = [&]() -> uint32_t {
+                const int s = it % C::STAGES;
+                wait_lead(&full[s], (it / C::STAGES) & 1);
+                FFN_EV(12, it & 255);
                 ptx::tc_fence_after();
-                for (int j = 0; j <= nch; j++) {
+                return static_cast<uint32_t>(s);
+            };
+            for (int u = unit0; u < units; u += ustride, i++) {
+                wait_lead(a_full, i & 1);
+                ptx::tc_fence_after();
+                for (int j = 0; j < nch + LA; j++) {
                     if (j < nch) {  // FFN1 chunk j -> acc1[b]
                         const int b = c1 & 1;
-                        ptx::mbar_wait(&acc1_empty[b], ((c1 >> 1) & 1) ^ 1);
+                        wait_lead(&acc1_empty[b], ((c1 >> 1) & 1) ^ 1);
+                        FFN_EV(1, j);
                         ptx::tc_fence_after();
-                        for (int kb = 0; kb < C::KB1; kb++, it++) {
-                            const int s = it % C::STAGES;
-                            ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
-                            ptx::tc_fence_after();
+                        for (int p = 0; p < C::S1; p++, it++) {
+                            const uint32_t s = next_slot();
+                            for (int w = 0; w < C::W1_PER_SLOT; w++) {
+                                const int kb = p * C::W1_PER_SLOT + w;
 #pragma unroll
-                            for (int k = 0; k < 4; k++)
-                                ptx::mma_bf16(T_ACC1 + b * C::CH, ptx::sdesc_sw128(a_base + kb * 16384 + k * 32),
-                                              ptx::sdesc_sw128(r_base + s * C::SLOT + k * 32), idesc1, (kb | k) != 0);
-                            ptx::mma_commit(&empty[s]);
+                                for (int k = 0; k < 4; k++)
+                                    mma(T_ACC1 + b * C::CH, a_base + kb * 16384 + k * 32,
+                                        r_base + s * C::SLOT + w * C::W1_BLK + k * 32, idesc1, (kb | k) != 0);
+                            }
+                            commit(&empty[s]);
                         }
-                        ptx::mma_commit(&acc1_full[b]);
+                        commit(&acc1_full[b]);
                         c1++;
-                        if (j == nch - 1) ptx::mma_commit(a_empty);  // the A tile is free once these complete
+                        if (j == nch - 1) commit(a_empty);  // the A tiles are free once these complete
                     }
-                    if (j > 0) {  // FFN2 of chunk j-1: acc2 += H . W2_chunk
+                    if (j >= LA) {  // FFN2 of chunk jj = j - LA: acc2 += H . W2_chunk
+                        const int jj = j - LA;
                         const int hb = c2 & 1;
-                        ptx::mbar_wait(&h_full[hb], (c2 >> 1) & 1);
-                        if (j == 1) ptx::mbar_wait(acc2_empty, (i & 1) ^ 1);
-                        ptx::tc_fence_after();
-                        for (int kb2 = 0; kb2 < 2; kb2++, it++) {
-                            const int s = it % C::STAGES;
-                            ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
+                        wait_lead(&h_full[hb], (c2 >> 1) & 1);
+                        FFN_EV(2, jj);
+                        if (jj == 0) {  // acc2 <- residual rows (tcgen05.cp, ordered before the MMAs)
+                            wait_lead(acc2_empty, (i & 1) ^ 1);
                             ptx::tc_fence_after();
+                            for (int cc = 0; cc < D; cc += 32, it++) {
+                                const uint32_t s = next_slot();
 #pragma unroll
-                            for (int k = 0; k < 4; k++)
-                                ptx::mma_bf16(T_ACC2, ptx::sdesc_sw128(h_base + hb * C::H_BUF + kb2 * 16384 + k * 32),
-                                              ptx::sdesc_sw128(r_base + s * C::SLOT + k * 32), idesc2,
-                                              (j > 1 || kb2 > 0 || k > 0));
-                            ptx::mma_commit(&empty[s]);
+                                for (int k = 0; k < 4; k++) {
+                                    const uint64_t sd = ptx::sdesc_sw128(r_base + s * C::SLOT + k * 32);
+                                    if constexpr (CL == 2) ptx::tmem_cp_128x256b_pair(T_ACC2 + cc + 8 * k, sd);
+                                    else ptx::tmem_cp_128x256b(T_ACC2 + cc + 8 * k, sd);
+                                }
+                                commit(&empty[s]);
+                            }
                         }
-                        ptx::mma_commit(&h_empty[hb]);
+                        ptx::tc_fence_after();
+                        if constexpr (CL == 1 && C::NW2 < D) {
+                            for (int kb2 = 0; kb2 < 2; kb2++)
+                                for (int nh = 0; nh < D / C::NW2; nh++, it++) {
+                                    const uint32_t s = next_slot();
+#pragma unroll
+                                    for (int k = 0; k < 4; k++)
+                                        mma(T_ACC2 + nh * C::NW2, h_base + hb * C::H_BUF + kb2 * 16384 + k * 32,
+                                            r_base + s * C::SLOT + k * 32, idesc2, 1u);
+                                    commit(&empty[s]);
+                                }
+                        } else {
+                            for (int p = 0; p < C::S2; p++, it++) {
+                                const uint32_t s = next_slot();
+                                for (int w = 0; w < C::W2_PER_SLOT; w++) {
+                                    const int kb2 = p * C::W2_PER_SLOT + w;
+#pragma unroll
+                                    for (int k = 0; k < 4; k++)
+                                        mma(T_ACC2, h_base + hb * C::H_BUF + kb2 * 16384 + k * 32,
+                                            r_base + s * C::SLOT + w * C::W2_BLK + k * 32, idesc2, 1u);
+                                }
+                                commit(&empty[s]);
+                            }
+                        }
+                        commit(&h_empty[hb]);
                         c2++;
                     }
                 }
-                ptx::mma_commit(acc2_full);
+                commit(acc2_full);
             }
         }
-    } else if (warp >= 4) {
-        const int ew = warp - 4, q = warp & 3, cg = ew >> 2;
+    } else {
+        const int ew = warp - 2, q = warp & 3, cg = ew >> 2;
         const int r = q * 32 + lane;  // tile row of this thread
         const uint32_t h_base = ptx::smem_u32(sH);
-        const uint32_t F0 = h_base + ew * 8192, H0 = F0 + 4096;  // final-epilogue staging (in the H buffers)
-        const uint32_t rb = ptx::smem_u32(&rbar[ew]);
-        uint32_t c1 = 0, rph = 0, i = 0;
-        float v[32], pp[32];
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
-            const int m0 = t * 128, row_base = m0 + q * 32;
-            // ---- GELU chunks
+        const uint32_t S0 = h_base + ew * C::STG;  // final-epilogue staging (in the H buffers)
+        const bool fin = cg < C::CGF;              // this warp takes part in the final epilogue
+        const int c0 = cg * C::FCOLS;
+        uint32_t c1 = 0, i = 0;
+        for (int u = unit0; u < units; u += ustride, i++) {
+            const int t = u * CL + static_cast<int>(rank);
+            const int m0 = t * 128, row_base = m0 + q * 32, row = row_base + lane;
+            // ---- GELU chunks: this warp owns columns [32 cg, 32 cg + 32) of every chunk
             for (int j = 0; j < nch; j++, c1++) {
                 const int b = c1 & 1;
                 ptx::mbar_wait(&acc1_full[b], (c1 >> 1) & 1);
+                if (lane == 0 && ew == 0) FFN_EV(3, j);
                 ptx::tc_fence_after();
-                float g[64];
-                tmem_load32(T_ACC1 + b * C::CH + cg * 64 + (static_cast<uint32_t>(q * 32) << 16), g);
-                tmem_load32(T_ACC1 + b * C::CH + cg * 64 + 32 + (static_cast<uint32_t>(q * 32) << 16), g + 32);
+                float g[32];
+                tmem_load32(T_ACC1 + b * C::CH + cg * 32 + (static_cast<uint32_t>(q * 32) << 16), g);
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&acc1_empty[b]);
-                const int pc = j * C::CH + cg * 64;
+                if (lane == 0) arrive_lead(&acc1_empty[b]);
+                const int pc = chunk(j) * C::CH + cg * 32;
+#if DCAT_FFN_ABLATE & 1  // kernel micro-bench only (tools/kbench): skip the GELU math
+                if (pc < 0)
+#endif
 #pragma unroll
-                for (int k = 0; k < 64; k += 4) {
+                for (int k = 0; k < 32; k += 4) {
                     float4 bb = lds4(s_par + 4u * (pc + k));
                     g[k] = gelu_fast(g[k] + bb.x);
                     g[k + 1] = gelu_fast(g[k + 1] + bb.y);
@@ -870,101 +1045,122 @@ __global__ void __launch_bounds__(FfnCfg<D>::THREADS, 1)
                     g[k + 3] = gelu_fast(g[k + 3] + bb.w);
                 }
                 ptx::mbar_wait(&h_empty[b], ((c1 >> 1) & 1) ^ 1);
-                // row r of k-block cg of H buffer b: 8 x 16 B chunks, 128 B swizzle
-                const uint32_t rowa = h_base + b * C::H_BUF + cg * 16384 + r * 128;
+                // row r of k-block cg/2 of H buffer b, 16-byte chunks 4 (cg & 1) .. +3, 128 B swizzle
+                const uint32_t rowa = h_base + b * C::H_BUF + (cg >> 1) * 16384 + r * 128;
 #pragma unroll
-                for (int k = 0; k < 8; k++)
-                    sts4u(rowa + ((k ^ (r & 7)) << 4), pack_bf16(g[8 * k], g[8 * k + 1]),
+                for (int k = 0; k < 4; k++)
+                    sts4u(rowa + ((((cg & 1) * 4 + k) ^ (r & 7)) << 4), pack_bf16(g[8 * k], g[8 * k + 1]),
                           pack_bf16(g[8 * k + 2], g[8 * k + 3]), pack_bf16(g[8 * k + 4], g[8 * k + 5]),
                           pack_bf16(g[8 * k + 6], g[8 * k + 7]));
                 fence_async_smem();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&h_full[b]);
+                if (lane == 0) arrive_lead(&h_full[b]);
+                if (lane == 0 && ew == 0) FFN_EV(4, j);
+                if (lane == 0 && ew == 15) FFN_EV(7, j);
             }
-            // ---- residual + LayerNorm on acc2 (all FFN2 MMAs of the tile are done: H buffers free)
-            ptx::mbar_wait(acc2_full, i & 1);
-            ptx::tc_fence_after();
-            const uint32_t tacc = T_ACC2 + (static_cast<uint32_t>(q * 32) << 16);
-            float s1[1] = {0.f};
-            bool bad = false;
+            // ---- residual + LayerNorm
+            if (fin) {
+                // acc2 started as the residual rows (tcgen05.cp): x = acc2 + b2 -> x_out, written
+                // back into acc2 for the LayerNorm passes.
+                const bool live = row < M;
+                const uint32_t tacc = T_ACC2 + (static_cast<uint32_t>(q * 32) << 16) + c0;
+                float v[32];
+                float s1[1] = {0.f};
+                bool bad = false;
+                ptx::mbar_wait(acc2_full, i & 1);
+                ptx::tc_fence_after();
+                if (lane == 0 && ew == 0) FFN_EV(5, 0);
 #pragma unroll 1
-            for (int ch = 0; ch < C::FCOLS / 32; ch++) {
-                const int c = cg * C::FCOLS + ch * 32;
-                if (lane == 0) {
-                    mbar_expect_tx_s(rb, F_BYTES);
-                    tma_load_s(F0, &mp.resid, rb, c, row_base);
-                }
-                mbar_wait_s(rb, rph);
-                rph ^= 1;
-                read_f32_row(F0, lane, pp);
-                tmem_load32(tacc + c, v);
+                for (int h = 0; h < C::FCOLS; h += 32) {
+                    if (h) staging_free<0>(lane);
+                    tmem_load32(tacc + h, v);
 #pragma unroll
-                for (int k = 0; k < 32; k++) v[k] = v[k] + pp[k];  // (acc + resid) + b2, as RESID_LN
-                lds32(s_par, P_B2 + c, pp);
-#pragma unroll
-                for (int k = 0; k < 32; k++) {
-                    v[k] += pp[k];
-                    bad |= !isfinite(v[k]);
-                    s1[0] += v[k];
-                }
-                __syncwarp();
-                write_f32_row(F0, lane, v);
-                store_block(&mp.xout, F0, c, row_base, lane);
-                if (e.ln_g == nullptr && e.ln_out) {
-                    staging_free<1>(lane);
-                    write_bf16_row(H0, lane, v);
-                    store_block(&mp.ln, H0, c, row_base, lane);
-                }
-                tmem_store32(tacc + c, v);
-                staging_free<0>(lane);
-            }
-            if (bad && row_base + lane < M && e.layer_idx >= 0) atomicMax(&e.st->nonfinite_layer, e.layer_idx + 1);
-            if (e.ln_g && e.ln_out) {
-                quad_reduce<C::CG, 1>(s_red, s1, cg, lane, q);
-                const float dn = static_cast<float>(D);
-                const float mu = s1[0] / dn;
-                float var[1] = {0.f};
-#pragma unroll 1
-                for (int ch = 0; ch < C::FCOLS / 32; ch++) {
-                    tmem_load32(tacc + cg * C::FCOLS + ch * 32, v);
+                    for (int j = 0; j < 8; j++) {  // (resid + acc) + b2
+                        const float4 bb = lds4(s_par + 4u * (P_B2 + c0 + h + 4 * j));
+                        float* w = v + 4 * j;
+                        w[0] += bb.x;
+                        w[1] += bb.y;
+                        w[2] += bb.z;
+                        w[3] += bb.w;
+                    }
 #pragma unroll
                     for (int k = 0; k < 32; k++) {
-                        float d0 = v[k] - mu;
-                        var[0] += d0 * d0;
+                        bad |= !isfinite(v[k]);
+                        s1[0] += v[k];
+                    }
+                    __syncwarp();
+#if DCAT_FFN_ABLATE & 2  // kernel micro-bench only (tools/kbench): skip the output stores / LayerNorm
+                    if (m0 < 0)
+#endif
+                    {
+                        write_f32_row(S0, lane, v);
+                        store_block(&mp.xout, S0, c0 + h, row_base, lane);
+                    }
+                    tmem_store32(tacc + h, v);
+                }
+                if (bad && live && e.layer_idx >= 0) atomicMax(&e.st->nonfinite_layer, e.layer_idx + 1);
+#if DCAT_FFN_ABLATE & 2
+                if (m0 < 0)
+#endif
+                if (e.ln_out) {
+                    float mu = 0.f, rs = 1.f;
+                    if (e.ln_g) {
+                        quad_reduce<C::CGF, 1>(s_red, s1, cg, lane, q);
+                        const float dn = static_cast<float>(D);
+                        mu = s1[0] / dn;
+                        float var[1] = {0.f};
+#pragma unroll 1
+                        for (int h = 0; h < C::FCOLS; h += 32) {
+                            tmem_load32(tacc + h, v);
+#pragma unroll
+                            for (int k = 0; k < 32; k++) {
+                                const float d0 = v[k] - mu;
+                                var[0] += d0 * d0;
+                            }
+                        }
+                        quad_reduce<C::CGF, 1>(s_red, var, cg, lane, q);
+                        rs = 1.0f / sqrtf(var[0] / dn + 1e-5f);
+                    }
+                    staging_free<0>(lane);
+#pragma unroll 1
+                    for (int h = 0; h < C::FCOLS; h += 32) {
+                        tmem_load32(tacc + h, v);
+                        if (e.ln_g) {
+#pragma unroll
+                            for (int j = 0; j < 8; j++) {
+                                const float4 gg = lds4(s_par + 4u * (P_G + c0 + h + 4 * j));
+                                const float4 bb = lds4(s_par + 4u * (P_BB + c0 + h + 4 * j));
+                                float* w = v + 4 * j;
+                                w[0] = gg.x * ((w[0] - mu) * rs) + bb.x;
+                                w[1] = gg.y * ((w[1] - mu) * rs) + bb.y;
+                                w[2] = gg.z * ((w[2] - mu) * rs) + bb.z;
+                                w[3] = gg.w * ((w[3] - mu) * rs) + bb.w;
+                            }
+                        }
+                        write_bf16_row(S0 + h * 64, lane, v);
+                        store_block(&mp.ln, S0 + h * 64, c0 + h, row_base, lane);
                     }
                 }
-                quad_reduce<C::CG, 1>(s_red, var, cg, lane, q);
-                const float rs = 1.0f / sqrtf(var[0] / dn + 1e-5f);
-#pragma unroll 1
-                for (int ch = 0; ch < C::FCOLS / 32; ch++) {
-                    const int c = cg * C::FCOLS + ch * 32;
-                    tmem_load32(tacc + c, v);
-                    lds32(s_par, P_G + c, pp);
-#pragma unroll
-                    for (int k = 0; k < 32; k++) v[k] = pp[k] * ((v[k] - mu) * rs);
-                    lds32(s_par, P_BB + c, pp);
-#pragma unroll
-                    for (int k = 0; k < 32; k++) v[k] += pp[k];
-                    staging_free<0>(lane);
-                    write_bf16_row(H0, lane, v);
-                    store_block(&mp.ln, H0, c, row_base, lane);
-                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) arrive_lead(acc2_empty);
+                if (lane == 0 && ew == 0) FFN_EV(6, 0);
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc2_empty);
             // the next tile's GELU writes reuse this staging: all epilogue warps drain first
             staging_free<0>(lane);
             named_bar(5, 32 * C::EPI_WARPS);
+            if (lane == 0 && ew == 0) FFN_EV(9, 0);
         }
         if (lane == 0) bulk_wait_all();
         __syncwarp();
     }
     ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 2) {
+    if constexpr (CL == 2) ptx::cluster_sync();  // the leader's MMAs / commits reach the peer until here
+    else __syncthreads();
+    if (warp == 0) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem, 512);
+        if constexpr (CL == 2) ptx::tmem_dealloc_pair(tmem, 512);
+        else ptx::tmem_dealloc(tmem, 512);
     }
 }
 
@@ -1004,14 +1200,14 @@ CUtensorMap tmap_bf16(const void* base, uint64_t inner, uint64_t outer, uint64_t
 }
 
 // epilogue I/O map: rows x cols matrix (ld elements), 32 x 32 boxes; fp32 -> 128B swizzle, bf16 -> 64B
-CUtensorMap tmap_epi(const void* base, bool f32, uint64_t cols, uint64_t rows, uint64_t ld) {
+CUtensorMap tmap_epi(const void* base, bool f32, uint64_t cols, uint64_t rows, uint64_t ld, uint32_t box_rows = 32) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof m);
     if (!base) return m;
     const uint64_t es = f32 ? 4 : 2;
     cuuint64_t dims[2] = {cols, rows};
     cuuint64_t strides[1] = {ld * es};
-    cuuint32_t box[2] = {32, 32};
+    cuuint32_t box[2] = {32, box_rows};
     cuuint32_t el[2] = {1, 1};
     if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * es) & 15))
         throw CudaError("epilogue tensor map: base / row stride must be 16-byte aligned");
@@ -1097,21 +1293,61 @@ void launch_mode(int BN, const CUtensorMap& ta, const CUtensorMap& tb, int M, in
 }  // namespace
 
 namespace {
-template <int D>
-void launch_ffn(const CUtensorMap& ta, const CUtensorMap& t1, const CUtensorMap& t2, int M, int F, const Epi& e,
+template <int D, int CL>
+void launch_ffn(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M, int F, const Epi& e,
                 const EpiMaps& mp, cudaStream_t s) {
-    using C = FfnCfg<D>;
+    using C = FfnCfg<D, CL>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
     static std::once_flag once;
     std::call_once(once, [] {
-        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_ffn_tc<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_ffn_tc<D, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     });
-    const int tiles = (M + 127) / 128;
-    const int grid = tiles < num_sms() ? tiles : num_sms();
-    k_ffn_tc<D><<<grid, C::THREADS, C::SMEM, s>>>(ta, t1, t2, M, F, e, mp);
-    DCAT_LAUNCH_CHECK();
+    const CUtensorMap ta = tmap_bf16(A, static_cast<uint64_t>(D), static_cast<uint64_t>(M),
+                                     static_cast<uint64_t>(lda) * 2, 128);
+    const CUtensorMap t1 = tmap_bf16(W1t, static_cast<uint64_t>(D), static_cast<uint64_t>(F),
+                                     static_cast<uint64_t>(D) * 2, static_cast<uint32_t>(C::W1_ROWS));
+    const CUtensorMap t2 = tmap_bf16(W2t, static_cast<uint64_t>(F), static_cast<uint64_t>(D),
+                                     static_cast<uint64_t>(F) * 2, static_cast<uint32_t>(C::W2_ROWS));
+    EpiMaps mpf = mp;  // residual in [128 x 32] fp32 blocks: one ring slot each, copied into acc2
+    mpf.resid = tmap_epi(e.resid, true, static_cast<uint64_t>(D), static_cast<uint64_t>(M), e.ld_x, 128);
+    const int units = ((M + 127) / 128 + CL - 1) / CL;
+    const int per = num_sms() / CL;
+    const int grid = CL * (units < per ? units : per);
+    if constexpr (CL == 1) {
+        k_ffn_tc<D, 1><<<grid, C::THREADS, C::SMEM, s>>>(ta, t1, t2, M, F, e, mpf);
+        DCAT_LAUNCH_CHECK();
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(C::THREADS);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        DCAT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_ffn_tc<D, CL>, ta, t1, t2, M, F, e, mpf));
+    }
 }
 }  // namespace
+
+#if DCAT_FFN_TRACE
+void ffn_trace_reset() {
+    unsigned z = 0;
+    DCAT_CUDA_CHECK(cudaMemcpyToSymbol(g_ffn_trace_n, &z, sizeof(z)));
+}
+int ffn_trace_read(unsigned long long* out, int cap) {
+    unsigned n = 0;
+    DCAT_CUDA_CHECK(cudaMemcpyFromSymbol(&n, g_ffn_trace_n, sizeof(n)));
+    if (n > 8192u) n = 8192u;
+    if (static_cast<int>(n) > cap) n = static_cast<unsigned>(cap);
+    DCAT_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_ffn_trace, n * sizeof(unsigned long long)));
+    return static_cast<int>(n);
+}
+#endif
 
 bool ffn_tc_supported(int D, int F) { return (D == 64 || D == 128 || D == 256) && F % 128 == 0 && F <= 1024; }
 
@@ -1119,19 +1355,22 @@ void ffn_tc(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M, int
             cudaStream_t s) {
     if (M <= 0) return;
     if (!ffn_tc_supported(D, F)) throw InvalidArg("ffn_tc: unsupported shape");
-    CUtensorMap ta = tmap_bf16(A, static_cast<uint64_t>(D), static_cast<uint64_t>(M), static_cast<uint64_t>(lda) * 2,
-                               128);
-    CUtensorMap t1 = tmap_bf16(W1t, static_cast<uint64_t>(D), static_cast<uint64_t>(F), static_cast<uint64_t>(D) * 2,
-                               128);
-    CUtensorMap t2 = tmap_bf16(W2t, static_cast<uint64_t>(F), static_cast<uint64_t>(D), static_cast<uint64_t>(F) * 2,
-                               static_cast<uint32_t>(D));
     Epi em = e;
     em.mode = EPI_RESID_LN;
     const EpiMaps mp = make_maps(em, M, D);
+    // One CTA per 128-row tile. DCAT_FFN_PAIR=1 selects the CTA-pair kernel (M = 256 per pair,
+    // half the weight bytes per SM); it measured slower on the PinFM-base step (profiles/r01_ffn.md).
+    static const bool single = getenv("DCAT_FFN_PAIR") == nullptr;
     switch (D) {
-        case 64: launch_ffn<64>(ta, t1, t2, M, F, e, mp, s); break;
-        case 128: launch_ffn<128>(ta, t1, t2, M, F, e, mp, s); break;
-        default: launch_ffn<256>(ta, t1, t2, M, F, e, mp, s); break;
+        case 64: launch_ffn<64, 1>(A, lda, W1t, W2t, M, F, e, mp, s); break;
+        case 128:
+            if (single) launch_ffn<128, 1>(A, lda, W1t, W2t, M, F, e, mp, s);
+            else launch_ffn<128, 2>(A, lda, W1t, W2t, M, F, e, mp, s);
+            break;
+        default:
+            if (single) launch_ffn<256, 1>(A, lda, W1t, W2t, M, F, e, mp, s);
+            else launch_ffn<256, 2>(A, lda, W1t, W2t, M, F, e, mp, s);
+            break;
     }
 }
 

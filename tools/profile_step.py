@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="pinfm-base")
 ap.add_argument("--calls", type=int, default=2)
 ap.add_argument("--users", type=int, default=0)
+ap.add_argument("--stages", action="store_true", help="print per-stage device times of the last call")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 U = a.users or cfg["U"]
@@ -27,6 +28,9 @@ dev = host.to(lambda x: torch.from_numpy(x.view(np.int64) if x.dtype == np.uint6
 m = api.DcatModel(w)
 ft = FinetuneSpec(max_events=cfg["L"])
 for _ in range(a.calls):
-    lg, ml, _ = m.rank_forward_batch(dev, ft)
+    lg, ml, _ = m.rank_forward_batch(dev, ft, profile=a.stages)
 torch.cuda.synchronize()
 print("ok", float(lg.float().abs().mean()))
+if a.stages:  # per-stage device times (ms) of the last call
+    for n, v in sorted(m.stage_times().items(), key=lambda kv: -kv[1]):
+        print(f"{n:28s} {v:8.4f}")
