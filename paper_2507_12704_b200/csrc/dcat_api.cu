@@ -314,7 +314,7 @@ void run_dedup(dcat_model* m, const Staged& sb, const DedupOut& o, cudaStream_t 
     uint64_t mask = debug_hash_mask();
     const int kTileCtx = m->tile_ctx, kTileCross = m->tile_cross;
     dedup_plan(sb.in, o, mask, kTileCtx, kTileCross, s);
-    m->stats.kernel_launches += 23;
+    m->stats.kernel_launches += 27;
     DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
     DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
     if (m->st_host->collisions > 0 && m->st_host->err_bits == 0) {

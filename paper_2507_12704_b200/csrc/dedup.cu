@@ -37,14 +37,9 @@ __device__ void record_error(Status* st, int bit, int row, int val) {
     if (row < prev) atomicExch(&st->err_val, val);
 }
 
-// one warp per row: content hash + validation (round 0 only)
-__global__ void k_hash(DedupIn in, const int32_t* rows, const int32_t* n_rows_dev, int64_t n_rows, uint64_t seed,
-                       uint64_t mask, uint64_t* hash, Status* st, int validate) {
-    int64_t n = n_rows_dev ? *n_rows_dev : n_rows;
-    int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (w >= n) return;
-    int r = rows ? rows[w] : static_cast<int>(w);
+// content hash of row r (one warp) + validation of its events (round 0)
+__device__ void hash_row(const DedupIn& in, int r, uint64_t seed, uint64_t mask, uint64_t* hash, Status* st,
+                         int validate, int lane) {
     int valid = in.row_valid[r];
     int64_t off = in.row_offset[r];
     if (validate) {
@@ -77,6 +72,66 @@ __global__ void k_hash(DedupIn in, const int32_t* rows, const int32_t* n_rows_de
         uint64_t h = mix64(acc ^ mix64(static_cast<uint64_t>(valid) + seed)) & mask;
         if (h == kEmpty) h = kEmpty - 1;
         hash[r] = h;
+    }
+}
+
+__global__ void k_hash(DedupIn in, const int32_t* rows, const int32_t* n_rows_dev, int64_t n_rows, uint64_t seed,
+                       uint64_t mask, uint64_t* hash, Status* st, int validate) {
+    const int64_t n = n_rows_dev ? *n_rows_dev : n_rows;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n; w += nw) {
+        const int r = rows ? rows[w] : static_cast<int>(w);
+        hash_row(in, r, seed, mask, hash, st, validate, lane);
+    }
+}
+
+// span fast path (round 0): rows with the same (row_offset, row_valid) are the same key
+// (dcat.cpp:45-56 compares contents; a shared span trivially compares equal), so only one
+// row per distinct span is content-hashed. k_span also performs the per-row range checks.
+constexpr uint64_t kSpanOffLimit = 1ull << 42;
+__global__ void k_span(DedupIn in, uint64_t* tkey, int32_t* tval, int64_t cap, int32_t* span_slot, Status* st) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= in.B) return;
+    const int r = static_cast<int>(i);
+    const int valid = in.row_valid[r];
+    const int64_t off = in.row_offset[r];
+    span_slot[r] = -1;
+    if (valid < 0 || off < 0 || off + valid > in.n_events) {
+        record_error(st, ERR_RANGE, r, valid);
+        return;
+    }
+    if (in.pos_learned) {
+        if (valid > in.max_len) record_error(st, ERR_POS_CTX, r, valid - 1 >= in.max_len ? in.max_len : valid);
+        else if (valid >= in.max_len) record_error(st, ERR_POS_CAND, r, valid);
+    }
+    if (static_cast<uint64_t>(off) >= kSpanOffLimit || valid >= (1 << 21)) return;  // hashed on its own
+    const uint64_t key = (static_cast<uint64_t>(off) << 21) | static_cast<uint64_t>(valid);
+    const uint64_t m = static_cast<uint64_t>(cap - 1);
+    for (uint64_t s = mix64(key) & m;; s = (s + 1) & m) {
+        const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long*>(tkey + s), kEmpty, key);
+        if (prev == kEmpty || prev == key) {
+            atomicMin(tval + s, r);
+            span_slot[r] = static_cast<int32_t>(s);
+            return;
+        }
+    }
+}
+// rows to content-hash: the first row of every span, and rows outside the span path
+__global__ void k_span_reps(int64_t B, const int32_t* span_slot, const int32_t* tval, const Status* st,
+                            int32_t* list, int32_t* list_n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= B) return;
+    const int s = span_slot[i];
+    if (s >= 0 ? tval[s] == static_cast<int32_t>(i) : true) list[atomicAdd(list_n, 1)] = static_cast<int32_t>(i);
+}
+__global__ void k_span_copy(int64_t B, const int32_t* span_slot, const int32_t* tval, uint64_t* hash) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= B) return;
+    const int s = span_slot[i];
+    if (s >= 0) {
+        const int h = tval[s];
+        if (h != static_cast<int32_t>(i)) hash[i] = hash[h];
     }
 }
 
@@ -119,17 +174,34 @@ __device__ bool same_key(const DedupIn& in, int a, int b, int lane) {
 __global__ void k_head_verify(DedupIn in, const int32_t* rows, const int32_t* n_rows_dev, int64_t n_rows,
                               const int32_t* slot, const int32_t* tval, int32_t* head, int32_t* collided,
                               Status* st) {
-    int64_t n = n_rows_dev ? *n_rows_dev : n_rows;
-    int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (w >= n) return;
-    int r = rows ? rows[w] : static_cast<int>(w);
-    int h = tval[slot[r]];
-    bool ok = (h == r) || same_key(in, r, h, lane);
-    if (lane == 0) {
-        head[r] = ok ? h : r;
-        collided[r] = ok ? 0 : 1;
-        if (!ok) atomicAdd(&st->collisions, 1);
+    const int64_t n = n_rows_dev ? *n_rows_dev : n_rows;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < n; w += nw) {
+        const int r = rows ? rows[w] : static_cast<int>(w);
+        const int h = tval[slot[r]];
+        const bool ok = (h == r) || same_key(in, r, h, lane);
+        if (lane == 0) {
+            head[r] = ok ? h : r;
+            collided[r] = ok ? 0 : 1;
+            if (!ok) atomicAdd(&st->collisions, 1);
+        }
+    }
+}
+
+// round 0, one thread per row: rows whose table head is themselves or shares their event span
+// are settled here; the rest go to a list for the warp-cooperative content comparison
+__global__ void k_verify_fast(DedupIn in, const int32_t* slot, const int32_t* tval, int32_t* head,
+                              int32_t* collided, int32_t* list, int32_t* list_n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= in.B) return;
+    const int r = static_cast<int>(i);
+    const int h = tval[slot[r]];
+    if (h == r || (in.row_valid[r] == in.row_valid[h] && in.row_offset[r] == in.row_offset[h])) {
+        head[r] = h;
+        collided[r] = 0;
+    } else {
+        list[atomicAdd(list_n, 1)] = r;
     }
 }
 
@@ -330,6 +402,11 @@ __global__ void k_tiles(DedupIn in, const int32_t* first, const int32_t* cnt, co
 }
 
 inline unsigned grid_for(int64_t n, int per_block) { return static_cast<unsigned>((n + per_block - 1) / per_block); }
+// grid for the grid-stride warp-per-row kernels (256 threads): <= 8 resident blocks per SM
+inline unsigned warp_grid(int64_t rows) {
+    const int64_t g = (rows * 32 + 255) / 256;
+    return static_cast<unsigned>(g < 148 * 8 ? (g > 0 ? g : 1) : 148 * 8);
+}
 
 }  // namespace
 
@@ -370,10 +447,19 @@ void dedup_plan(const DedupIn& in, const DedupOut& o, uint64_t hash_mask, int ti
     DCAT_CUDA_CHECK(cudaMemsetAsync(&o.st->err_row, 0x7f, sizeof(int), s));
     DCAT_CUDA_CHECK(cudaMemsetAsync(o.tab_key, 0xff, sizeof(uint64_t) * o.tab_cap, s));
     DCAT_CUDA_CHECK(cudaMemsetAsync(o.tab_val, 0x7f, sizeof(int32_t) * o.tab_cap, s));
-    k_hash<<<grid_for(B * 32, 256), 256, 0, s>>>(in, nullptr, nullptr, B, 0, hash_mask, o.hash, o.st, 1);
+    // span fast path: content-hash one row per distinct (offset, valid) span, copy to the rest
+    DCAT_CUDA_CHECK(cudaMemsetAsync(o.list_n, 0, sizeof(int32_t), s));
+    k_span<<<grid_for(B, 256), 256, 0, s>>>(in, o.tab_key, o.tab_val, o.tab_cap, o.cursor, o.st);
+    k_span_reps<<<grid_for(B, 256), 256, 0, s>>>(B, o.cursor, o.tab_val, o.st, o.list, o.list_n);
+    k_hash<<<warp_grid(B), 256, 0, s>>>(in, o.list, o.list_n, 0, 0, hash_mask, o.hash, o.st, 1);
+    k_span_copy<<<grid_for(B, 256), 256, 0, s>>>(B, o.cursor, o.tab_val, o.hash);
+    DCAT_CUDA_CHECK(cudaMemsetAsync(o.tab_key, 0xff, sizeof(uint64_t) * o.tab_cap, s));
+    DCAT_CUDA_CHECK(cudaMemsetAsync(o.tab_val, 0x7f, sizeof(int32_t) * o.tab_cap, s));
+    // content-hash table: head = first row with the same key, verified by comparing contents
     k_insert<<<grid_for(B, 256), 256, 0, s>>>(nullptr, nullptr, B, o.hash, o.tab_key, o.tab_val, o.tab_cap, o.slot);
-    k_head_verify<<<grid_for(B * 32, 256), 256, 0, s>>>(in, nullptr, nullptr, B, o.slot, o.tab_val, o.head,
-                                                         o.collided, o.st);
+    DCAT_CUDA_CHECK(cudaMemsetAsync(o.list_n, 0, sizeof(int32_t), s));
+    k_verify_fast<<<grid_for(B, 256), 256, 0, s>>>(in, o.slot, o.tab_val, o.head, o.collided, o.list, o.list_n);
+    k_head_verify<<<warp_grid(B), 256, 0, s>>>(in, o.list, o.list_n, 0, o.slot, o.tab_val, o.head, o.collided, o.st);
     DCAT_LAUNCH_CHECK();
     finish_plan(in, o, tile_ctx, tile_cross, s);
 }
@@ -388,7 +474,7 @@ void dedup_repair(const DedupIn& in, const DedupOut& o, int n_collided, int tile
         if (round <= kRounds) {
             DCAT_CUDA_CHECK(cudaMemsetAsync(o.tab_key, 0xff, sizeof(uint64_t) * o.tab_cap, s));
             DCAT_CUDA_CHECK(cudaMemsetAsync(o.tab_val, 0x7f, sizeof(int32_t) * o.tab_cap, s));
-            unsigned g32 = grid_for(static_cast<int64_t>(n_collided) * 32, 256);
+            unsigned g32 = warp_grid(n_collided);
             k_hash<<<g32, 256, 0, s>>>(in, o.list, o.list_n, 0, 0x9e3779b97f4a7c15ull * round, hash_mask, o.hash,
                                        o.st, 0);
             k_insert<<<grid_for(n_collided, 256), 256, 0, s>>>(o.list, o.list_n, 0, o.hash, o.tab_key, o.tab_val,

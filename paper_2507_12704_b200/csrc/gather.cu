@@ -36,51 +36,148 @@ __device__ __forceinline__ float4 add4(float4 a, float4 b) {
     return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
 }
 
-__device__ __forceinline__ float4 lookup4(const EmbParams& ep, uint64_t item, int c) {
-    int j = c / ep.d_sub;
-    int cc = c - j * ep.d_sub;
-    uint32_t r = static_cast<uint32_t>(mix64(item ^ ep.seed_mix[j]) % static_cast<uint64_t>(ep.R));
-    return __ldg(reinterpret_cast<const float4*>(ep.table + (static_cast<size_t>(j) * ep.R + r) * ep.d_sub + cc));
+// hash_id(item, seed_j, R) = mix64(item ^ mix64(seed_j)) % R (embed.cpp:11-14)
+__device__ __forceinline__ uint32_t table_row(const EmbParams& ep, uint64_t item, int j) {
+    const uint64_t h = mix64(item ^ ep.seed_mix[j]);
+    const uint64_t R = static_cast<uint64_t>(ep.R);
+    return static_cast<uint32_t>((R & (R - 1)) == 0 ? (h & (R - 1)) : h % R);
+}
+// The J sub-table rows of one item are hashed once per warp: lane j (< J <= 32) holds row j
+// and lanes fetch it by shuffle. Every lane must call this (all 32 take part in the shuffle).
+__device__ __forceinline__ uint32_t warp_rows(const EmbParams& ep, uint64_t item, int lane) {
+    return lane < ep.J ? table_row(ep, item, lane) : 0u;
+}
+__device__ __forceinline__ const float* sub_row(const EmbParams& ep, uint32_t rows, int c, int lane_c) {
+    const int j = lane_c / ep.d_sub;
+    const uint32_t r = ep.J <= 32 ? __shfl_sync(0xffffffffu, rows, j & 31) : 0u;
+    return ep.table + (static_cast<size_t>(j) * ep.R + r) * ep.d_sub + (c - j * ep.d_sub);
+}
+__device__ __forceinline__ float4 lookup4(const EmbParams& ep, uint64_t item, uint32_t rows, int c) {
+    const int cl = c < ep.d_emb ? c : ep.d_emb - 1;  // inactive lanes shuffle a valid source lane
+    const float* p = sub_row(ep, rows, cl, cl);
+    if (ep.J > 32) {
+        const int j = cl / ep.d_sub;
+        p = ep.table + (static_cast<size_t>(j) * ep.R + table_row(ep, item, j)) * ep.d_sub + (cl - j * ep.d_sub);
+    }
+    return c < ep.d_emb ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ float lookup1(const EmbParams& ep, uint64_t item, uint32_t rows, int c) {
+    const int cl = c < ep.d_emb ? c : ep.d_emb - 1;
+    const float* p = sub_row(ep, rows, cl, cl);
+    if (ep.J > 32) {
+        const int j = cl / ep.d_sub;
+        p = ep.table + (static_cast<size_t>(j) * ep.R + table_row(ep, item, j)) * ep.d_sub + (cl - j * ep.d_sub);
+    }
+    return c < ep.d_emb ? __ldg(p) : 0.f;
 }
 
-__device__ __forceinline__ float lookup1(const EmbParams& ep, uint64_t item, int c) {
-    int j = c / ep.d_sub;
-    int cc = c - j * ep.d_sub;
-    uint32_t r = static_cast<uint32_t>(mix64(item ^ ep.seed_mix[j]) % static_cast<uint64_t>(ep.R));
-    return __ldg(ep.table + (static_cast<size_t>(j) * ep.R + r) * ep.d_sub + cc);
+// this lane's 4-column groups of a d_emb row (c = 128 k + 4 lane): sub-table j and offset
+// in it, computed once per kernel instead of once per token
+constexpr int kMaxSteps = 8;  // d_emb <= 1024 on the vectorised path
+struct LaneCols {
+    int j[kMaxSteps], cc[kMaxSteps];
+};
+__device__ __forceinline__ LaneCols lane_cols(const EmbParams& ep, int lane) {
+    LaneCols L;
+#pragma unroll
+    for (int k = 0; k < kMaxSteps; k++) {
+        int c = 128 * k + 4 * lane;
+        c = c < ep.d_emb ? c : ep.d_emb - 4;
+        L.j[k] = c / ep.d_sub;
+        L.cc[k] = c - L.j[k] * ep.d_sub;
+    }
+    return L;
 }
-
-template <typename T, bool VEC>
-__global__ void k_gather_ctx(DedupIn in, const int32_t* __restrict__ first, const int64_t* __restrict__ tok_off,
-                             EmbParams ep, const int32_t* __restrict__ tok_unique, int64_t T_ctx, T* __restrict__ E,
-                             int ldE) {
-    int64_t t = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (t >= T_ctx) return;
-    int u = tok_unique[t];
-    int i = static_cast<int>(t - tok_off[u]);
-    int64_t ev = in.row_offset[first[u]] + i;
-    uint64_t item = in.item[ev];
-    int a = in.action[ev], s = in.surface[ev];
+// vectorised token row: all lanes shuffle (uniform trip count), inactive lanes skip the I/O
+template <typename T>
+__device__ __forceinline__ void gather_ctx_token_vec(const EmbParams& ep, const LaneCols& L, int64_t t, int i,
+                                                     uint64_t item, int a, int s, T* __restrict__ E, int ldE,
+                                                     int lane) {
+    const uint32_t rows = warp_rows(ep, item, lane);
     const float* ae = ep.action_emb + static_cast<size_t>(a) * ep.d_emb;
     const float* se = ep.surface_emb + static_cast<size_t>(s) * ep.d_emb;
     const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(i) * ep.d_emb : nullptr;
     T* out = E + t * ldE;
-    if constexpr (VEC) {
-        for (int c = lane * 4; c < ep.d_emb; c += 128) {
-            float4 v = lookup4(ep, item, c);
+#pragma unroll
+    for (int k = 0; k < kMaxSteps; k++) {
+        if (128 * k >= ep.d_emb) break;
+        const int c = 128 * k + 4 * lane;
+        const uint32_t r = __shfl_sync(0xffffffffu, rows, L.j[k] & 31);
+        if (c < ep.d_emb) {
+            const float* tp = ep.table + (static_cast<size_t>(L.j[k]) * ep.R + r) * ep.d_sub + L.cc[k];
+            float4 v = __ldg(reinterpret_cast<const float4*>(tp));
             v = add4(v, __ldg(reinterpret_cast<const float4*>(ae + c)));
             v = add4(v, __ldg(reinterpret_cast<const float4*>(se + c)));
             if (pe) v = add4(v, __ldg(reinterpret_cast<const float4*>(pe + c)));
             store4<T>(out + c, v);
         }
-    } else {
-        for (int c = lane; c < ep.d_emb; c += 32) {
-            float v = lookup1(ep, item, c);
-            v = v + ae[c];
-            v = v + se[c];
-            if (pe) v = v + pe[c];
-            ActIO<T>::store(out + c, v);
+    }
+}
+
+// one context token row (one warp): E[t] = ((lookup + action) + surface) + pos, model.cpp:517-540
+template <typename T, bool VEC>
+__device__ __forceinline__ void gather_ctx_token(const EmbParams& ep, int64_t t, int i, uint64_t item, int a, int s,
+                                                 T* __restrict__ E, int ldE, int lane) {
+    {
+        const uint32_t rows = warp_rows(ep, item, lane);
+        const float* ae = ep.action_emb + static_cast<size_t>(a) * ep.d_emb;
+        const float* se = ep.surface_emb + static_cast<size_t>(s) * ep.d_emb;
+        const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(i) * ep.d_emb : nullptr;
+        T* out = E + t * ldE;
+        if constexpr (VEC) {
+            for (int c0 = 0; c0 < ep.d_emb; c0 += 128) {
+                const int c = c0 + lane * 4;
+                float4 v = lookup4(ep, item, rows, c);
+                if (c < ep.d_emb) {
+                    v = add4(v, __ldg(reinterpret_cast<const float4*>(ae + c)));
+                    v = add4(v, __ldg(reinterpret_cast<const float4*>(se + c)));
+                    if (pe) v = add4(v, __ldg(reinterpret_cast<const float4*>(pe + c)));
+                    store4<T>(out + c, v);
+                }
+            }
+        } else {
+            for (int c0 = 0; c0 < ep.d_emb; c0 += 32) {
+                const int c = c0 + lane;
+                float v = lookup1(ep, item, rows, c);
+                if (c < ep.d_emb) {
+                    v = v + ae[c];
+                    v = v + se[c];
+                    if (pe) v = v + pe[c];
+                    ActIO<T>::store(out + c, v);
+                }
+            }
+        }
+    }
+}
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(256, 4) k_gather_ctx(DedupIn in, const int32_t* __restrict__ first, const int64_t* __restrict__ tok_off,
+                             EmbParams ep, const int32_t* __restrict__ tok_unique, int64_t T_ctx, T* __restrict__ E,
+                             int ldE) {
+    constexpr int TOK = 8;  // tokens per warp step: lanes 0..7 resolve their metadata in parallel
+    const int lane = threadIdx.x & 31;
+    const LaneCols L = lane_cols(ep, lane);
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t tb = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * TOK; tb < T_ctx;
+         tb += nw * TOK) {
+        int mi = 0, ma = 0, ms = 0;
+        uint64_t mitem = 0;
+        if (lane < TOK && tb + lane < T_ctx) {
+            const int64_t t = tb + lane;
+            const int u = tok_unique[t];
+            mi = static_cast<int>(t - tok_off[u]);
+            const int64_t ev = in.row_offset[first[u]] + mi;
+            mitem = in.item[ev];
+            ma = in.action[ev];
+            ms = in.surface[ev];
+        }
+        const int nt = T_ctx - tb < TOK ? static_cast<int>(T_ctx - tb) : TOK;
+        for (int k = 0; k < nt; k++) {
+            const int ti = __shfl_sync(0xffffffffu, mi, k), ta = __shfl_sync(0xffffffffu, ma, k);
+            const int ts = __shfl_sync(0xffffffffu, ms, k);
+            const uint64_t titem = __shfl_sync(0xffffffffu, mitem, k);
+            if constexpr (VEC) gather_ctx_token_vec<T>(ep, L, tb + k, ti, titem, ta, ts, E, ldE, lane);
+            else gather_ctx_token<T, VEC>(ep, tb + k, ti, titem, ta, ts, E, ldE, lane);
         }
     }
 }
@@ -100,23 +197,23 @@ __device__ float ctx_feature(int k, double age, int valid, int last_surface, int
 }
 
 template <typename T>
-__global__ void k_gather_cand(DedupIn in, const int32_t* __restrict__ perm, const int32_t* __restrict__ rep,
-                              const int32_t* __restrict__ first, EmbParams ep, CandParams cp, int64_t B,
-                              T* __restrict__ E, int ldE, T* __restrict__ feat, Status* st) {
-    int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    int lane = threadIdx.x & 31;
-    if (p >= B) return;
+__device__ void gather_cand_row(DedupIn in, const int32_t* __restrict__ perm, const int32_t* __restrict__ rep,
+                                const int32_t* __restrict__ first, const EmbParams& ep, const CandParams& cp,
+                                int64_t p, T* __restrict__ E, int ldE, T* __restrict__ feat, Status* st, int lane) {
     int i = perm[p];
     int n = in.row_valid[first[rep[i]]];
     uint64_t item = cp.candidate[i];
+    const uint32_t rows = warp_rows(ep, item, lane);
     const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(n) * ep.d_emb : nullptr;
     const float* aux = cp.variant_aux ? cp.aux + static_cast<size_t>(i) * cp.d_aux : nullptr;
     T* out = E + p * ldE;
     T* fo = feat ? feat + p * cp.feat_ld : nullptr;
     bool vec = (ep.d_sub % 4) == 0 && (ep.d_emb % 4) == 0;
     if (vec) {
-        for (int c = lane * 4; c < ep.d_emb; c += 128) {
-            float4 raw = lookup4(ep, item, c);
+        for (int c0 = 0; c0 < ep.d_emb; c0 += 128) {
+            const int c = c0 + lane * 4;
+            float4 raw = lookup4(ep, item, rows, c);
+            if (c >= ep.d_emb) continue;
             if (fo) store4<T>(fo + cp.d_model + c, raw);
             float4 v = raw;
             if (pe) v = add4(v, __ldg(reinterpret_cast<const float4*>(pe + c)));
@@ -133,8 +230,10 @@ __global__ void k_gather_cand(DedupIn in, const int32_t* __restrict__ perm, cons
             store4<T>(out + c, v);
         }
     } else {
-        for (int c = lane; c < ep.d_emb; c += 32) {
-            float raw = lookup1(ep, item, c);
+        for (int c0 = 0; c0 < ep.d_emb; c0 += 32) {
+            const int c = c0 + lane;
+            float raw = lookup1(ep, item, rows, c);
+            if (c >= ep.d_emb) continue;
             if (fo) ActIO<T>::store(fo + cp.d_model + c, raw);
             float v = raw;
             if (pe) v = v + pe[c];
@@ -161,14 +260,30 @@ __global__ void k_gather_cand(DedupIn in, const int32_t* __restrict__ perm, cons
     }
 }
 
+template <typename T>
+__global__ void k_gather_cand(DedupIn in, const int32_t* __restrict__ perm, const int32_t* __restrict__ rep,
+                              const int32_t* __restrict__ first, EmbParams ep, CandParams cp, int64_t B,
+                              T* __restrict__ E, int ldE, T* __restrict__ feat, Status* st) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; p < B; p += nw)
+        gather_cand_row(in, perm, rep, first, ep, cp, p, E, ldE, feat, st, lane);
+}
+
+// grid for the grid-stride warp-per-row kernels (256 threads): <= 8 resident blocks per SM
+inline unsigned warp_grid(int64_t rows) {
+    const int64_t g = (rows * 32 + 255) / 256;
+    return static_cast<unsigned>(g < 148 * 8 ? (g > 0 ? g : 1) : 148 * 8);
+}
+
 }  // namespace
 
 template <typename T>
 void gather_context(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const int32_t* tok_unique,
                     int64_t T_ctx, T* E, int ldE, cudaStream_t s) {
     if (T_ctx <= 0) return;
-    unsigned g = static_cast<unsigned>((T_ctx * 32 + 255) / 256);
-    if ((ep.d_sub % 4) == 0 && (ep.d_emb % 4) == 0 && (ldE % 4) == 0)
+    const unsigned g = warp_grid(T_ctx);
+    if ((ep.d_sub % 4) == 0 && (ep.d_emb % 4) == 0 && (ldE % 4) == 0 && ep.d_emb <= 128 * 8 && ep.J <= 32)
         k_gather_ctx<T, true><<<g, 256, 0, s>>>(in, o.first, o.tok_off, ep, tok_unique, T_ctx, E, ldE);
     else
         k_gather_ctx<T, false><<<g, 256, 0, s>>>(in, o.first, o.tok_off, ep, tok_unique, T_ctx, E, ldE);
@@ -179,7 +294,7 @@ template <typename T>
 void gather_candidates(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const CandParams& cp, int64_t B,
                        T* E, int ldE, T* feat, cudaStream_t s) {
     if (B <= 0) return;
-    unsigned g = static_cast<unsigned>((B * 32 + 255) / 256);
+    const unsigned g = warp_grid(B);
     k_gather_cand<T><<<g, 256, 0, s>>>(in, o.perm, o.rep, o.first, ep, cp, B, E, ldE, feat, o.st);
     DCAT_LAUNCH_CHECK();
 }
