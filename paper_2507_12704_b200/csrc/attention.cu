@@ -84,8 +84,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_flash(AttnArgs p) {
     const uint32_t sK0 = sQ + C::Q_ELEMS * 2;
     const uint32_t sV0 = sK0 + 2 * C::KV_ELEMS * 2;
 
-    const Tile tile = p.tiles[blockIdx.x];
-    const int h = blockIdx.y;
+    // linear grid, head fastest: the heads of one tile run together and share its K/V lines in L2
+    const Tile tile = p.tiles[blockIdx.x / p.n_heads];
+    const int h = blockIdx.x % p.n_heads;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t4 = lane & 3;
     const bf16* Q = static_cast<const bf16*>(p.q);
@@ -283,8 +284,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_flash(AttnArgs p) {
 template <typename T>
 __global__ void k_attn_simt(AttnArgs p, int max_keys) {
     extern __shared__ float logits_all[];
-    const Tile tile = p.tiles[blockIdx.x];
-    const int h = blockIdx.y;
+    // linear grid, head fastest: the heads of one tile run together and share its K/V lines in L2
+    const Tile tile = p.tiles[blockIdx.x / p.n_heads];
+    const int h = blockIdx.x % p.n_heads;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     float* logits = logits_all + warp * (max_keys + 1);
     const T* Q = static_cast<const T*>(p.q);
@@ -331,7 +333,7 @@ template <typename T>
 void launch_simt(const AttnArgs& a, cudaStream_t s) {
     const int warps = 4;
     size_t smem = static_cast<size_t>(warps) * (a.max_keys + 2) * sizeof(float);
-    dim3 grid(a.n_tiles, a.n_heads);
+    const dim3 grid(static_cast<unsigned>(a.n_tiles) * static_cast<unsigned>(a.n_heads));
     if (smem > 48 * 1024)
         DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_attn_simt<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(smem)));
@@ -347,7 +349,7 @@ void launch_flash_t(const AttnArgs& a, cudaStream_t s) {
         DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_flash<DH, CAUSAL, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM));
     });
-    dim3 grid(a.n_tiles, a.n_heads);
+    const dim3 grid(static_cast<unsigned>(a.n_tiles) * static_cast<unsigned>(a.n_heads));
     k_flash<DH, CAUSAL, WARPS><<<grid, WARPS * 32, C::SMEM, s>>>(a);
     DCAT_LAUNCH_CHECK();
 }

@@ -97,8 +97,9 @@ __global__ void __launch_bounds__(256, 2)
     uint64_t* bar_oread = bars + 5;  // O_chunk read back (4 softmax warps)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
 
-    const Tile tile = p.tiles[blockIdx.x];
-    const int h = blockIdx.y, hc = h * DH;
+    // linear grid, head fastest: the heads of one tile run together and share its K/V lines in L2
+    const Tile tile = p.tiles[blockIdx.x / p.n_heads];
+    const int h = blockIdx.x % p.n_heads, hc = h * DH;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // Key chunks start at kv0 rounded down to 8 tokens: the V^T box's inner (token)
     // coordinate must be 16-byte aligned for TMA. S column j of chunk c is key
@@ -339,7 +340,7 @@ void launch_tc(const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t 
     CUtensorMap tk = map2d(a.k, static_cast<uint64_t>(d), static_cast<uint64_t>(kv_rows), a.ldkv, DH, C::KC, sw);
     CUtensorMap tv = map2d(a.v, static_cast<uint64_t>(a.ldvt), static_cast<uint64_t>(d), a.ldvt, 64, DH,
                            CU_TENSOR_MAP_SWIZZLE_128B);
-    dim3 grid(a.n_tiles, a.n_heads);
+    const dim3 grid(static_cast<unsigned>(a.n_tiles) * static_cast<unsigned>(a.n_heads));
     k_attn_tc<DH, CAUSAL><<<grid, 256, C::SMEM, s>>>(tq, tk, tv, a);
     DCAT_LAUNCH_CHECK();
 }
