@@ -29,7 +29,7 @@ namespace dcat {
 
 namespace {
 
-constexpr int BKV = 64;  // keys per block
+constexpr int BKV = 64;  // keys per block (cp.async stage)
 
 __device__ __forceinline__ void cp_async16(uint32_t s, const void* gmem, bool pred) {
     int n = pred ? 16 : 0;
@@ -73,7 +73,10 @@ struct FlashCfg {
 };
 
 template <int DH, bool CAUSAL, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_flash(AttnArgs p) {
+__global__ void __launch_bounds__(WARPS * 32, CAUSAL ? 6 : 4) k_flash(AttnArgs p) {
+    // keys per online-softmax step: the context kernel keeps whole 64-key blocks (6 CTAs/SM at
+    // 80 registers), the crossing kernel halves them to fit 4 CTAs of 8 warps (measured best)
+    constexpr int SUB = CAUSAL ? 64 : 32;
     using C = FlashCfg<DH, WARPS>;
     constexpr int LD = C::LD;
     constexpr int CHUNKS = DH / 8;  // 16-byte chunks per row
@@ -179,86 +182,91 @@ __global__ void __launch_bounds__(WARPS * 32) k_flash(AttnArgs p) {
         if (blk + 1 < nblk) load_kv(blk + 1, buf ^ 1);
         cp_async_commit();
 
-        float s[8][4];
 #pragma unroll
-        for (int j = 0; j < 8; j++) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
-        const uint32_t kb = sK0 + 2 * buf * C::KV_ELEMS;
+        for (int sub = 0; sub < BKV / SUB; sub++) {  // SUB-key online-softmax steps (register footprint)
+            constexpr int NJ = SUB / 8;                // n-tiles of S
+            float s[NJ][4];
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; kk++) {
+            for (int j = 0; j < NJ; j++) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+            const uint32_t kb = sK0 + 2 * (buf * C::KV_ELEMS + sub * SUB * LD);
 #pragma unroll
-            for (int j = 0; j < 8; j += 2) {
-                uint32_t b[4];
-                int key = 8 * (j + (lane >> 4)) + (lane & 7);
-                int col = kk * 16 + 8 * ((lane >> 3) & 1);
-                ldsm_x4(b, kb + 2 * (key * LD + col));
-                mma16816(s[j], qf[kk], b[0], b[1]);
-                mma16816(s[j + 1], qf[kk], b[2], b[3]);
-            }
-        }
-        const int kbase = blk * BKV;
-        const bool full = (kbase + BKV <= tile.nkv) && (!CAUSAL || kbase + BKV - 1 <= tile.qloc + warp * 16);
-        if (!full) {
+            for (int kk = 0; kk < DH / 16; kk++) {
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
-#pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    int key = kbase + 8 * j + 2 * t4 + (e & 1);
-                    int row = (e < 2) ? r0 : r1;
-                    bool ok = key < tile.nkv;
-                    if (CAUSAL) ok = ok && key <= tile.qloc + row;
-                    if (!ok) s[j][e] = -INFINITY;
+                for (int j = 0; j < NJ; j += 2) {
+                    uint32_t b[4];
+                    int key = 8 * (j + (lane >> 4)) + (lane & 7);
+                    int col = kk * 16 + 8 * ((lane >> 3) & 1);
+                    ldsm_x4(b, kb + 2 * (key * LD + col));
+                    mma16816(s[j], qf[kk], b[0], b[1]);
+                    mma16816(s[j + 1], qf[kk], b[2], b[3]);
                 }
             }
-        }
-        float bm0 = s[0][0], bm1 = s[0][2];
+            const int kbase = blk * BKV + sub * SUB;
+            if (kbase >= tile.nkv) break;  // uniform across the CTA
+            const bool full = (kbase + SUB <= tile.nkv) && (!CAUSAL || kbase + SUB - 1 <= tile.qloc + warp * 16);
+            if (!full) {
 #pragma unroll
-        for (int j = 0; j < 8; j++) {
-            bm0 = fmaxf(bm0, fmaxf(s[j][0], s[j][1]));
-            bm1 = fmaxf(bm1, fmaxf(s[j][2], s[j][3]));
-        }
-        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
-        bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
-        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
-        bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
-        const float nm0 = fmaxf(m0, bm0), nm1 = fmaxf(m1, bm1);
-        const float u0 = nm0 == -INFINITY ? 0.f : -nm0 * sl2;  // exponent offset (scaled)
-        const float u1 = nm1 == -INFINITY ? 0.f : -nm1 * sl2;
-        const float a0 = ex2(fmaf(m0, sl2, u0)), a1 = ex2(fmaf(m1, sl2, u1));  // m = -inf -> 0
-        m0 = nm0;
-        m1 = nm1;
+                for (int j = 0; j < NJ; j++) {
 #pragma unroll
-        for (int j = 0; j < NT; j++) {
-            o[j][0] *= a0;
-            o[j][1] *= a0;
-            o[j][2] *= a1;
-            o[j][3] *= a1;
-        }
-        lacc[0] *= a0;
-        lacc[1] *= a0;
-        lacc[2] *= a1;
-        lacc[3] *= a1;
-        uint32_t pf[4][4];
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-            float p0 = ex2(fmaf(s[j][0], sl2, u0)), p1 = ex2(fmaf(s[j][1], sl2, u0));
-            float p2 = ex2(fmaf(s[j][2], sl2, u1)), p3 = ex2(fmaf(s[j][3], sl2, u1));
-            pf[j >> 1][(j & 1) * 2 + 0] = pack_bf16(p0, p1);
-            pf[j >> 1][(j & 1) * 2 + 1] = pack_bf16(p2, p3);
-        }
-        // O += P V, l += P 1
-        const uint32_t vb = sV0 + 2 * buf * C::KV_ELEMS;
-#pragma unroll
-        for (int kk = 0; kk < 4; kk++) {
-            const uint32_t* a = pf[kk];
-            int key = kk * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
-#pragma unroll
-            for (int j = 0; j < NT; j += 2) {
-                uint32_t b[4];
-                ldsm_x4_t(b, vb + 2 * (key * LD + 8 * (j + (lane >> 4))));
-                mma16816(o[j], a, b[0], b[1]);
-                mma16816(o[j + 1], a, b[2], b[3]);
+                    for (int e = 0; e < 4; e++) {
+                        int key = kbase + 8 * j + 2 * t4 + (e & 1);
+                        int row = (e < 2) ? r0 : r1;
+                        bool ok = key < tile.nkv;
+                        if (CAUSAL) ok = ok && key <= tile.qloc + row;
+                        if (!ok) s[j][e] = -INFINITY;
+                    }
+                }
             }
-            mma16816(lacc, a, ONES, ONES);
+            float bm0 = s[0][0], bm1 = s[0][2];
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+                bm0 = fmaxf(bm0, fmaxf(s[j][0], s[j][1]));
+                bm1 = fmaxf(bm1, fmaxf(s[j][2], s[j][3]));
+            }
+            bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 1));
+            bm0 = fmaxf(bm0, __shfl_xor_sync(0xffffffffu, bm0, 2));
+            bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 1));
+            bm1 = fmaxf(bm1, __shfl_xor_sync(0xffffffffu, bm1, 2));
+            const float nm0 = fmaxf(m0, bm0), nm1 = fmaxf(m1, bm1);
+            const float u0 = nm0 == -INFINITY ? 0.f : -nm0 * sl2;  // exponent offset (scaled)
+            const float u1 = nm1 == -INFINITY ? 0.f : -nm1 * sl2;
+            const float a0 = ex2(fmaf(m0, sl2, u0)), a1 = ex2(fmaf(m1, sl2, u1));  // m = -inf -> 0
+            m0 = nm0;
+            m1 = nm1;
+#pragma unroll
+            for (int j = 0; j < NT; j++) {
+                o[j][0] *= a0;
+                o[j][1] *= a0;
+                o[j][2] *= a1;
+                o[j][3] *= a1;
+            }
+            lacc[0] *= a0;
+            lacc[1] *= a0;
+            lacc[2] *= a1;
+            lacc[3] *= a1;
+            uint32_t pf[NJ / 2][4];
+#pragma unroll
+            for (int j = 0; j < NJ; j++) {
+                float p0 = ex2(fmaf(s[j][0], sl2, u0)), p1 = ex2(fmaf(s[j][1], sl2, u0));
+                float p2 = ex2(fmaf(s[j][2], sl2, u1)), p3 = ex2(fmaf(s[j][3], sl2, u1));
+                pf[j >> 1][(j & 1) * 2 + 0] = pack_bf16(p0, p1);
+                pf[j >> 1][(j & 1) * 2 + 1] = pack_bf16(p2, p3);
+            }
+            // O += P V, l += P 1
+            const uint32_t vb = sV0 + 2 * (buf * C::KV_ELEMS + sub * SUB * LD);
+#pragma unroll
+            for (int kk = 0; kk < NJ / 2; kk++) {
+                const uint32_t* a = pf[kk];
+                int key = kk * 16 + (lane & 7) + 8 * ((lane >> 3) & 1);
+#pragma unroll
+                for (int j = 0; j < NT; j += 2) {
+                    uint32_t b[4];
+                    ldsm_x4_t(b, vb + 2 * (key * LD + 8 * (j + (lane >> 4))));
+                    mma16816(o[j], a, b[0], b[1]);
+                    mma16816(o[j + 1], a, b[2], b[3]);
+                }
+                mma16816(lacc, a, ONES, ONES);
+            }
         }
         cp_async_wait<0>();
         __syncthreads();
