@@ -299,14 +299,19 @@ uint64_t debug_hash_mask() {
     return (1ull << bits) - 1;
 }
 
-// Attention tiling: the tcgen05 attention (bf16, head dim 16/32/64, V cache stored
-// transposed) takes 128-query tiles in both passes; the mma.sync / SIMT kernels take
-// 64-query context tiles.
+// Attention kernels (bf16 path):
+//   default: attention.cu's mma.sync flash kernel (64-query context tiles, 128 crossing);
+//   DCAT_ATTN_PIPE=1 (head dim 32): attn_pipe.cu, persistent with two tcgen05 pipelines per SM
+//     (ties the flash kernel on the crossing pass, slower on the causal context pass; see
+//     profiles/r01_attention.md);
+//   DCAT_TC_ATTENTION=1 (head dim 32/64): attn_tc.cu, one CTA per tile x head.
+// The tcgen05 kernels take 128-query tiles and read the V cache transposed (keys
+// contiguous), so the K/V projection stores it that way when one of them is selected.
 bool use_tc_attention(const dcat_model* m, bool f32) {
     const int dh = m->cfg.d_model / m->cfg.n_heads;
-    // opt-in until it beats the mma.sync flash kernel (per-CTA TMA -> MMA -> softmax -> MMA
-    // chain is serialized at 2 CTAs/SM; see profiles/r01_summary.md)
-    return !f32 && (dh == 32 || dh == 64) && getenv("DCAT_TC_ATTENTION") != nullptr;
+    if (f32) return false;
+    if (getenv("DCAT_ATTN_PIPE") != nullptr && attention_pipe_supported(dh)) return true;
+    return getenv("DCAT_TC_ATTENTION") != nullptr && (dh == 32 || dh == 64);
 }
 
 // dedup + validation; leaves the plan on the device and the counts in m->st_host
@@ -405,8 +410,13 @@ template <typename T>
 void attn(dcat_model* m, const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t s) {
     int t0 = mark(m, s);
     if constexpr (std::is_same<T, bf16>::value) {
-        if (a.ldvt > 0) attention_tc(a, q_rows, kv_rows, s);
-        else attention_bf16(a, s);
+        if (a.ldvt > 0) {
+            const bool pipe = getenv("DCAT_ATTN_PIPE") != nullptr;
+            if (pipe && attention_pipe_supported(a.dh)) attention_pipe(a, q_rows, kv_rows, s);
+            else attention_tc(a, q_rows, kv_rows, s);
+        } else {
+            attention_bf16(a, s);
+        }
     } else {
         attention_f32(a, s);
     }

@@ -165,12 +165,16 @@ def test_bf16_pinfm_base_sample_vs_oracle(api, orc):
     assert rel_err(lf, rl) <= 1e-4
 
 
-@pytest.mark.parametrize("impl", ["tcgen05", "flash"])
+@pytest.mark.parametrize("impl", ["pipe", "tcgen05", "flash"])
 def test_bf16_attention_impls_and_kv_cache(api, orc, impl, monkeypatch):
-    """Both bf16 attention kernels (tcgen05 with the V^T cache, mma.sync flash with the
-    row-major cache) against the oracle, and the bf16 K/V cache against context_forward's."""
+    """Every bf16 attention kernel (the mma.sync flash default with the row-major cache, the
+    pipelined and the per-tile tcgen05 kernels with the V^T cache) against
+    the oracle on ragged users (unaligned, multi-chunk key ranges), and the bf16 K/V cache
+    against context_forward's."""
     if impl == "tcgen05":
         monkeypatch.setenv("DCAT_TC_ATTENTION", "1")
+    if impl == "pipe":
+        monkeypatch.setenv("DCAT_ATTN_PIPE", "1")
     spec, w, b = _base_setup(orc, 5, 9, 200, seed=6, ragged=True, layout="grouped")
     ft = FinetuneSpec(max_events=200)
     m = api.DcatModel(w)
