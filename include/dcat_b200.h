@@ -106,6 +106,15 @@ typedef struct dcat_finetune_config {
     int32_t d_aux;
     double fresh_days;
     double mid_days;
+    /* Fixed-window variant of the sequence module (context_forward_fixed /
+     * cross_forward_fixed, dcat.cpp:281-415): 0 = off; window W >= 1 keeps each
+     * unique's newest min(valid, W - 1) events with positions restarting at 0
+     * and puts the candidate at position kept (the ring's free slot). Results
+     * are the ring's (which are rotation invariant, test_dcat.cpp:341-361);
+     * dedup still keys on the full event prefix; the ranking-head context
+     * features use the full row. */
+    int32_t window;
+    int32_t reserved;
 } dcat_finetune_config;
 
 /* A request batch: the std::vector<RankingExample> of the reference

@@ -586,6 +586,27 @@ static void validate_batch(const dcat_batch* b) {
     }
 }
 
+/* Fixed-window view of a batch for the sequence module (context_forward_fixed,
+ * dcat.cpp:300-313): row i keeps its newest kept = min(valid, window - 1) events,
+ * positions restarting at 0. The reference stores them in a ring of `window`
+ * slots with the candidate in the free slot; the scores are rotation invariant
+ * (test_dcat.cpp:341-361) and equal the truncate-then-forward DCAT result
+ * (test_dcat.cpp:300-339), which is what this view feeds to the plain path. */
+static dcat_batch window_view(const dcat_batch* b, int window) {
+    dcat_batch v = *b;
+    int64_t B = b->n_rows;
+    int64_t* off = (int64_t*)amalloc(sizeof(int64_t) * (B ? B : 1));
+    int32_t* val = (int32_t*)amalloc(sizeof(int32_t) * (B ? B : 1));
+    for (int64_t i = 0; i < B; i++) {
+        int kept = b->row_valid[i] < window - 1 ? b->row_valid[i] : window - 1;
+        off[i] = b->row_offset[i] + (b->row_valid[i] - kept);
+        val[i] = kept;
+    }
+    v.row_offset = off;
+    v.row_valid = val;
+    return v;
+}
+
 static int run_rank_batch(const Model* M, const dcat_table* t, const dcat_head* hp, const dcat_finetune_config* ft,
                           const dcat_batch* b, double* logits, double* mlogits, double* probs, float* h_cand) {
     const dcat_model_config* cfg = &M->cfg;
@@ -598,21 +619,25 @@ static int run_rank_batch(const Model* M, const dcat_table* t, const dcat_head* 
           cfg->max_len, ft->max_events);
     CHECK(ft->use_seq_module || ft->variant == DCAT_VARIANT_BASE,
           "disabling the sequence module requires the base variant");
+    CHECK(ft->window >= 0, "context_forward_fixed: window must be >= 1, got %d", ft->window);
+    const int fixed = ft->use_seq_module && ft->window > 0;
     int empty_seq = 0;
     for (int64_t i = 0; i < B; i++) empty_seq |= b->row_valid[i] == 0;
-    /* finetune.cpp:428-431 */
-    if (!ft->use_seq_module || empty_seq) {
+    /* finetune.cpp:428-431 (the fixed-window path has no per-example fallback: its
+     * cross_forward_fixed handles an empty ring, dcat.cpp:360-390) */
+    if (!ft->use_seq_module || (empty_seq && !fixed)) {
         for (int64_t i = 0; i < B; i++)
             rank_forward_one(M, t, hp, ft, b, i, logits + 3 * i, mlogits + 3 * i, probs + 3 * i);
         return 0;
     }
     int32_t* rep = (int32_t*)amalloc(sizeof(int32_t) * B);
     int32_t* first = (int32_t*)amalloc(sizeof(int32_t) * B);
-    int b_u = dedup(b, rep, first);
-    SeqKV* cache = context_forward(M, t, b, first, b_u);
+    int b_u = dedup(b, rep, first); /* dedup keys on the full prefix in both variants */
+    dcat_batch sb = fixed ? window_view(b, ft->window) : *b;
+    SeqKV* cache = context_forward(M, t, &sb, first, b_u);
     uint64_t* items = (uint64_t*)amalloc(sizeof(uint64_t) * B);
     int* pos = (int*)amalloc(sizeof(int) * B);
-    for (int64_t i = 0; i < B; i++) { items[i] = b->candidate[i]; pos[i] = b->row_valid[first[rep[i]]]; }
+    for (int64_t i = 0; i < B; i++) { items[i] = b->candidate[i]; pos[i] = sb.row_valid[first[rep[i]]]; }
     Mat e_cand = candidate_inputs(M, t, items, pos, B);
     if (ft->variant == DCAT_VARIANT_AUX) { /* finetune.cpp:469-479 */
         CHECK(b->aux != NULL && b->d_aux > 0, "variant 'aux' requires an auxiliary embedding");
@@ -777,6 +802,26 @@ int oracle_naive_candidate_outputs(const dcat_model_config* cfg, const dcat_para
         Mat h = forward_rows(&M, &e2);
         memcpy(out + (size_t)i * d, row(&h, n), sizeof(float) * d);
     }
+    API_END
+}
+
+int oracle_dcat_outputs_fixed(const dcat_model_config* cfg, const dcat_params* params, const dcat_table* table,
+                              const dcat_batch* b, int32_t window, float* h_cand) {
+    API_BEGIN
+    Model M = bind_model(cfg, params);
+    validate_batch(b);
+    CHECK(window >= 1, "context_forward_fixed: window must be >= 1, got %d", window);
+    int64_t B = b->n_rows;
+    int32_t* rep = (int32_t*)amalloc(sizeof(int32_t) * (B ? B : 1));
+    int32_t* first = (int32_t*)amalloc(sizeof(int32_t) * (B ? B : 1));
+    int b_u = dedup(b, rep, first);
+    dcat_batch sb = window_view(b, window);
+    SeqKV* cache = context_forward(&M, table, &sb, first, b_u);
+    int* pos = (int*)amalloc(sizeof(int) * (B ? B : 1));
+    for (int64_t i = 0; i < B; i++) pos[i] = sb.row_valid[first[rep[i]]];
+    Mat e_cand = candidate_inputs(&M, table, b->candidate, pos, B);
+    Mat H = cross_forward(&M, cache, b_u, rep, B, &e_cand);
+    memcpy(h_cand, H.a, sizeof(float) * (size_t)B * cfg->d_model);
     API_END
 }
 

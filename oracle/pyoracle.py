@@ -54,6 +54,10 @@ class CpuImpl:
         self._f("context_kv").argtypes = common + [P(BatchC), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
         self._f("naive_candidate_outputs").argtypes = common + [P(BatchC), C.c_void_p]
         self._f("dcat_outputs").argtypes = common + [P(BatchC), C.c_void_p]
+        if prefix == "oracle":
+            self._f("dcat_outputs_fixed").argtypes = common + [P(BatchC), C.c_int32, C.c_void_p]
+        else:
+            self._f("dcat_outputs_fixed").argtypes = common + [P(BatchC), C.c_int32, C.c_int32, C.c_void_p]
         rfb = common + [P(HeadC), P(FinetuneConfigC), P(BatchC), C.c_void_p, C.c_void_p, C.c_void_p]
         if prefix == "oracle":
             self._f("rank_forward_batch").argtypes = rfb + [C.c_void_p, C.c_void_p]
@@ -135,6 +139,17 @@ class CpuImpl:
         out = np.zeros((max(batch.n_rows, 1), w.spec.d_model), np.float32)
         self._check(self._f("naive_candidate_outputs")(C.byref(w.spec.c()), C.byref(w.params_c()),
                                                        C.byref(w.table_c()), C.byref(batch.c()), out.ctypes.data))
+        return out[:batch.n_rows]
+
+    def dcat_outputs_fixed(self, w: Weights, batch: Batch, window: int, rotation: int = 0):
+        """Fixed-window DCAT (context_forward_fixed / cross_forward_fixed, dcat.cpp:281-415).
+        The oracle restates it as truncate-then-DCAT (its ring is rotation 0); the reference
+        runs its ring at `rotation`."""
+        out = np.zeros((max(batch.n_rows, 1), w.spec.d_model), np.float32)
+        args = [C.byref(w.spec.c()), C.byref(w.params_c()), C.byref(w.table_c()), C.byref(batch.c()), window]
+        if self.prefix != "oracle":
+            args.append(rotation)
+        self._check(self._f("dcat_outputs_fixed")(*args, out.ctypes.data))
         return out[:batch.n_rows]
 
     def dcat_outputs(self, w: Weights, batch: Batch):

@@ -318,4 +318,29 @@ int ref_dcat_outputs(const dcat_model_config* c, const dcat_params* prm, const d
     });
 }
 
+// dedup -> context_forward_fixed(window, rotation) -> candidate_inputs(pos = kept) ->
+// cross_forward_fixed (dcat.cpp:281-415), the composition test_dcat.cpp:300-339 checks.
+int ref_dcat_outputs_fixed(const dcat_model_config* c, const dcat_params* prm, const dcat_table* t,
+                           const dcat_batch* b, int32_t window, int32_t rotation, float* h_cand) {
+    return guard([&] {
+        TransformerParams p = make_params(c, prm);
+        HashedEmbeddingTable tab = make_table(t);
+        std::vector<Segment> segs;
+        std::vector<u64> items;
+        for (int64_t i = 0; i < b->n_rows; i++) {
+            segs.push_back(make_segment(b, i));
+            items.push_back(b->candidate[i]);
+        }
+        std::vector<Segment> uniques;
+        DedupPlan plan = dedup_segments(segs, &uniques);
+        FixedKVCache cache = context_forward_fixed(p, tab, uniques, window, rotation);
+        std::vector<int> pos;
+        for (int i = 0; i < plan.b; i++)
+            pos.push_back(cache.seqs[static_cast<size_t>(plan.rep[static_cast<size_t>(i)])].kept);
+        Mat e = candidate_inputs(p, tab, items, pos);
+        Mat h = cross_forward_fixed(p, cache, plan, e);
+        std::memcpy(h_cand, h.a.data(), sizeof(float) * h.a.size());
+    });
+}
+
 } // extern "C"

@@ -45,7 +45,8 @@ class HeadC(C.Structure):
 
 class FinetuneConfigC(C.Structure):
     _fields_ = [("variant", C.c_int32), ("use_seq_module", C.c_int32), ("max_events", C.c_int32),
-                ("d_aux", C.c_int32), ("fresh_days", C.c_double), ("mid_days", C.c_double)]
+                ("d_aux", C.c_int32), ("fresh_days", C.c_double), ("mid_days", C.c_double),
+                ("window", C.c_int32), ("reserved", C.c_int32)]
 
 
 class BatchC(C.Structure):
@@ -139,10 +140,11 @@ class FinetuneSpec:
     d_aux: int = 16
     fresh_days: float = 7.0
     mid_days: float = 28.0
+    window: int = 0  # fixed-window sequence module (dcat.cpp:281-415); 0 = off
 
     def c(self) -> FinetuneConfigC:
         return FinetuneConfigC(VARIANTS[self.variant], int(self.use_seq_module), self.max_events,
-                               self.d_aux, self.fresh_days, self.mid_days)
+                               self.d_aux, self.fresh_days, self.mid_days, self.window, 0)
 
 
 @dataclass

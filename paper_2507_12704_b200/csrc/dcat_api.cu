@@ -252,6 +252,7 @@ Staged stage_batch(dcat_model* m, const dcat_batch* b, bool device, bool aux_nee
     st.in.n_surfaces = m->cfg.n_surfaces;
     st.in.max_len = m->cfg.max_len;
     st.in.pos_learned = m->cfg.pos_learned;
+    st.in.window = 0;
     st.candidate = stage(m->b_in[6], b->candidate, B, device, s, &h2d);
     st.age = stage(m->b_in[7], b->age_seconds, B, device, s, &h2d);
     st.aux = nullptr;
@@ -683,6 +684,9 @@ int validate_ft(const dcat_model* m, const dcat_finetune_config* ft, const dcat_
     if (!(ft->fresh_days > 0.0 && ft->fresh_days < ft->mid_days))
         return set_err(DCAT_EINVAL, "age bands must satisfy 0 < fresh_days < mid_days");
     if (ft->max_events < 0) return set_err(DCAT_EINVAL, "max_events must be >= 0");
+    // context_forward_fixed (dcat.cpp:285): window >= 1 when the fixed-window variant is on
+    if (ft->window < 0) return set_err(DCAT_EINVAL, "context_forward_fixed: window must be >= 1, got " +
+                                                         std::to_string(ft->window));
     if (m->cfg.max_len < ft->max_events + 2)
         return set_err(DCAT_EINVAL, "model.max_len " + std::to_string(m->cfg.max_len) + " too small for max_events " +
                                         std::to_string(ft->max_events) + " plus candidate tokens");
@@ -873,6 +877,7 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         m->tile_cross = 128;
         int t0 = mark(m, s);
         Staged sb = stage_batch(m, batch, device, ft->variant == DCAT_VARIANT_AUX, s);
+        sb.in.window = ft->use_seq_module ? ft->window : 0;  // fixed-window sequence module
         DedupOut o = dedup_buffers(m, B);
         int t1 = mark(m, s);
         run_dedup(m, sb, o, s);

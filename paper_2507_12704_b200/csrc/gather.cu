@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(256, 4) k_gather_ctx(DedupIn in, const int32_t
             const int64_t t = tb + lane;
             const int u = tok_unique[t];
             mi = static_cast<int>(t - tok_off[u]);
-            const int64_t ev = in.row_offset[first[u]] + mi;
+            const int fr = first[u], rv = in.row_valid[fr];
+            const int64_t ev = in.row_offset[fr] + (rv - seq_kept(in, rv)) + mi;  // fixed window: newest events
             mitem = in.item[ev];
             ma = in.action[ev];
             ms = in.surface[ev];
@@ -201,7 +202,7 @@ __device__ void gather_cand_row(DedupIn in, const int32_t* __restrict__ perm, co
                                 const int32_t* __restrict__ first, const EmbParams& ep, const CandParams& cp,
                                 int64_t p, T* __restrict__ E, int ldE, T* __restrict__ feat, Status* st, int lane) {
     int i = perm[p];
-    int n = in.row_valid[first[rep[i]]];
+    int n = seq_kept(in, in.row_valid[first[rep[i]]]);  // candidate position (the ring's free slot)
     uint64_t item = cp.candidate[i];
     const uint32_t rows = warp_rows(ep, item, lane);
     const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(n) * ep.d_emb : nullptr;

@@ -22,7 +22,14 @@ struct DedupIn {
     const uint8_t* surface;
     const uint64_t* item;
     int n_actions, n_surfaces, max_len, pos_learned;
+    int window;  // fixed-window variant: keep the newest min(valid, window - 1) events (0 = off)
 };
+
+// Events of a row's span the sequence module uses: all of them, or the newest window - 1
+// (context_forward_fixed, dcat.cpp:301-302); `skip` = leading events dropped.
+__host__ __device__ __forceinline__ int seq_kept(const DedupIn& in, int valid) {
+    return in.window > 0 ? (valid < in.window - 1 ? valid : in.window - 1) : valid;
+}
 
 struct Tile {  // one attention work item: <= BM query rows of one unique
     int q0, nq;     // first query row, number of query rows

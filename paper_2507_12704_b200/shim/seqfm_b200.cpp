@@ -165,6 +165,19 @@ Mat Scorer::candidate_outputs(const std::vector<RankingExample>& batch, const Fi
     return h;
 }
 
+Mat Scorer::candidate_outputs_fixed(const std::vector<RankingExample>& batch, const FinetuneConfig& cfg,
+                                    int window) const {
+    SEQFM_CHECK(window >= 1, "context_forward_fixed: window must be >= 1, got " << window);
+    Mat h(static_cast<int>(batch.size()), d_model_);
+    if (batch.empty()) return h;
+    BatchSoA b(batch, cfg.variant == FusionVariant::Aux);
+    dcat_finetune_config fc = to_c(cfg);
+    fc.window = window;
+    std::vector<float> logits(batch.size() * 3), mlog(batch.size() * 3);
+    check(dcat_rank_forward_batch(m_, &b.c, &fc, logits.data(), mlog.data(), h.a.data(), flags_, nullptr));
+    return h;
+}
+
 DedupPlan Scorer::dedup_segments(const std::vector<Segment>& batch, std::vector<Segment>* uniques) const {
     std::vector<RankingExample> ex(batch.size());
     for (size_t i = 0; i < batch.size(); i++) ex[i].seq = batch[i];

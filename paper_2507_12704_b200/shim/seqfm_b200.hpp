@@ -35,6 +35,11 @@ public:
     DedupPlan dedup_segments(const std::vector<Segment>& batch, std::vector<Segment>* uniques) const;
     // cross_forward output rows (unit-norm H_cand) of the DCAT path, B x d_model.
     Mat candidate_outputs(const std::vector<RankingExample>& batch, const FinetuneConfig& cfg) const;
+    // The fixed-window variant (window >= 1): dedup_segments -> context_forward_fixed ->
+    // candidate_inputs(pos = kept) -> cross_forward_fixed (dcat.cpp:281-415), B x d_model.
+    // Scores equal the reference ring at any rotation (test_dcat.cpp:341-361).
+    Mat candidate_outputs_fixed(const std::vector<RankingExample>& batch, const FinetuneConfig& cfg,
+                                int window) const;
 
     // true: fp32 storage + CUDA-core math (parity mode, DCAT_PRECISION_FP32)
     void set_fp32(bool on) { flags_ = on ? 0x2 : 0; }

@@ -178,6 +178,43 @@ int main() {
             EXPECT(m <= 1e-4, "cross vs naive");
         }
 
+    // 3b. fixed-window variant against the reference ring (dcat.cpp:281-415) at a non-zero rotation
+    for (int window : {1, 4, 8, 64}) {
+        ModelConfig c;
+        c.d_model = 16;
+        c.n_layers = 2;
+        c.n_heads = 4;
+        c.d_emb = 16;
+        c.max_len = 16;
+        TransformerParams p;
+        p.init(c, 101);
+        HashedEmbeddingTable table(4, 64, 4, 15);
+        RankingHeadParams rp;
+        rp.init(16, 16, 16, 8, 64, 1, 11);
+        Rng r2(12);
+        auto batch = make_batch(4, 3, 12, 0, r2, false);
+        std::vector<Segment> segs, uniques;
+        std::vector<u64> items;
+        for (auto& ex : batch) {
+            segs.push_back(ex.seq);
+            items.push_back(ex.candidate);
+        }
+        DedupPlan plan = dedup_segments(segs, &uniques);
+        FixedKVCache cache = context_forward_fixed(p, table, uniques, window, 3);
+        std::vector<int> pos;
+        for (int i = 0; i < plan.b; i++) pos.push_back(cache.seqs[static_cast<size_t>(plan.rep[static_cast<size_t>(i)])].kept);
+        Mat ref = cross_forward_fixed(p, cache, plan, candidate_inputs(p, table, items, pos));
+        b200::Scorer sc(p, table, rp);
+        sc.set_fp32(true);
+        FinetuneConfig cfg;
+        cfg.max_events = 12;
+        Mat h = sc.candidate_outputs_fixed(batch, cfg, window);
+        double m = 0;
+        for (size_t i = 0; i < h.a.size(); i++) m = std::max(m, static_cast<double>(std::fabs(h.a[i] - ref.a[i])));
+        std::printf("fixed window %d vs reference ring (rotation 3): max abs %.3e\n", window, m);
+        EXPECT(m <= 1e-4, "fixed window vs cross_forward_fixed");
+    }
+
     // 4. errors surface as std::runtime_error (SEQFM_CHECK)
     {
         TransformerParams p;

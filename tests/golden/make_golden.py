@@ -179,6 +179,36 @@ def gen_cross(ref):
     np.savez_compressed(os.path.join(HERE, "cross.npz"), **out)
 
 
+def gen_fixed(ref):
+    """test_dcat.cpp:300-361: fixed-window ring (context_forward_fixed + cross_forward_fixed)
+    on every fill level, and the ring's rotation invariance."""
+    out = {}
+    names = []
+    W = 8
+    rng = np.random.default_rng(12)
+    spec = small_config(2, 4, 64)
+    tab = (4, 64, 4, 15, 0.05)
+    w, sha = make_weights(ref, spec, 101, 0.05, tab, 11, 64, 16, 1)
+    out.update({"spec": spec_fields(spec)["spec"], "sha": np.array(sha), "window": np.array(W),
+                **init_args(101, 0.05, tab, 11, 64, 16, 1)})
+    for valid in (0, 1, 3, 6, 7, 8, 9, 20):
+        rows = [rand_row(rng, valid), rand_row(rng, max(0, valid - 1))]
+        b = seg_batch(rows, 24)
+        b.candidate[:] = rng.integers(0, 1000, b.n_rows).astype(np.uint64)
+        n = f"fill{valid}"
+        names.append(n)
+        out.update(batch_fields(b, n + "."))
+        out[n + ".h"] = ref.dcat_outputs_fixed(w, b, W, 0)
+    # rotation invariance on a ragged multi-candidate rig (test_dcat.cpp:341-361)
+    b = make_batch(6, 2, 20, seed=13, ragged=True)
+    out.update(batch_fields(b, "rot."))
+    out["rot.h0"] = ref.dcat_outputs_fixed(w, b, W, 0)
+    for r in (1, 3, 7, 29):
+        out[f"rot.h{r}"] = ref.dcat_outputs_fixed(w, b, W, r)
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "fixed.npz"), **out)
+
+
 def gen_kv(ref):
     """test_dcat.cpp:166-213: context K/V per layer."""
     spec = small_config(2, 4, 16)
@@ -273,6 +303,7 @@ if __name__ == "__main__":
     gen_kv(ref)
     gen_cross(ref)
     gen_rank(ref)
+    gen_fixed(ref)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -280,3 +280,34 @@ def test_errors(api, orc):
         m.rank_forward_batch(b, FinetuneSpec(variant="aux-lt", max_events=16))
     with pytest.raises(RuntimeError, match="max_len"):
         m.rank_forward_batch(b, FinetuneSpec(max_events=19))
+
+
+@pytest.mark.gpu
+def test_fixed_window(api, orc):
+    """Fixed-window sequence module (context_forward_fixed / cross_forward_fixed,
+    dcat.cpp:281-415) through the C ABI's `window` field: the reference-pinned goldens on every
+    fill level (fp32, 1e-4), and a ragged d=256 batch in both precisions against the oracle —
+    h_cand (sequence module) and logits (ranking head on the full row's context features)."""
+    z = G.load("fixed")
+    _, w = G.weights_from(z, orc)
+    W = int(z["window"])
+    m = api.DcatModel(w)
+    for n in G.names(z):
+        b = G.batch_from(z, n + ".")
+        _, _, h = m.rank_forward_batch(b, FinetuneSpec(max_events=24, window=W), precision="fp32", want_h=True)
+        assert float(np.abs(h - z[n + ".h"]).max()) <= 1e-4, n
+    spec, w, b = _base_setup(orc, 4, 6, 120, seed=21, ragged=True, layout="grouped")
+    m = api.DcatModel(w)
+    for window in (1, 17, 64, 400):
+        ft = FinetuneSpec(max_events=120, window=window)
+        rl, rm, _, rh = orc.rank_forward_batch(w, ft, b)
+        np.testing.assert_allclose(rh, orc.dcat_outputs_fixed(w, b, window), atol=1e-6)
+        lf, mf, hf = m.rank_forward_batch(b, ft, precision="fp32", want_h=True)
+        assert float(np.abs(hf - rh).max()) <= 1e-4 and rel_err(lf, rl) <= 1e-4, window
+        lb, mb, hb = m.rank_forward_batch(b, ft, want_h=True)
+        assert float(np.abs(hb - rh).max()) <= 3e-2 and cos_min(hb, rh) >= 0.999, window
+        assert rel_err(lb, rl) <= 3e-2 and rel_err(mb, rm) <= 3e-2, window
+        # the cache holds at most window - 1 tokens per unique (test_dcat.cpp:363-382)
+        rep, first, b_u = orc.dedup(b)
+        kept = np.minimum(b.row_valid[first], max(window - 1, 0)).sum()
+        assert m.last_stats()["ctx_tokens"] == kept

@@ -145,3 +145,37 @@ def test_oracle_vs_reference_fresh_inputs(orc):
             lr = ref.rank_forward_batch(w_r, ft, b)
             for a, c in zip(lo[:3], lr[:3]):
                 np.testing.assert_array_equal(a, c)
+
+
+def test_fixed_window_bitwise(orc):
+    """Fixed-window DCAT (context_forward_fixed / cross_forward_fixed, dcat.cpp:281-415) on every
+    fill level of an 8-slot ring (test_dcat.cpp:300-339): the oracle's truncate-then-DCAT
+    restatement reproduces the reference ring (rotation 0) bit for bit, and the reference's
+    rotation invariance (test_dcat.cpp:341-361) holds within its own 1e-5."""
+    z = G.load("fixed")
+    _, w = G.weights_from(z, orc)
+    W = int(z["window"])
+    for n in G.names(z):
+        b = G.batch_from(z, n + ".")
+        np.testing.assert_array_equal(orc.dcat_outputs_fixed(w, b, W), z[n + ".h"], err_msg=n)
+    b = G.batch_from(z, "rot.")
+    np.testing.assert_array_equal(orc.dcat_outputs_fixed(w, b, W), z["rot.h0"])
+    for r in (1, 3, 7, 29):
+        assert np.abs(z[f"rot.h{r}"] - z["rot.h0"]).max() <= 1e-5
+
+
+def test_fixed_window_equals_truncated_dcat(orc):
+    """The ring's defining property (test_dcat.cpp:326-338): fixed-window scores equal plain
+    DCAT on the newest window - 1 events, and equal the unwindowed result when nothing is
+    truncated."""
+    z = G.load("fixed")
+    _, w = G.weights_from(z, orc)
+    W = int(z["window"])
+    b = G.batch_from(z, "rot.")
+    kept = np.minimum(b.row_valid, W - 1)
+    t = b.take(np.arange(b.n_rows))
+    t.row_offset = (b.row_offset + (b.row_valid - kept)).astype(np.int64)
+    t.row_valid = kept.astype(np.int32)
+    np.testing.assert_allclose(orc.dcat_outputs_fixed(w, b, W), orc.naive_candidate_outputs(w, t), atol=1e-5)
+    big = W + int(b.row_valid.max())
+    np.testing.assert_array_equal(orc.dcat_outputs_fixed(w, b, big), orc.dcat_outputs(w, b))
