@@ -69,7 +69,15 @@ typedef struct dcat_table {
     int32_t rows;
     int32_t d_sub;
     const uint64_t* seeds;          /* [J] per-subtable hash seeds          */
-    const float* const* subtables;  /* [J] pointers, each R x d_sub         */
+    const float* const* subtables;  /* [J] pointers, each R x d_sub (bits == 0) */
+    /* QuantizedTable (embed.hpp:80-125): bits = 4 or 8 selects `packed`, the
+     * J x R rows of ceil(d_sub * bits / 8) code bytes (int4: element e in byte
+     * e / 2, low nibble first) followed by fp16 scale and fp16 bias, exactly
+     * the reference's payload (and PQTB1 body, embed.cpp:212-240). Rows are
+     * dequantized on the fly in the gathers: (float)code * scale + bias
+     * (dequantize_row, embed.cpp:99-103). bits = 0: fp32 `subtables`. */
+    int32_t bits;
+    const uint8_t* packed;
 } dcat_table;
 
 /* RankingHeadParams (finetune.hpp:70-85). d_feat = d_module + d_emb + n_ctx. */

@@ -303,10 +303,46 @@ static uint32_t hash_id(uint64_t id, uint64_t seed, uint32_t rows) {
 }
 
 /* HashedEmbeddingTable::lookup (embed.cpp:38-43) */
+/* IEEE binary16 conversions (fp16.hpp): round-to-nearest-even to half, exact back.
+ * _Float16 casts are IEEE conversions, identical to the reference's bit routines
+ * for every finite value (quantize rejects non-finite rows, embed.cpp:138-140). */
+static uint16_t f32_to_f16(float f) {
+    _Float16 h = (_Float16)f;
+    uint16_t u;
+    memcpy(&u, &h, 2);
+    return u;
+}
+static float f16_to_f32(uint16_t u) {
+    _Float16 h;
+    memcpy(&h, &u, 2);
+    return (float)h;
+}
+
+static int q_code_bytes(const dcat_table* t) { return (t->d_sub * t->bits + 7) / 8; }
+static int q_row_bytes(const dcat_table* t) { return q_code_bytes(t) + 4; }
+
+/* QuantizedTable::dequantize_row (embed.cpp:92-103): codes (int4: element e in byte
+ * e / 2, low nibble first), fp16 scale, fp16 bias; v = (float)code * scale + bias */
+static void dequantize_row(const dcat_table* t, int j, uint32_t r, float* out) {
+    const uint8_t* row = t->packed + ((size_t)j * t->rows + r) * (size_t)q_row_bytes(t);
+    const int cb = q_code_bytes(t);
+    const float s = f16_to_f32((uint16_t)(row[cb] | (row[cb + 1] << 8)));
+    const float b = f16_to_f32((uint16_t)(row[cb + 2] | (row[cb + 3] << 8)));
+    for (int e = 0; e < t->d_sub; e++) {
+        uint32_t code = t->bits == 8 ? row[e] : (uint32_t)((row[e / 2] >> ((e % 2) * 4)) & 15);
+        float cs = (float)code * s;
+        out[e] = cs + b;
+    }
+}
+
+/* HashedEmbeddingTable::lookup (embed.cpp:38-43) / QuantizedTable::qlookup (:111-113) */
 static void lookup(const dcat_table* t, uint64_t id, float* out) {
     for (int j = 0; j < t->num_subtables; j++) {
         uint32_t r = hash_id(id, t->seeds[j], (uint32_t)t->rows);
-        memcpy(out + (size_t)j * t->d_sub, t->subtables[j] + (size_t)r * t->d_sub, sizeof(float) * t->d_sub);
+        if (t->bits)
+            dequantize_row(t, j, r, out + (size_t)j * t->d_sub);
+        else
+            memcpy(out + (size_t)j * t->d_sub, t->subtables[j] + (size_t)r * t->d_sub, sizeof(float) * t->d_sub);
     }
 }
 
@@ -802,6 +838,46 @@ int oracle_naive_candidate_outputs(const dcat_model_config* cfg, const dcat_para
         Mat h = forward_rows(&M, &e2);
         memcpy(out + (size_t)i * d, row(&h, n), sizeof(float) * d);
     }
+    API_END
+}
+
+/* quantize (embed.cpp:124-171): per-row min-max; bias = half(min), scale =
+ * half((max - min) / (2^b - 1)); codes = round-half-even((x - bias) / scale)
+ * clamped to [0, 2^b - 1]; a non-positive scale stores 0 and zero codes. */
+int oracle_quantize_table(const dcat_table* t, int32_t bits, uint8_t* packed) {
+    API_BEGIN
+    CHECK(bits == 4 || bits == 8, "quantize: bits must be 4 or 8, got %d", bits);
+    dcat_table q = *t;
+    q.bits = bits;
+    const int cb = q_code_bytes(&q), rb = q_row_bytes(&q);
+    const uint32_t max_code = (1u << bits) - 1;
+    memset(packed, 0, (size_t)t->num_subtables * t->rows * rb);
+    for (int j = 0; j < t->num_subtables; j++)
+        for (int r = 0; r < t->rows; r++) {
+            const float* src = t->subtables[j] + (size_t)r * t->d_sub;
+            float lo = src[0], hi = src[0];
+            for (int e = 0; e < t->d_sub; e++) {
+                CHECK(isfinite(src[e]), "quantize: non-finite value at subtable %d row %d elem %d", j, r, e);
+                lo = src[e] < lo ? src[e] : lo;
+                hi = src[e] > hi ? src[e] : hi;
+            }
+            float bias = f16_to_f32(f32_to_f16(lo));
+            float scale = f16_to_f32(f32_to_f16((hi - lo) / (float)max_code));
+            uint8_t* dst = packed + ((size_t)j * t->rows + r) * rb;
+            if (scale > 0.0f) {
+                for (int e = 0; e < t->d_sub; e++) {
+                    long c = lrintf((src[e] - bias) / scale);
+                    c = c < 0 ? 0 : (c > (long)max_code ? (long)max_code : c);
+                    if (bits == 8) dst[e] = (uint8_t)c;
+                    else dst[e / 2] |= (uint8_t)(c << ((e % 2) * 4));
+                }
+            } else {
+                scale = 0.0f;
+            }
+            uint16_t sb = f32_to_f16(scale), bb = f32_to_f16(bias);
+            dst[cb] = (uint8_t)(sb & 255); dst[cb + 1] = (uint8_t)(sb >> 8);
+            dst[cb + 2] = (uint8_t)(bb & 255); dst[cb + 3] = (uint8_t)(bb >> 8);
+        }
     API_END
 }
 

@@ -54,6 +54,9 @@ class CpuImpl:
         self._f("context_kv").argtypes = common + [P(BatchC), C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
         self._f("naive_candidate_outputs").argtypes = common + [P(BatchC), C.c_void_p]
         self._f("dcat_outputs").argtypes = common + [P(BatchC), C.c_void_p]
+        self._f("quantize_table").argtypes = [P(TableC), C.c_int32, C.c_void_p]
+        if prefix != "oracle":
+            self._f("save_quantized").argtypes = [P(TableC), C.c_int32, C.c_char_p, C.c_char_p]
         if prefix == "oracle":
             self._f("dcat_outputs_fixed").argtypes = common + [P(BatchC), C.c_int32, C.c_void_p]
         else:
@@ -151,6 +154,19 @@ class CpuImpl:
             args.append(rotation)
         self._check(self._f("dcat_outputs_fixed")(*args, out.ctypes.data))
         return out[:batch.n_rows]
+
+    def quantize_table(self, w: Weights, bits: int) -> np.ndarray:
+        """quantize (embed.cpp:124-171) of w's fp32 table: the QuantizedTable payload."""
+        J, R, ds = w.table.shape
+        out = np.zeros(J * R * ((ds * bits + 7) // 8 + 4), np.uint8)
+        self._check(self._f("quantize_table")(C.byref(w.table_c()), bits, out.ctypes.data))
+        return out
+
+    def save_quantized(self, w: Weights, bits: int, path: str, config_text=None) -> None:
+        """save_quantized (embed.cpp:212-240) of quantize(w.table, bits) — reference only."""
+        self._check(self._f("save_quantized")(C.byref(w.table_c()), bits,
+                                              None if config_text is None else config_text.encode(),
+                                              path.encode()))
 
     def dcat_outputs(self, w: Weights, batch: Batch):
         out = np.zeros((max(batch.n_rows, 1), w.spec.d_model), np.float32)

@@ -77,6 +77,21 @@ HashedEmbeddingTable make_table(const dcat_table* t) {
     return tab;
 }
 
+// The id source a call scores with: the fp32 HashedEmbeddingTable, or (bits 4 / 8) the
+// reference's own quantize() of it (embed.cpp:124-171) as a QuantizedTable.
+struct IdSource {
+    HashedEmbeddingTable fp;
+    QuantizedTable q;
+    bool quant;
+    explicit IdSource(const dcat_table* t) : fp(make_table(t)), quant(t->bits != 0) {
+        if (quant) q = quantize(fp, t->bits);
+    }
+    const IdEmbSource& get() const {
+        if (quant) return q;
+        return fp;
+    }
+};
+
 RankingHeadParams make_head(const dcat_head* h, int d_model) {
     RankingHeadParams rp;
     int sel = d_model > 0 ? h->d_module / d_model : 0;
@@ -216,7 +231,8 @@ int ref_rank_forward_batch(const dcat_model_config* c, const dcat_params* prm, c
                            double* logits, double* mlogits, double* probs) {
     return guard([&] {
         TransformerParams p = make_params(c, prm);
-        HashedEmbeddingTable tab = make_table(t);
+        IdSource ids(t);
+        const IdEmbSource& tab = ids.get();
         RankingHeadParams rp = make_head(h, c->d_model);
         FinetuneConfig ft = make_ft(f, h);
         ft.validate(p.cfg);
@@ -235,7 +251,8 @@ int ref_rank_forward_batch_mt(const dcat_model_config* c, const dcat_params* prm
                               double* logits, double* mlogits, double* probs, int32_t n_threads) {
     return guard([&] {
         TransformerParams p = make_params(c, prm);
-        HashedEmbeddingTable tab = make_table(t);
+        IdSource ids(t);
+        const IdEmbSource& tab = ids.get();
         RankingHeadParams rp = make_head(h, c->d_model);
         FinetuneConfig ft = make_ft(f, h);
         ft.validate(p.cfg);
@@ -268,7 +285,8 @@ int ref_context_kv(const dcat_model_config* c, const dcat_params* prm, const dca
                    const dcat_batch* uniques, int32_t layer, int32_t unique, float* k, float* v) {
     return guard([&] {
         TransformerParams p = make_params(c, prm);
-        HashedEmbeddingTable tab = make_table(t);
+        IdSource ids(t);
+        const IdEmbSource& tab = ids.get();
         std::vector<Segment> u = {make_segment(uniques, unique)};
         KVCache cache = context_forward(p, tab, u, false);
         const SeqKV& s = cache.seqs[0];
@@ -283,7 +301,8 @@ int ref_naive_candidate_outputs(const dcat_model_config* c, const dcat_params* p
                                 const dcat_batch* b, float* out) {
     return guard([&] {
         TransformerParams p = make_params(c, prm);
-        HashedEmbeddingTable tab = make_table(t);
+        IdSource ids(t);
+        const IdEmbSource& tab = ids.get();
         std::vector<Segment> segs;
         std::vector<u64> items;
         for (int64_t i = 0; i < b->n_rows; i++) {
@@ -300,7 +319,8 @@ int ref_dcat_outputs(const dcat_model_config* c, const dcat_params* prm, const d
                      const dcat_batch* b, float* h_cand) {
     return guard([&] {
         TransformerParams p = make_params(c, prm);
-        HashedEmbeddingTable tab = make_table(t);
+        IdSource ids(t);
+        const IdEmbSource& tab = ids.get();
         std::vector<Segment> segs;
         std::vector<u64> items;
         for (int64_t i = 0; i < b->n_rows; i++) {
@@ -324,7 +344,8 @@ int ref_dcat_outputs_fixed(const dcat_model_config* c, const dcat_params* prm, c
                            const dcat_batch* b, int32_t window, int32_t rotation, float* h_cand) {
     return guard([&] {
         TransformerParams p = make_params(c, prm);
-        HashedEmbeddingTable tab = make_table(t);
+        IdSource ids(t);
+        const IdEmbSource& tab = ids.get();
         std::vector<Segment> segs;
         std::vector<u64> items;
         for (int64_t i = 0; i < b->n_rows; i++) {
@@ -340,6 +361,24 @@ int ref_dcat_outputs_fixed(const dcat_model_config* c, const dcat_params* prm, c
         Mat e = candidate_inputs(p, tab, items, pos);
         Mat h = cross_forward_fixed(p, cache, plan, e);
         std::memcpy(h_cand, h.a.data(), sizeof(float) * h.a.size());
+    });
+}
+
+// quantize (embed.cpp:124-171): the QuantizedTable payload (J x R packed rows)
+int ref_quantize_table(const dcat_table* t, int32_t bits, uint8_t* packed) {
+    return guard([&] {
+        QuantizedTable q = quantize(make_table(t), bits);
+        std::memcpy(packed, q.packed_row(0, 0), q.payload_bytes());
+    });
+}
+
+// save_quantized (embed.cpp:212-240): a PQTB1 file of the quantized table, with an
+// optional config trailer
+int ref_save_quantized(const dcat_table* t, int32_t bits, const char* config_text, const char* path) {
+    return guard([&] {
+        QuantizedTable q = quantize(make_table(t), bits);
+        if (config_text) q.set_config_text(config_text);
+        save_quantized(q, path);
     });
 }
 

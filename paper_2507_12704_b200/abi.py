@@ -34,7 +34,8 @@ class ParamsC(C.Structure):
 
 class TableC(C.Structure):
     _fields_ = [("num_subtables", C.c_int32), ("rows", C.c_int32), ("d_sub", C.c_int32),
-                ("seeds", C.c_void_p), ("subtables", C.POINTER(C.c_void_p))]
+                ("seeds", C.c_void_p), ("subtables", C.POINTER(C.c_void_p)),
+                ("bits", C.c_int32), ("packed", C.c_void_p)]
 
 
 class HeadC(C.Structure):
@@ -113,6 +114,10 @@ class Weights:
     table_seeds: np.ndarray            # uint64 [J]
     table: np.ndarray                  # float32 [J, R, d_sub]
     head: dict                         # w1,b1,w2,b2,mod_w,mod_b,aux_proj,lt + ints
+    # QuantizedTable (embed.hpp:80-125): bits 4 / 8 and its J x R packed rows (uint8,
+    # ceil(d_sub * bits / 8) code bytes + fp16 scale + fp16 bias each); bits 0 = fp32 table
+    table_bits: int = 0
+    table_packed: Optional[np.ndarray] = None
     _keep: list = field(default_factory=list, repr=False)
 
     def params_c(self) -> ParamsC:
@@ -124,7 +129,16 @@ class Weights:
         J, R, ds = self.table.shape
         subs = (C.c_void_p * J)(*[self.table.ctypes.data + j * R * ds * 4 for j in range(J)])
         self._keep.append(subs)
-        return TableC(J, R, ds, ptr(self.table_seeds), C.cast(subs, C.POINTER(C.c_void_p)))
+        return TableC(J, R, ds, ptr(self.table_seeds), C.cast(subs, C.POINTER(C.c_void_p)),
+                      self.table_bits, ptr(self.table_packed))
+
+    def with_quantized_table(self, bits: int, packed: np.ndarray) -> "Weights":
+        """The same weights scoring through a QuantizedTable payload (e.g. a PQTB1 file's body)."""
+        J, R, ds = self.table.shape
+        assert bits in (4, 8) and packed.dtype == np.uint8
+        assert packed.size == J * R * ((ds * bits + 7) // 8 + 4), "packed payload size"
+        return Weights(self.spec, self.tensors, self.table_seeds, self.table, self.head, bits,
+                       np.ascontiguousarray(packed.reshape(-1)))
 
     def head_c(self) -> HeadC:
         h = self.head

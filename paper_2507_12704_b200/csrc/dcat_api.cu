@@ -99,6 +99,8 @@ struct dcat_model {
     DevAlloc mem;
     // embeddings (fp32)
     float* table = nullptr;
+    uint8_t* qtable = nullptr;  // QuantizedTable payload (bits 4 / 8), dequantized in the gathers
+    int qbits = 0, qrow_bytes = 0, qcode_bytes = 0;
     uint64_t* seed_mix = nullptr;
     int J = 0, R = 0, d_sub = 0;
     float *action_emb = nullptr, *surface_emb = nullptr, *pos_emb = nullptr;
@@ -470,7 +472,8 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     m->last_kv = A.kv;
     m->last_Tp = Tp;
 
-    EmbParams ep{m->table, m->seed_mix, m->J, m->R, m->d_sub, m->action_emb, m->surface_emb, m->pos_emb, de};
+    EmbParams ep{m->table,    m->qtable,     m->qbits,       m->qrow_bytes, m->qcode_bytes, m->seed_mix, m->J,
+                 m->R,        m->d_sub,      m->action_emb,  m->surface_emb, m->pos_emb,    de};
     const float scale = 1.0f / std::sqrt(static_cast<float>(dh));
     auto K_l = [&](int l) { return A.kv + static_cast<size_t>(2 * l) * Tp * d; };
     auto V_l = [&](int l) { return A.kv + static_cast<size_t>(2 * l + 1) * Tp * d; };
@@ -651,7 +654,8 @@ void run_head_only(dcat_model* m, const Staged& sb, const DedupOut& o, const dca
     float* logits_p = m->b_act[11].get<float>(Bp * 3);
     float* mlog_p = m->b_act[12].get<float>(Bp * 3);
     float* tmp = f32 ? m->b_act[13].get<float>(Bp * m->hidden) : nullptr;
-    EmbParams ep{m->table, m->seed_mix, m->J, m->R, m->d_sub, m->action_emb, m->surface_emb, m->pos_emb,
+    EmbParams ep{m->table, m->qtable, m->qbits, m->qrow_bytes, m->qcode_bytes, m->seed_mix, m->J, m->R, m->d_sub,
+                 m->action_emb, m->surface_emb, m->pos_emb,
                  m->cfg.d_emb};
     CandParams cp{sb.candidate, sb.age, nullptr, m->aux_proj, 0, 0, ft.max_events, ft.fresh_days, ft.mid_days,
                   0, kh};
@@ -783,11 +787,21 @@ int dcat_model_create(const dcat_model_config* cfg, const dcat_params* params, c
         m->J = table->num_subtables;
         m->R = table->rows;
         m->d_sub = table->d_sub;
-        std::vector<float> tab(static_cast<size_t>(m->J) * m->R * m->d_sub);
-        for (int j = 0; j < m->J; j++)
-            std::memcpy(tab.data() + static_cast<size_t>(j) * m->R * m->d_sub, table->subtables[j],
-                        sizeof(float) * m->R * m->d_sub);
-        m->table = m->mem.upload(tab.data(), tab.size());
+        if (table->bits != 0) {  // QuantizedTable (embed.hpp:80-125)
+            if (table->bits != 4 && table->bits != 8)
+                return set_err(DCAT_EINVAL, "quantized table: unsupported bit width " + std::to_string(table->bits));
+            if (!table->packed) return set_err(DCAT_EINVAL, "quantized table: packed rows missing");
+            m->qbits = table->bits;
+            m->qcode_bytes = (m->d_sub * m->qbits + 7) / 8;
+            m->qrow_bytes = m->qcode_bytes + 4;  // + fp16 scale + fp16 bias
+            m->qtable = m->mem.upload(table->packed, static_cast<size_t>(m->J) * m->R * m->qrow_bytes);
+        } else {
+            std::vector<float> tab(static_cast<size_t>(m->J) * m->R * m->d_sub);
+            for (int j = 0; j < m->J; j++)
+                std::memcpy(tab.data() + static_cast<size_t>(j) * m->R * m->d_sub, table->subtables[j],
+                            sizeof(float) * m->R * m->d_sub);
+            m->table = m->mem.upload(tab.data(), tab.size());
+        }
         std::vector<uint64_t> sm(m->J);
         for (int j = 0; j < m->J; j++) sm[j] = host_mix64(table->seeds[j]);
         m->seed_mix = m->mem.upload(sm.data(), sm.size());

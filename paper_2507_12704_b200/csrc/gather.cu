@@ -12,6 +12,8 @@
 // One warp per row, 128-bit loads of the fp32 table rows (4 MB at PinFM-base,
 // L2-resident), additions in the reference's order, output bf16 (or fp32 in
 // the parity path).
+#include <cuda_fp16.h>
+
 #include "launch.h"
 
 namespace dcat {
@@ -47,28 +49,43 @@ __device__ __forceinline__ uint32_t table_row(const EmbParams& ep, uint64_t item
 __device__ __forceinline__ uint32_t warp_rows(const EmbParams& ep, uint64_t item, int lane) {
     return lane < ep.J ? table_row(ep, item, lane) : 0u;
 }
-__device__ __forceinline__ const float* sub_row(const EmbParams& ep, uint32_t rows, int c, int lane_c) {
-    const int j = lane_c / ep.d_sub;
+// QuantizedTable row element (dequantize_row, embed.cpp:92-103): codes, then fp16 scale and
+// fp16 bias (read bytewise: rows are not 2-byte aligned for odd code byte counts);
+// value = (float)code * scale + bias with the reference's separate rounding of * and +.
+__device__ __forceinline__ float deq1(const EmbParams& ep, int j, uint32_t r, int e) {
+    const uint8_t* row = ep.q + (static_cast<size_t>(j) * ep.R + r) * ep.row_bytes;
+    const int cb = ep.code_bytes;
+    const float sc = __half2float(__ushort_as_half(static_cast<unsigned short>(row[cb] | (row[cb + 1] << 8))));
+    const float bi = __half2float(__ushort_as_half(static_cast<unsigned short>(row[cb + 2] | (row[cb + 3] << 8))));
+    const uint32_t code = ep.bits == 8 ? row[e] : ((row[e >> 1] >> ((e & 1) * 4)) & 15u);
+    return __fadd_rn(__fmul_rn(static_cast<float>(code), sc), bi);
+}
+// elements cc .. cc + 3 of sub-table j row r (fp32 or quantized table)
+__device__ __forceinline__ float4 sub4(const EmbParams& ep, int j, uint32_t r, int cc) {
+    if (ep.q == nullptr)
+        return __ldg(reinterpret_cast<const float4*>(ep.table + (static_cast<size_t>(j) * ep.R + r) * ep.d_sub + cc));
+    return make_float4(deq1(ep, j, r, cc), deq1(ep, j, r, cc + 1), deq1(ep, j, r, cc + 2), deq1(ep, j, r, cc + 3));
+}
+__device__ __forceinline__ float sub1(const EmbParams& ep, int j, uint32_t r, int cc) {
+    if (ep.q == nullptr) return __ldg(ep.table + (static_cast<size_t>(j) * ep.R + r) * ep.d_sub + cc);
+    return deq1(ep, j, r, cc);
+}
+// row of sub-table j holding column c: lane j's hash (shuffled) or, past 32 sub-tables, recomputed
+__device__ __forceinline__ uint32_t col_row(const EmbParams& ep, uint64_t item, uint32_t rows, int j) {
     const uint32_t r = ep.J <= 32 ? __shfl_sync(0xffffffffu, rows, j & 31) : 0u;
-    return ep.table + (static_cast<size_t>(j) * ep.R + r) * ep.d_sub + (c - j * ep.d_sub);
+    return ep.J > 32 ? table_row(ep, item, j) : r;
 }
 __device__ __forceinline__ float4 lookup4(const EmbParams& ep, uint64_t item, uint32_t rows, int c) {
     const int cl = c < ep.d_emb ? c : ep.d_emb - 1;  // inactive lanes shuffle a valid source lane
-    const float* p = sub_row(ep, rows, cl, cl);
-    if (ep.J > 32) {
-        const int j = cl / ep.d_sub;
-        p = ep.table + (static_cast<size_t>(j) * ep.R + table_row(ep, item, j)) * ep.d_sub + (cl - j * ep.d_sub);
-    }
-    return c < ep.d_emb ? __ldg(reinterpret_cast<const float4*>(p)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int j = cl / ep.d_sub;
+    const uint32_t r = col_row(ep, item, rows, j);
+    return c < ep.d_emb ? sub4(ep, j, r, cl - j * ep.d_sub) : make_float4(0.f, 0.f, 0.f, 0.f);
 }
 __device__ __forceinline__ float lookup1(const EmbParams& ep, uint64_t item, uint32_t rows, int c) {
     const int cl = c < ep.d_emb ? c : ep.d_emb - 1;
-    const float* p = sub_row(ep, rows, cl, cl);
-    if (ep.J > 32) {
-        const int j = cl / ep.d_sub;
-        p = ep.table + (static_cast<size_t>(j) * ep.R + table_row(ep, item, j)) * ep.d_sub + (cl - j * ep.d_sub);
-    }
-    return c < ep.d_emb ? __ldg(p) : 0.f;
+    const int j = cl / ep.d_sub;
+    const uint32_t r = col_row(ep, item, rows, j);
+    return c < ep.d_emb ? sub1(ep, j, r, cl - j * ep.d_sub) : 0.f;
 }
 
 // this lane's 4-column groups of a d_emb row (c = 128 k + 4 lane): sub-table j and offset
@@ -104,8 +121,7 @@ __device__ __forceinline__ void gather_ctx_token_vec(const EmbParams& ep, const 
         const int c = 128 * k + 4 * lane;
         const uint32_t r = __shfl_sync(0xffffffffu, rows, L.j[k] & 31);
         if (c < ep.d_emb) {
-            const float* tp = ep.table + (static_cast<size_t>(L.j[k]) * ep.R + r) * ep.d_sub + L.cc[k];
-            float4 v = __ldg(reinterpret_cast<const float4*>(tp));
+            float4 v = sub4(ep, L.j[k], r, L.cc[k]);
             v = add4(v, __ldg(reinterpret_cast<const float4*>(ae + c)));
             v = add4(v, __ldg(reinterpret_cast<const float4*>(se + c)));
             if (pe) v = add4(v, __ldg(reinterpret_cast<const float4*>(pe + c)));

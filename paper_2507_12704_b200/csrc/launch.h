@@ -79,7 +79,9 @@ void scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* blk, cudaStre
 
 // ---------------------------------------------------------------- gather.cu
 struct EmbParams {
-    const float* table;       // J x R x d_sub
+    const float* table;       // J x R x d_sub (fp32 table) or null
+    const uint8_t* q;         // quantized table rows (QuantizedTable payload) or null
+    int bits, row_bytes, code_bytes;
     const uint64_t* seed_mix; // J: mix64(seed_j)
     int J, R, d_sub;
     const float* action_emb;  // n_actions x d_emb

@@ -107,13 +107,24 @@ dcat_finetune_config to_c(const FinetuneConfig& f) {
 
 Scorer::Scorer(const TransformerParams& p, const HashedEmbeddingTable& table, const RankingHeadParams& rp,
                int device) {
+    std::vector<const float*> subs;
+    for (int j = 0; j < table.num_subtables(); j++) subs.push_back(table.subtable(j).a.data());
+    dcat_table tab{table.num_subtables(), table.rows(), table.d_sub(), table.seeds().data(), subs.data(), 0, nullptr};
+    init(p, tab, rp, device);
+}
+
+// QuantizedTable id source (embed.hpp:80-125): its packed payload goes to the device as is
+Scorer::Scorer(const TransformerParams& p, const QuantizedTable& table, const RankingHeadParams& rp, int device) {
+    dcat_table tab{table.num_subtables(), table.rows(), table.d_sub(), table.seeds().data(), nullptr,
+                   table.bits(),          table.packed_row(0, 0)};
+    init(p, tab, rp, device);
+}
+
+void Scorer::init(const TransformerParams& p, const dcat_table& tab, const RankingHeadParams& rp, int device) {
     std::vector<const Param*> all = p.all_params();
     std::vector<const float*> tensors;
     for (const Param* q : all) tensors.push_back(q->v.a.data());
     dcat_params prm{tensors.data(), static_cast<int32_t>(tensors.size())};
-    std::vector<const float*> subs;
-    for (int j = 0; j < table.num_subtables(); j++) subs.push_back(table.subtable(j).a.data());
-    dcat_table tab{table.num_subtables(), table.rows(), table.d_sub(), table.seeds().data(), subs.data()};
     dcat_head head{};
     head.d_module = rp.d_module;
     head.d_emb = p.cfg.d_emb;
@@ -203,12 +214,17 @@ std::map<std::tuple<const void*, const void*, const void*>, std::unique_ptr<Scor
 
 Scorer& cached(const TransformerParams& p, const IdEmbSource& ids, const RankingHeadParams& rp) {
     const auto* table = dynamic_cast<const HashedEmbeddingTable*>(&ids);
-    SEQFM_CHECK(table != nullptr, "B200 scorer needs a HashedEmbeddingTable id source");
+    const auto* qtable = dynamic_cast<const QuantizedTable*>(&ids);
+    SEQFM_CHECK(table != nullptr || qtable != nullptr,
+                "B200 scorer needs a HashedEmbeddingTable or QuantizedTable id source");
     std::lock_guard<std::mutex> lk(g_mu);
     auto key = std::make_tuple(static_cast<const void*>(&p), static_cast<const void*>(&ids),
                                static_cast<const void*>(&rp));
     auto it = g_cache.find(key);
-    if (it == g_cache.end()) it = g_cache.emplace(key, std::make_unique<Scorer>(p, *table, rp)).first;
+    if (it == g_cache.end())
+        it = g_cache
+                 .emplace(key, table ? std::make_unique<Scorer>(p, *table, rp) : std::make_unique<Scorer>(p, *qtable, rp))
+                 .first;
     return *it->second;
 }
 }  // namespace

@@ -15,6 +15,7 @@
 #include "seqfm/finetune.hpp"
 
 struct dcat_model;
+struct dcat_table;
 
 namespace seqfm {
 namespace b200 {
@@ -24,6 +25,9 @@ class Scorer {
 public:
     Scorer(const TransformerParams& p, const HashedEmbeddingTable& table, const RankingHeadParams& rp,
            int device = 0);
+    // QuantizedTable id source (int4 / int8 rows, fp16 scale / bias; embed.hpp:80-125), e.g. from
+    // load_quantized (PQTB1, embed.cpp:242-287): rows are dequantized on the device
+    Scorer(const TransformerParams& p, const QuantizedTable& table, const RankingHeadParams& rp, int device = 0);
     ~Scorer();
     Scorer(const Scorer&) = delete;
     Scorer& operator=(const Scorer&) = delete;
@@ -45,13 +49,14 @@ public:
     void set_fp32(bool on) { flags_ = on ? 0x2 : 0; }
 
 private:
+    void init(const TransformerParams& p, const struct dcat_table& tab, const RankingHeadParams& rp, int device);
     dcat_model* m_ = nullptr;
     int d_model_ = 0;
     int flags_ = 0;
 };
 
 // Free function with the reference signature. The ids source must be a
-// HashedEmbeddingTable. Weights are uploaded once per (p, ids, rp) address
+// HashedEmbeddingTable or a QuantizedTable. Weights are uploaded once per (p, ids, rp) address
 // triple and cached; call invalidate() after changing weights in place.
 std::vector<RankingOutputs> rank_forward_batch(const TransformerParams& p, const IdEmbSource& ids,
                                                const RankingHeadParams& rp,

@@ -215,6 +215,41 @@ int main() {
         EXPECT(m <= 1e-4, "fixed window vs cross_forward_fixed");
     }
 
+    // 3c. QuantizedTable id source (int4 / int8): the free function with ids = quantize(table)
+    for (int bits : {4, 8}) {
+        ModelConfig c;
+        c.d_model = 16;
+        c.n_layers = 2;
+        c.n_heads = 4;
+        c.d_emb = 16;
+        c.max_len = 16;
+        TransformerParams p;
+        p.init(c, 141);
+        HashedEmbeddingTable table(4, 64, 4, 23);
+        QuantizedTable qt = quantize(table, bits);
+        RankingHeadParams rp;
+        FinetuneConfig cfg;
+        cfg.max_events = 12;
+        rp.init(16, 16, cfg.d_aux, cfg.n_ctx(), cfg.crossing_hidden, 1, 11);
+        Rng r4(19);
+        auto batch = make_batch(4, 3, 12, 0, r4, false);
+        auto ref = rank_forward_batch(p, qt, rp, batch, cfg);
+        b200::Scorer sc(p, qt, rp);
+        sc.set_fp32(true);
+        auto got = sc.rank_forward_batch(batch, cfg);
+        double m = 0;
+        for (size_t i = 0; i < ref.size(); i++)
+            for (int k = 0; k < kRankHeadCount; k++)
+                m = std::max(m, std::fabs(got[i].logit[k] - ref[i].logit[k]) / (std::fabs(ref[i].logit[k]) + 1e-3));
+        std::printf("quantized int%d table vs reference: max rel %.3e\n", bits, m);
+        EXPECT(m <= 1e-4, "quantized table vs rank_forward_batch(QuantizedTable)");
+        auto free_fn = b200::rank_forward_batch(p, qt, rp, batch, cfg);  // bf16 via the free function
+        double mb = 0;
+        for (size_t i = 0; i < ref.size(); i++)
+            for (int k = 0; k < kRankHeadCount; k++) mb = std::max(mb, std::fabs(free_fn[i].logit[k] - ref[i].logit[k]));
+        EXPECT(mb <= 3e-2, "quantized table via the free function");
+    }
+
     // 4. errors surface as std::runtime_error (SEQFM_CHECK)
     {
         TransformerParams p;

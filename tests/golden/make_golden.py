@@ -209,6 +209,45 @@ def gen_fixed(ref):
     np.savez_compressed(os.path.join(HERE, "fixed.npz"), **out)
 
 
+def gen_quant(ref):
+    """test_embed.cpp:90-312: quantize (int4 / int8, fp16 scale/bias, degenerate rows, an odd
+    d_sub whose fp16 fields are unaligned), the PQTB1 container bytes, and rank_forward_batch
+    scoring through the QuantizedTable id source."""
+    import tempfile
+    out = {}
+    spec = small_config(2, 4, 24)
+    for bits in (4, 8):
+        for ds in (4, 5):
+            tab = (4, 64, ds, 23, 0.05)
+            w, sha = make_weights(ref, ModelSpec(d_model=16, n_layers=2, n_heads=4, mlp_ratio=4, max_len=24,
+                                                 d_emb=4 * ds), 31, 0.05, tab, 11, 64, 16, 1)
+            w.table[1, 5, :] = 0.25          # degenerate row: scale 0, codes 0
+            w.table[2, 7, :] = np.linspace(-3.0, 7.5, ds, dtype=np.float32)  # wide range
+            n = f"b{bits}d{ds}"
+            out[n + ".table"] = w.table.copy()
+            out[n + ".seeds"] = w.table_seeds.copy()
+            out[n + ".packed"] = ref.quantize_table(w, bits)
+            with tempfile.TemporaryDirectory() as d:
+                path = os.path.join(d, "t.pqtb1")
+                ref.save_quantized(w, bits, path, config_text=f"bits={bits}\nd_sub={ds}\n" if ds == 4 else None)
+                out[n + ".file"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+    # scoring through the quantized table (rank_forward_batch with ids = QuantizedTable)
+    tab = (4, 64, 4, 23, 0.05)
+    w, sha = make_weights(ref, spec, 41, 0.05, tab, 11, 64, 16, 1)
+    out.update({"rank.spec": spec_fields(spec)["spec"], "rank.sha": np.array(sha),
+                **{"rank." + k: v for k, v in init_args(41, 0.05, tab, 11, 64, 16, 1).items()}})
+    b = make_batch(5, 3, 12, seed=19, ragged=True)
+    out.update(batch_fields(b, "rank."))
+    ft = FinetuneSpec(max_events=12)
+    for bits in (4, 8):
+        wq = w.with_quantized_table(bits, ref.quantize_table(w, bits))
+        logits, mlog, probs, h = ref.rank_forward_batch(wq, ft, b)
+        out[f"rank.b{bits}.logits"] = logits
+        out[f"rank.b{bits}.probs"] = probs
+        out[f"rank.b{bits}.h"] = ref.dcat_outputs(wq, b)
+    np.savez_compressed(os.path.join(HERE, "quant.npz"), **out)
+
+
 def gen_kv(ref):
     """test_dcat.cpp:166-213: context K/V per layer."""
     spec = small_config(2, 4, 16)
@@ -304,6 +343,7 @@ if __name__ == "__main__":
     gen_cross(ref)
     gen_rank(ref)
     gen_fixed(ref)
+    gen_quant(ref)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -311,3 +311,35 @@ def test_fixed_window(api, orc):
         rep, first, b_u = orc.dedup(b)
         kept = np.minimum(b.row_valid[first], max(window - 1, 0)).sum()
         assert m.last_stats()["ctx_tokens"] == kept
+
+
+@pytest.mark.gpu
+def test_quantized_id_table(api, orc):
+    """QuantizedTable id source (int4 / int8 rows, fp16 scale / bias; embed.hpp:80-125) through
+    the C ABI: the gathers dequantize on the fly. Reference-pinned goldens in fp32 (1e-4) and a
+    d=256 PinFM-shaped batch in both precisions against the oracle."""
+    z = G.load("quant")
+    _, w = G.weights_from(z, orc, "rank.")
+    b = G.batch_from(z, "rank.")
+    ft = FinetuneSpec(max_events=12)
+    for bits in (4, 8):
+        wq = w.with_quantized_table(bits, orc.quantize_table(w, bits))
+        m = api.DcatModel(wq)
+        lf, _, hf = m.rank_forward_batch(b, ft, precision="fp32", want_h=True)
+        assert rel_err(lf, z[f"rank.b{bits}.logits"]) <= 1e-4
+        assert float(np.abs(hf - z[f"rank.b{bits}.h"]).max()) <= 1e-4
+    spec, w, b = _base_setup(orc, 4, 8, 96, seed=23, ragged=True)
+    ft = FinetuneSpec(max_events=96)
+    for bits in (4, 8):
+        wq = w.with_quantized_table(bits, orc.quantize_table(w, bits))
+        rl, rm, _, rh = orc.rank_forward_batch(wq, ft, b)
+        m = api.DcatModel(wq)
+        lf, _, hf = m.rank_forward_batch(b, ft, precision="fp32", want_h=True)
+        assert float(np.abs(hf - rh).max()) <= 1e-4 and rel_err(lf, rl) <= 1e-4, bits
+        lb, mb, hb = m.rank_forward_batch(b, ft, want_h=True)
+        assert float(np.abs(hb - rh).max()) <= 3e-2 and cos_min(hb, rh) >= 0.999, bits
+        assert rel_err(lb, rl) <= 3e-2 and rel_err(mb, rm) <= 3e-2, bits
+        # the quantized source really is what scores: int4 differs from the fp32 table
+        if bits == 4:
+            l32, _, _ = api.DcatModel(w).rank_forward_batch(b, ft, precision="fp32")
+            assert float(np.abs(l32 - lf).max()) > 1e-5

@@ -13,6 +13,7 @@ import pytest
 
 import golden_util as G
 from oracle import pyoracle
+from paper_2507_12704_b200.abi import FinetuneSpec
 
 
 @pytest.fixture(scope="module")
@@ -179,3 +180,61 @@ def test_fixed_window_equals_truncated_dcat(orc):
     np.testing.assert_allclose(orc.dcat_outputs_fixed(w, b, W), orc.naive_candidate_outputs(w, t), atol=1e-5)
     big = W + int(b.row_valid.max())
     np.testing.assert_array_equal(orc.dcat_outputs_fixed(w, b, big), orc.dcat_outputs(w, b))
+
+
+def _table_only(table, seeds):
+    from paper_2507_12704_b200.abi import Weights
+    return Weights(None, [], np.ascontiguousarray(seeds), np.ascontiguousarray(table), {})
+
+
+def test_quantize_bitwise(orc):
+    """quantize (embed.cpp:124-171) restated: int4 / int8 payloads, fp16 scale/bias, a degenerate
+    row (scale 0), and an odd d_sub (unaligned fp16 fields) reproduce the reference bytes."""
+    z = G.load("quant")
+    for bits in (4, 8):
+        for ds in (4, 5):
+            n = f"b{bits}d{ds}"
+            w = _table_only(z[n + ".table"], z[n + ".seeds"])
+            np.testing.assert_array_equal(orc.quantize_table(w, bits), z[n + ".packed"], err_msg=n)
+
+
+def test_pqtb1_container():
+    """PQTB1 (embed.cpp:212-287): the package's reader parses the reference's files, dequantizes
+    rows like dequantize_row, and writes them back byte for byte; bad files fail with the
+    reference's messages."""
+    from paper_2507_12704_b200 import pqtb1
+    z = G.load("quant")
+    for bits in (4, 8):
+        for ds in (4, 5):
+            n = f"b{bits}d{ds}"
+            raw = z[n + ".file"].tobytes()
+            q = pqtb1.loads(raw)
+            assert (q.bits, q.num_subtables, q.rows, q.d_sub) == (bits, 4, 64, ds)
+            np.testing.assert_array_equal(q.seeds, z[n + ".seeds"])
+            np.testing.assert_array_equal(q.packed, z[n + ".packed"])
+            assert (q.config_text is not None) == (ds == 4)
+            assert pqtb1.dumps(q) == raw
+            row = q.dequantize_row(2, 7)
+            orig = z[n + ".table"][2, 7]
+            assert np.abs(row - orig).max() <= (orig.max() - orig.min()) / (2 ** bits - 1)
+            np.testing.assert_array_equal(q.dequantize_row(1, 5), np.full(ds, np.float16(0.25), np.float32))
+    raw, bare = z["b8d4.file"].tobytes(), z["b8d5.file"].tobytes()  # with / without config trailer
+    for bad, msg in ((b"XQTB1" + raw[5:], "bad magic"), (raw[:20], "truncated"),
+                     (bare + b"junkjunk", "not a config trailer"), (bare + b"junk", "truncated"), (raw + b"x", "after config trailer")):
+        with pytest.raises(ValueError, match=msg):
+            pqtb1.loads(bad)
+
+
+def test_quantized_rank_bitwise(orc):
+    """rank_forward_batch scoring through a QuantizedTable id source (int4 / int8) reproduces the
+    reference's logits, probs and DCAT rows bit for bit."""
+    z = G.load("quant")
+    _, w = G.weights_from(z, orc, "rank.")
+    b = G.batch_from(z, "rank.")
+    ft = FinetuneSpec(max_events=12)
+    for bits in (4, 8):
+        wq = w.with_quantized_table(bits, orc.quantize_table(w, bits))
+        logits, _, probs, h = orc.rank_forward_batch(wq, ft, b)
+        np.testing.assert_array_equal(logits, z[f"rank.b{bits}.logits"])
+        np.testing.assert_array_equal(probs, z[f"rank.b{bits}.probs"])
+        np.testing.assert_array_equal(orc.dcat_outputs(wq, b), z[f"rank.b{bits}.h"])
