@@ -57,6 +57,8 @@ class CpuImpl:
         self._f("quantize_table").argtypes = [P(TableC), C.c_int32, C.c_void_p]
         if prefix != "oracle":
             self._f("save_quantized").argtypes = [P(TableC), C.c_int32, C.c_char_p, C.c_char_p]
+            self._f("save_checkpoint").argtypes = common + [C.c_void_p, C.c_char_p, C.c_char_p]
+            self._f("write_sequences").argtypes = [C.c_int32] + [C.c_void_p] * 6 + [C.c_char_p, C.c_char_p]
         if prefix == "oracle":
             self._f("dcat_outputs_fixed").argtypes = common + [P(BatchC), C.c_int32, C.c_void_p]
         else:
@@ -167,6 +169,18 @@ class CpuImpl:
         self._check(self._f("save_quantized")(C.byref(w.table_c()), bits,
                                               None if config_text is None else config_text.encode(),
                                               path.encode()))
+
+    def save_checkpoint(self, w: Weights, path: str, extra_config: str = "", with_head: bool = False) -> None:
+        """save_checkpoint (model.cpp:645-666), head as rank.* extra blobs — reference only."""
+        head = C.byref(w.head_c()) if with_head else None
+        self._check(self._f("save_checkpoint")(C.byref(w.spec.c()), C.byref(w.params_c()), C.byref(w.table_c()),
+                                               head, extra_config.encode(), path.encode()))
+
+    def write_sequences(self, user_ids, offsets, ts, action, surface, item, path: str, config_text: str = "") -> None:
+        """write_sequences (seqdata.cpp:235-259) — reference only."""
+        arrs = [np.ascontiguousarray(a) for a in (user_ids, offsets, ts, action, surface, item)]
+        self._check(self._f("write_sequences")(len(arrs[0]), *[a.ctypes.data for a in arrs], config_text.encode(),
+                                               path.encode()))
 
     def dcat_outputs(self, w: Weights, batch: Batch):
         out = np.zeros((max(batch.n_rows, 1), w.spec.d_model), np.float32)

@@ -382,4 +382,42 @@ int ref_save_quantized(const dcat_table* t, int32_t bits, const char* config_tex
     });
 }
 
+// save_checkpoint (model.cpp:645-666): PFMC1 file of the model + table, with extra config
+// text and the ranking head as extra "rank.*" blobs when `head` is non-null
+int ref_save_checkpoint(const dcat_model_config* c, const dcat_params* prm, const dcat_table* t,
+                        const dcat_head* head, const char* extra_config, const char* path) {
+    return guard([&] {
+        TransformerParams p = make_params(c, prm);
+        HashedEmbeddingTable tab = make_table(t);
+        std::vector<std::pair<std::string, Mat>> extra;
+        if (head) {
+            RankingHeadParams rp = make_head(head, c->d_model);
+            for (const Param* q : rp.all_params()) extra.emplace_back(q->name, q->v);
+        }
+        save_checkpoint(p, tab, path, extra_config ? extra_config : "", extra);
+    });
+}
+
+// write_sequences (seqdata.cpp:235-259): PSEQ1 file of n_users users; user u's events are
+// [offset[u], offset[u + 1]) of the pool
+int ref_write_sequences(int32_t n_users, const uint64_t* user_ids, const int64_t* offsets, const uint64_t* ts,
+                        const uint8_t* action, const uint8_t* surface, const uint64_t* item,
+                        const char* config_text, const char* path) {
+    return guard([&] {
+        std::vector<UserSequence> seqs(static_cast<size_t>(n_users));
+        for (int u = 0; u < n_users; u++) {
+            seqs[u].user_id = user_ids[u];
+            for (int64_t e = offsets[u]; e < offsets[u + 1]; e++) {
+                Event ev;
+                ev.timestamp = ts[e];
+                ev.action = static_cast<Action>(action[e]);
+                ev.surface = static_cast<Surface>(surface[e]);
+                ev.item_id = item[e];
+                seqs[u].events.push_back(ev);
+            }
+        }
+        write_sequences(seqs, path, config_text ? config_text : "");
+    });
+}
+
 } // extern "C"

@@ -248,6 +248,44 @@ def gen_quant(ref):
     np.savez_compressed(os.path.join(HERE, "quant.npz"), **out)
 
 
+def gen_files(ref):
+    """On-disk inputs written by the reference: PFMC1 checkpoints (save_checkpoint, with and
+    without the ranking head as rank.* blobs, learned / no positions) and a PSEQ1 sequence file
+    with a config trailer (write_sequences), plus the rank_forward_batch logits of the saved model."""
+    import tempfile
+    out = {}
+    for n, pos in (("ckpt_learned", 1), ("ckpt_nopos", 0)):
+        spec = ModelSpec(d_model=16, n_layers=2, n_heads=4, mlp_ratio=4, max_len=20, d_emb=16, pos_learned=pos)
+        tab = (4, 64, 4, 29, 0.05)
+        w, sha = make_weights(ref, spec, 51 + pos, 0.05, tab, 11, 64, 16, 1)
+        with tempfile.TemporaryDirectory() as d:
+            p = os.path.join(d, "m.pfmc1")
+            ref.save_checkpoint(w, p, extra_config="run.note=golden\n", with_head=bool(pos))
+            out[n + ".file"] = np.frombuffer(open(p, "rb").read(), np.uint8)
+        out.update({n + ".spec": spec_fields(spec)["spec"], n + ".sha": np.array(sha),
+                    **{n + "." + k: v for k, v in init_args(51 + pos, 0.05, tab, 11, 64, 16, 1).items()}})
+        if pos:
+            b = make_batch(3, 2, 10, seed=5, ragged=True)
+            out.update(batch_fields(b, n + "."))
+            out[n + ".logits"] = ref.rank_forward_batch(w, FinetuneSpec(max_events=10), b)[0]
+    rng = np.random.default_rng(31)
+    counts = np.array([5, 0, 12, 1, 7])
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    E = int(offs[-1])
+    ts = np.concatenate([np.sort(rng.integers(1_700_000_000, 1_700_100_000, c)) for c in counts]).astype(np.uint64)
+    uids = rng.integers(0, 2**62, len(counts)).astype(np.uint64)
+    act = rng.integers(0, 7, E).astype(np.uint8)
+    sur = rng.integers(0, 4, E).astype(np.uint8)
+    item = rng.integers(0, 2**40, E).astype(np.uint64)
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "s.pseq1")
+        ref.write_sequences(uids, offs, ts, act, sur, item, p, config_text="data.seed=31\n")
+        out["seq.file"] = np.frombuffer(open(p, "rb").read(), np.uint8)
+    out.update({"seq.user_ids": uids, "seq.offsets": offs, "seq.ts": ts, "seq.action": act, "seq.surface": sur,
+                "seq.item": item})
+    np.savez_compressed(os.path.join(HERE, "files.npz"), **out)
+
+
 def gen_kv(ref):
     """test_dcat.cpp:166-213: context K/V per layer."""
     spec = small_config(2, 4, 16)
@@ -344,6 +382,7 @@ if __name__ == "__main__":
     gen_rank(ref)
     gen_fixed(ref)
     gen_quant(ref)
+    gen_files(ref)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

@@ -343,3 +343,21 @@ def test_quantized_id_table(api, orc):
         if bits == 4:
             l32, _, _ = api.DcatModel(w).rank_forward_batch(b, ft, precision="fp32")
             assert float(np.abs(l32 - lf).max()) > 1e-5
+
+
+@pytest.mark.gpu
+def test_checkpoint_and_sequence_files(api, orc):
+    """A PFMC1 checkpoint written by the reference scores on the device like the saved model,
+    and a PSEQ1 file becomes a request batch (on-disk inputs, SURVEY §8f #3)."""
+    from paper_2507_12704_b200 import ckpt, seqfile
+    z = G.load("files")
+    w = ckpt.loads_checkpoint(z["ckpt_learned.file"].tobytes()).weights()
+    b = G.batch_from(z, "ckpt_learned.")
+    m = api.DcatModel(w)
+    lf, _, _ = m.rank_forward_batch(b, FinetuneSpec(max_events=10), precision="fp32")
+    assert rel_err(lf, z["ckpt_learned.logits"]) <= 1e-4
+    s = seqfile.loads(z["seq.file"].tobytes())
+    sb = seqfile.ranking_batch(s, [0, 2, 2, 3, 4, 0], [11, 12, 13, 14, 15, 16], [3600.0] * 6, max_events=6)
+    rl = orc.rank_forward_batch(w, FinetuneSpec(max_events=10), sb)[0]
+    ls, _, _ = m.rank_forward_batch(sb, FinetuneSpec(max_events=10), precision="fp32")
+    assert rel_err(ls, rl) <= 1e-4
