@@ -34,7 +34,7 @@ extern "C" {
 #define DCAT_OK 0
 #define DCAT_EINVAL (-1)      /* input violates a reference SEQFM_CHECK      */
 #define DCAT_ECUDA (-2)       /* CUDA runtime / launch failure               */
-#define DCAT_EUNSUPPORTED (-3) /* variant not on the device path (AuxLt, Lite) */
+#define DCAT_EUNSUPPORTED (-3) /* shape outside the device kernels (e.g. head dim) */
 #define DCAT_ENOMEM (-4)
 #define DCAT_ENONFINITE (-5)  /* non-finite activation (model.cpp:25-28)     */
 
@@ -171,8 +171,12 @@ int dcat_dedup(dcat_model* m, const dcat_batch* batch, int32_t* rep, int32_t* fi
 /* rank_forward_batch (finetune.cpp:414-493): logits[n_rows*3] and
  * module_logits[n_rows*3] in fp32 (the reference converts the fp32 values to
  * double, finetune.cpp:353-356), h_cand[n_rows*d_model] (cross_forward output,
- * unit-norm rows) when non-NULL. Base and Aux variants and use_seq_module = 0
- * run on the device; AuxLt and the Lite variants return DCAT_EUNSUPPORTED. */
+ * unit-norm rows) when non-NULL. Every fusion variant runs on the device:
+ *   Base / Aux: cross_forward rows;
+ *   AuxLt: the learnable token joins each unique's context (selectors [H_lt | H_cand],
+ *     ranking head d_module = 2 d_model);
+ *   LiteMean / LiteLast: the pooled per-unique selector (h_cand = that selector);
+ *   use_seq_module = 0: ranking head on [cand_emb | ctx] only. */
 int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch,
                             const dcat_finetune_config* cfg, float* logits,
                             float* module_logits, float* h_cand, int32_t flags, void* stream);

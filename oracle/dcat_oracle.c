@@ -583,8 +583,24 @@ static void crossing_forward(const dcat_head* hp, const dcat_finetune_config* ft
     }
 }
 
-/* build_input + forward_one for Base/Aux (finetune.cpp:160-205, 326-348):
- * the per-example path rank_forward (finetune.cpp:403-409). */
+/* gather_selectors for the lite variants (finetune.cpp:258-274): the mean of H's rows
+ * (axpy in row order, then one division per element) or its last row; zeros when empty. */
+static void lite_selector(const Mat* H, int variant, float* sel, int d) {
+    memset(sel, 0, sizeof(float) * d);
+    if (H->rows <= 0) return;
+    if (variant == DCAT_VARIANT_LITE_LAST) {
+        memcpy(sel, row(H, H->rows - 1), sizeof(float) * d);
+        return;
+    }
+    for (int r = 0; r < H->rows; r++) axpy(1.0f, row(H, r), sel, d);
+    for (int j = 0; j < d; j++) sel[j] /= (float)H->rows;
+}
+
+/* build_input + forward_one (finetune.cpp:160-205, 326-348): the per-example path
+ * rank_forward (finetune.cpp:403-409) for every fusion variant:
+ *   Base / Aux: [seq; cand] -> selector H[cand];
+ *   AuxLt: [seq; lt + pos[n]; cand] -> selectors [H[lt]; H[cand]] (d_module = 2 d);
+ *   LiteMean / LiteLast: [seq] -> mean / last row of H (zeros for an empty sequence). */
 static void rank_forward_one(const Model* M, const dcat_table* t, const dcat_head* hp, const dcat_finetune_config* ft,
                              const dcat_batch* b, int64_t i, double* logit, double* mlogit, double* prob) {
     const dcat_model_config* cfg = &M->cfg;
@@ -592,25 +608,45 @@ static void rank_forward_one(const Model* M, const dcat_table* t, const dcat_hea
     float* cand_emb = (float*)amalloc(sizeof(float) * cfg->d_emb);
     lookup(t, b->candidate[i], cand_emb);
     if (!ft->use_seq_module) { crossing_forward(hp, ft, NULL, cand_emb, b, i, logit, mlogit, prob); return; }
+    const int lite = ft->variant == DCAT_VARIANT_LITE_MEAN || ft->variant == DCAT_VARIANT_LITE_LAST;
+    const int with_lt = ft->variant == DCAT_VARIANT_AUXLT;
+    const int with_aux = ft->variant == DCAT_VARIANT_AUX || ft->variant == DCAT_VARIANT_AUXLT;
     int n_seq = b->row_valid[i];
-    int n = n_seq + 1;
+    int n = lite ? n_seq : n_seq + (with_lt ? 2 : 1);
     CHECK(n <= cfg->max_len, "input of %d tokens exceeds max_len %d", n, cfg->max_len);
     Mat e = mat(n, cfg->d_emb);
     if (n_seq > 0) {
         Mat s = segment_inputs(M, t, b, b->row_offset[i], n_seq, 0);
         memcpy(e.a, s.a, sizeof(float) * (size_t)n_seq * cfg->d_emb);
     }
-    float* crow = row(&e, n - 1);
-    memcpy(crow, cand_emb, sizeof(float) * cfg->d_emb);
-    if (ft->variant == DCAT_VARIANT_AUX) {
-        CHECK(b->aux != NULL && b->d_aux > 0, "variant 'aux' requires an auxiliary embedding");
-        CHECK(b->d_aux == hp->d_aux, "aux dim %d != projector rows %d", b->d_aux, hp->d_aux);
-        for (int r = 0; r < hp->d_aux; r++)
-            axpy(b->aux[(size_t)i * b->d_aux + r], hp->aux_proj + (size_t)r * hp->d_emb, crow, cfg->d_emb);
+    if (!lite) {
+        if (with_lt) { /* learnable token between context and candidate (finetune.cpp:186-191) */
+            float* lrow = row(&e, n_seq);
+            memcpy(lrow, hp->lt, sizeof(float) * cfg->d_emb);
+            if (cfg->pos_learned) axpy(1.0f, M->pos_emb + (size_t)n_seq * cfg->d_emb, lrow, cfg->d_emb);
+        }
+        float* crow = row(&e, n - 1);
+        memcpy(crow, cand_emb, sizeof(float) * cfg->d_emb);
+        if (with_aux) {
+            CHECK(b->aux != NULL && b->d_aux > 0, "variant requires an auxiliary embedding");
+            CHECK(b->d_aux == hp->d_aux, "aux dim %d != projector rows %d", b->d_aux, hp->d_aux);
+            for (int r = 0; r < hp->d_aux; r++)
+                axpy(b->aux[(size_t)i * b->d_aux + r], hp->aux_proj + (size_t)r * hp->d_emb, crow, cfg->d_emb);
+        }
+        if (cfg->pos_learned) axpy(1.0f, M->pos_emb + (size_t)(n - 1) * cfg->d_emb, crow, cfg->d_emb);
     }
-    if (cfg->pos_learned) axpy(1.0f, M->pos_emb + (size_t)(n - 1) * cfg->d_emb, crow, cfg->d_emb);
-    Mat H = forward_rows(M, &e);
-    crossing_forward(hp, ft, row(&H, n - 1), cand_emb, b, i, logit, mlogit, prob);
+    Mat H = n > 0 ? forward_rows(M, &e) : mat(0, cfg->d_model);
+    int d = cfg->d_model;
+    float* sel = (float*)amalloc(sizeof(float) * 2 * d);
+    if (lite) {
+        lite_selector(&H, ft->variant, sel, d);
+    } else if (with_lt) {
+        memcpy(sel, row(&H, n - 2), sizeof(float) * d);
+        memcpy(sel + d, row(&H, n - 1), sizeof(float) * d);
+    } else {
+        memcpy(sel, row(&H, n - 1), sizeof(float) * d);
+    }
+    crossing_forward(hp, ft, sel, cand_emb, b, i, logit, mlogit, prob);
 }
 
 static void validate_batch(const dcat_batch* b) {
@@ -648,8 +684,9 @@ static int run_rank_batch(const Model* M, const dcat_table* t, const dcat_head* 
     const dcat_model_config* cfg = &M->cfg;
     int64_t B = b->n_rows;
     if (B == 0) return 0;
-    CHECK(ft->variant == DCAT_VARIANT_BASE || ft->variant == DCAT_VARIANT_AUX,
-          "oracle: variant %d not restated (Base/Aux only)", ft->variant);
+    CHECK(ft->variant >= DCAT_VARIANT_BASE && ft->variant <= DCAT_VARIANT_LITE_LAST, "unknown fusion variant %d",
+          ft->variant);
+    const int lite = ft->variant == DCAT_VARIANT_LITE_MEAN || ft->variant == DCAT_VARIANT_LITE_LAST;
     /* FinetuneConfig::validate essentials (finetune.cpp:54-72) */
     CHECK(cfg->max_len >= ft->max_events + 2, "model.max_len %d too small for max_events %d plus candidate tokens",
           cfg->max_len, ft->max_events);
@@ -659,9 +696,10 @@ static int run_rank_batch(const Model* M, const dcat_table* t, const dcat_head* 
     const int fixed = ft->use_seq_module && ft->window > 0;
     int empty_seq = 0;
     for (int64_t i = 0; i < B; i++) empty_seq |= b->row_valid[i] == 0;
-    /* finetune.cpp:428-431 (the fixed-window path has no per-example fallback: its
-     * cross_forward_fixed handles an empty ring, dcat.cpp:360-390) */
-    if (!ft->use_seq_module || (empty_seq && !fixed)) {
+    /* finetune.cpp:428-431: no sequence module, AuxLt, or an empty sequence run one example at
+     * a time (the fixed-window path has no such fallback: cross_forward_fixed handles an
+     * empty ring, dcat.cpp:360-390) */
+    if (!ft->use_seq_module || ft->variant == DCAT_VARIANT_AUXLT || (empty_seq && !fixed)) {
         for (int64_t i = 0; i < B; i++)
             rank_forward_one(M, t, hp, ft, b, i, logits + 3 * i, mlogits + 3 * i, probs + 3 * i);
         return 0;
@@ -669,6 +707,24 @@ static int run_rank_batch(const Model* M, const dcat_table* t, const dcat_head* 
     int32_t* rep = (int32_t*)amalloc(sizeof(int32_t) * B);
     int32_t* first = (int32_t*)amalloc(sizeof(int32_t) * B);
     int b_u = dedup(b, rep, first); /* dedup keys on the full prefix in both variants */
+    if (lite) { /* finetune.cpp:439-456: the candidate-independent selector once per unique */
+        const int d = cfg->d_model;
+        float* sel_u = (float*)amalloc(sizeof(float) * (size_t)(b_u ? b_u : 1) * d);
+        for (int u = 0; u < b_u; u++) {
+            const int64_t r0 = first[u];
+            Mat e = segment_inputs(M, t, b, b->row_offset[r0], b->row_valid[r0], 0);
+            Mat H = forward_rows(M, &e);
+            lite_selector(&H, ft->variant, sel_u + (size_t)u * d, d);
+        }
+        float* cand_emb = (float*)amalloc(sizeof(float) * cfg->d_emb);
+        for (int64_t i = 0; i < B; i++) {
+            CHECK(b->age_seconds[i] >= 0.0, "candidate age must be non-negative");
+            lookup(t, b->candidate[i], cand_emb);
+            crossing_forward(hp, ft, sel_u + (size_t)rep[i] * d, cand_emb, b, i, logits + 3 * i, mlogits + 3 * i,
+                             probs + 3 * i);
+        }
+        return 0;
+    }
     dcat_batch sb = fixed ? window_view(b, ft->window) : *b;
     SeqKV* cache = context_forward(M, t, &sb, first, b_u);
     uint64_t* items = (uint64_t*)amalloc(sizeof(uint64_t) * B);

@@ -109,7 +109,7 @@ struct dcat_model {
     // ranking head
     int d_module = 0, head_demb = 0, n_ctx = 0, hidden = 0, d_aux = 0, kh = 0, d_feat = 0;
     Lin head1;  // [feat -> hidden], wt zero-padded to kh columns
-    float *hw2 = nullptr, *hb2 = nullptr, *mod_w = nullptr, *mod_b = nullptr, *aux_proj = nullptr;
+    float *hw2 = nullptr, *hb2 = nullptr, *mod_w = nullptr, *mod_b = nullptr, *aux_proj = nullptr, *lt = nullptr;
     // status
     Status* st_dev = nullptr;
     Status* st_host = nullptr;
@@ -255,6 +255,7 @@ Staged stage_batch(dcat_model* m, const dcat_batch* b, bool device, bool aux_nee
     st.in.max_len = m->cfg.max_len;
     st.in.pos_learned = m->cfg.pos_learned;
     st.in.window = 0;
+    st.in.lt_token = 0;
     st.candidate = stage(m->b_in[6], b->candidate, B, device, s, &h2d);
     st.age = stage(m->b_in[7], b->age_seconds, B, device, s, &h2d);
     st.aux = nullptr;
@@ -427,7 +428,13 @@ void attn(dcat_model* m, const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cud
     span(m, a.causal ? "attn.ctx" : "attn.cross", t0, mark(m, s));
 }
 
-// Base / Aux with the sequence module (finetune.cpp:459-492)
+// rank_forward_batch with the sequence module, every fusion variant (finetune.cpp:414-492):
+//   Base / Aux: context pass (last layer K/V only), candidates cross the cached K/V;
+//   LiteMean / LiteLast: full context pass + phi_out, selector = mean / last token row per unique
+//     (the reference's model_forward per unique, :439-456), no crossing pass;
+//   AuxLt: the learnable token is appended to every unique's context (its K/V enter the cache,
+//     its final row through phi_out is the first selector) and candidates cross at position n + 1;
+//     the reference computes the same per example (:428-431), here once per unique.
 template <typename T>
 void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_finetune_config& ft, float* logits,
               float* mlogits, float* h_cand, cudaStream_t s) {
@@ -439,6 +446,9 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     const int64_t Tp = (T_ctx + 127) / 128 * 128, Bp = (B + 127) / 128 * 128, Rr = std::max(Tp, Bp);
     const bool f32 = std::is_same<T, float>::value;
     const int kh = f32 ? m->d_feat : m->kh;
+    const bool lite = ft.variant == DCAT_VARIANT_LITE_MEAN || ft.variant == DCAT_VARIANT_LITE_LAST;
+    const bool auxlt = ft.variant == DCAT_VARIANT_AUXLT;
+    const bool full_last = lite || auxlt;  // the context pass must emit the final hidden rows
 
     int t_stage0 = mark(m, s);
     // tiles + token map
@@ -472,8 +482,8 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     m->last_kv = A.kv;
     m->last_Tp = Tp;
 
-    EmbParams ep{m->table,    m->qtable,     m->qbits,       m->qrow_bytes, m->qcode_bytes, m->seed_mix, m->J,
-                 m->R,        m->d_sub,      m->action_emb,  m->surface_emb, m->pos_emb,    de};
+    EmbParams ep{m->table, m->qtable,     m->qbits,       m->qrow_bytes, m->qcode_bytes, m->seed_mix, m->J,
+                 m->R,     m->d_sub,      m->action_emb,  m->surface_emb, m->pos_emb,    de,          m->lt};
     const float scale = 1.0f / std::sqrt(static_cast<float>(dh));
     auto K_l = [&](int l) { return A.kv + static_cast<size_t>(2 * l) * Tp * d; };
     auto V_l = [&](int l) { return A.kv + static_cast<size_t>(2 * l + 1) * Tp * d; };
@@ -503,7 +513,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         gemm<T>(m, "gemm.ctx.phi_in2", A.h1, d, m->phi_in2, 0, d, M, e, A.tmp, s);
         for (int l = 0; l < nl; l++) {
             const LayerW& L = m->layers[l];
-            if (l == nl - 1) {  // kv_only (dcat.cpp:60-65): K, V of the final layer
+            if (l == nl - 1 && !full_last) {  // kv_only (dcat.cpp:60-65): K, V of the final layer
                 e = base_epi(m, EPI_BIAS);
                 e.bias = L.qkv.bias + d;
                 e.out[0] = K_l(l);
@@ -543,19 +553,73 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             e.resid = A.x;
             e.x_out = A.x;
             e.ld_x = d;
-            e.ln_g = m->layers[l + 1].ln1_g;
-            e.ln_b = m->layers[l + 1].ln1_b;
+            e.ln_g = l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr;  // emitted hidden rows: plain copy
+            e.ln_b = l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr;
             e.ln_out = A.a;
             e.ln_ld = d;
             ffn<T>(m, "ctx", A.a, L, M, e, A.f1, A.tmp, s);
         }
     }
+    // per-unique selector rows (fp32 b_u x d): Lite pools phi_out(H) over a unique's tokens,
+    // AuxLt takes phi_out of its learnable token (the unique's last context row)
+    float* sel = nullptr;
+    if (full_last) {
+        sel = m->b_act[14].get<float>(static_cast<size_t>(std::max(b_u, 1)) * d);
+        const T* src = A.a;
+        int rows = static_cast<int>(T_ctx);
+        if (auxlt) {
+            T* lt_rows = m->b_act[15].get<T>(static_cast<size_t>(std::max(b_u, 1)) * d);
+            gather_last_rows<T>(o.tok_off, b_u, A.a, d, lt_rows, s);
+            m->stats.kernel_launches += 1;
+            src = lt_rows;
+            rows = b_u;
+        }
+        Epi e = base_epi(m, EPI_BIAS);
+        e.act = 1;
+        e.bias = m->phi_out1.bias;
+        e.out[0] = A.h1;
+        e.out_ld[0] = d;
+        e.seg_cols = d;
+        gemm<T>(m, "gemm.ctx.phi_out1", src, d, m->phi_out1, 0, d, rows, e, A.tmp, s);
+        e = base_epi(m, EPI_L2NORM);
+        e.bias = m->phi_out2.bias;
+        e.x_out = lite ? A.x : sel;
+        e.ld_x = d;
+        gemm<T>(m, "gemm.ctx.phi_out2", A.h1, d, m->phi_out2, 0, d, rows, e, A.tmp, s);
+        if (lite) {
+            pool_selectors(o.tok_off, b_u, A.x, d, ft.variant == DCAT_VARIANT_LITE_LAST, sel, s);
+            m->stats.kernel_launches += 1;
+        }
+    }
     int t_ctx1 = mark(m, s);
+    if (lite) {  // candidate-independent selector: no crossing pass (finetune.cpp:439-456)
+        CandParams cp{sb.candidate, sb.age, sb.aux, m->aux_proj, m->d_aux, 0, ft.max_events, ft.fresh_days,
+                      ft.mid_days, m->d_module, kh, 0};
+        gather_candidates<T>(sb.in, o, ep, cp, B, A.E, de, A.feat, s);
+        broadcast_selectors<T>(o.perm, o.rep, B, sel, d, A.feat, kh, 0, h_cand ? A.hc : nullptr, s);
+        module_logits(o.perm, o.rep, B, sel, nullptr, d, m->mod_w, m->mod_b, A.mlog_p, s);
+        m->stats.kernel_launches += 3;
+        int t_cross1 = mark(m, s);
+        Epi e = base_epi(m, EPI_HEAD);
+        e.bias = m->head1.bias;
+        e.w2 = m->hw2;
+        e.b2 = m->hb2;
+        e.logits = A.logits_p;
+        gemm<T>(m, "gemm.head", A.feat, kh, m->head1, 0, m->hidden, static_cast<int>(B), e, A.tmp, s);
+        scatter_outputs(o.perm, B, A.logits_p, A.mlog_p, h_cand ? A.hc : nullptr, d, logits, mlogits, h_cand, s);
+        m->stats.kernel_launches += 1;
+        int t_end = mark(m, s);
+        span(m, "plan", t_stage0, t_ctx0);
+        span(m, "context", t_ctx0, t_ctx1);
+        span(m, "head", t_cross1, t_end);
+        return;
+    }
 
     // ============ crossing pass (candidate_inputs + cross_forward) ============
     const int M = static_cast<int>(B);
-    CandParams cp{sb.candidate, sb.age, sb.aux, m->aux_proj, m->d_aux, ft.variant == DCAT_VARIANT_AUX,
-                  ft.max_events, ft.fresh_days, ft.mid_days, m->d_module, kh};
+    CandParams cp{sb.candidate, sb.age, sb.aux, m->aux_proj, m->d_aux,
+                  ft.variant == DCAT_VARIANT_AUX || ft.variant == DCAT_VARIANT_AUXLT,
+                  ft.max_events, ft.fresh_days, ft.mid_days, m->d_module, kh, auxlt ? 1 : 0};
     gather_candidates<T>(sb.in, o, ep, cp, B, A.E, de, A.feat, s);
     m->stats.kernel_launches += 1;
     Epi e = base_epi(m, EPI_BIAS);
@@ -617,14 +681,19 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     gemm<T>(m, "gemm.cross.phi_out1", A.a, d, m->phi_out1, 0, d, M, e, A.tmp, s);
     e = base_epi(m, EPI_L2NORM);
     e.bias = m->phi_out2.bias;
-    e.x_out = h_cand ? A.hc : nullptr;
+    e.x_out = h_cand || auxlt ? A.hc : nullptr;
     e.ld_x = d;
-    e.out2 = A.feat;  // H_cand occupies feat columns [0, d)
+    e.out2 = auxlt ? A.feat + d : A.feat;  // H_cand: feat columns [0, d) (AuxLt: [d, 2d), after H_lt)
     e.out2_ld = kh;
-    e.mod_w = m->mod_w;
+    e.mod_w = auxlt ? nullptr : m->mod_w;
     e.mod_b = m->mod_b;
     e.mlogits = A.mlog_p;
     gemm<T>(m, "gemm.cross.phi_out2", A.h1, d, m->phi_out2, 0, d, M, e, A.tmp, s);
+    if (auxlt) {  // selectors [H_lt | H_cand] (gather_selectors, finetune.cpp:251-256)
+        broadcast_selectors<T>(o.perm, o.rep, B, sel, d, A.feat, kh, 0, nullptr, s);
+        module_logits(o.perm, o.rep, B, sel, A.hc, d, m->mod_w, m->mod_b, A.mlog_p, s);
+        m->stats.kernel_launches += 2;
+    }
     int t_cross1 = mark(m, s);
     // ranking head: crossing MLP on [H_cand | cand_emb | ctx] (finetune.cpp:301-316)
     e = base_epi(m, EPI_HEAD);
@@ -656,9 +725,9 @@ void run_head_only(dcat_model* m, const Staged& sb, const DedupOut& o, const dca
     float* tmp = f32 ? m->b_act[13].get<float>(Bp * m->hidden) : nullptr;
     EmbParams ep{m->table, m->qtable, m->qbits, m->qrow_bytes, m->qcode_bytes, m->seed_mix, m->J, m->R, m->d_sub,
                  m->action_emb, m->surface_emb, m->pos_emb,
-                 m->cfg.d_emb};
+                 m->cfg.d_emb, m->lt};
     CandParams cp{sb.candidate, sb.age, nullptr, m->aux_proj, 0, 0, ft.max_events, ft.fresh_days, ft.mid_days,
-                  0, kh};
+                  0, kh, 0};
     gather_candidates<T>(sb.in, o, ep, cp, B, E, m->cfg.d_emb, feat, s);
     m->stats.kernel_launches += 1;
     Epi e = base_epi(m, EPI_HEAD);
@@ -680,10 +749,7 @@ void run_head_only(dcat_model* m, const Staged& sb, const DedupOut& o, const dca
 
 int validate_ft(const dcat_model* m, const dcat_finetune_config* ft, const dcat_batch* b) {
     // FinetuneConfig::validate (finetune.cpp:54-72) + ColdStartConfig::validate (:41-47)
-    if (ft->variant == DCAT_VARIANT_AUXLT || ft->variant == DCAT_VARIANT_LITE_MEAN ||
-        ft->variant == DCAT_VARIANT_LITE_LAST)
-        return set_err(DCAT_EUNSUPPORTED, "variant not on the device path (Base / Aux / no-sequence only)");
-    if (ft->variant != DCAT_VARIANT_BASE && ft->variant != DCAT_VARIANT_AUX)
+    if (ft->variant < DCAT_VARIANT_BASE || ft->variant > DCAT_VARIANT_LITE_LAST)
         return set_err(DCAT_EINVAL, "unknown fusion variant");
     if (!(ft->fresh_days > 0.0 && ft->fresh_days < ft->mid_days))
         return set_err(DCAT_EINVAL, "age bands must satisfy 0 < fresh_days < mid_days");
@@ -696,11 +762,15 @@ int validate_ft(const dcat_model* m, const dcat_finetune_config* ft, const dcat_
                                         std::to_string(ft->max_events) + " plus candidate tokens");
     if (!ft->use_seq_module && ft->variant != DCAT_VARIANT_BASE)
         return set_err(DCAT_EINVAL, "disabling the sequence module requires the base variant");
-    if (ft->use_seq_module && m->d_module != m->cfg.d_model)
+    // selector rows per variant (gather_selectors, finetune.cpp:243-274): AuxLt two, else one
+    const int sel_rows = ft->variant == DCAT_VARIANT_AUXLT ? 2 : 1;
+    if (ft->use_seq_module && m->d_module != sel_rows * m->cfg.d_model)
         return set_err(DCAT_EINVAL, "ranking head d_module does not match the sequence module width");
+    if (ft->use_seq_module && ft->variant == DCAT_VARIANT_AUXLT && ft->window > 0)
+        return set_err(DCAT_EINVAL, "the fixed-window module has no learnable token (AuxLt)");
     if (!ft->use_seq_module && m->d_module != 0)
         return set_err(DCAT_EINVAL, "ranking head expects module outputs but use_seq_module is off");
-    if (ft->use_seq_module && ft->variant == DCAT_VARIANT_AUX) {
+    if (ft->use_seq_module && (ft->variant == DCAT_VARIANT_AUX || ft->variant == DCAT_VARIANT_AUXLT)) {
         if (!b->aux || b->d_aux <= 0) return set_err(DCAT_EINVAL, "variant 'aux' requires an auxiliary embedding");
         if (b->d_aux != m->d_aux) return set_err(DCAT_EINVAL, "aux dim mismatch in batch");
     }
@@ -813,8 +883,8 @@ int dcat_model_create(const dcat_model_config* cfg, const dcat_params* params, c
         m->d_aux = head->d_aux;
         if (head->d_emb != c.d_emb || head->n_ctx != 8)
             return set_err(DCAT_EINVAL, "ranking head shape does not match the model (d_emb, n_ctx = 8)");
-        if (m->d_module != 0 && m->d_module != d)
-            return set_err(DCAT_EUNSUPPORTED, "ranking head with more than one selector (AuxLt) is not supported");
+        if (m->d_module != 0 && m->d_module != d && m->d_module != 2 * d)
+            return set_err(DCAT_EINVAL, "ranking head d_module must be 0, d_model or 2 d_model (AuxLt)");
         if (m->hidden < 1 || m->hidden > 256) return set_err(DCAT_EUNSUPPORTED, "crossing hidden must be in [1, 256]");
         m->d_feat = m->d_module + head->d_emb + head->n_ctx;
         m->kh = (m->d_feat + 63) / 64 * 64;
@@ -827,6 +897,8 @@ int dcat_model_create(const dcat_model_config* cfg, const dcat_params* params, c
         m->mod_b = m->mem.upload(head->mod_b ? head->mod_b : zero3.data(), 3);
         std::vector<float> za(static_cast<size_t>(std::max(1, m->d_aux)) * c.d_emb, 0.0f);
         m->aux_proj = m->mem.upload(head->aux_proj && m->d_aux ? head->aux_proj : za.data(), za.size());
+        std::vector<float> zl(static_cast<size_t>(c.d_emb), 0.0f);
+        m->lt = m->mem.upload(head->lt ? head->lt : zl.data(), zl.size());  // AuxLt learnable token
         DCAT_CUDA_CHECK(cudaMalloc(&m->st_dev, sizeof(Status)));
         m->mem.ptrs.push_back(m->st_dev);
         DCAT_CUDA_CHECK(cudaMallocHost(&m->st_host, sizeof(Status)));
@@ -890,8 +962,10 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         m->tile_ctx = m->vt ? 128 : 64;
         m->tile_cross = 128;
         int t0 = mark(m, s);
-        Staged sb = stage_batch(m, batch, device, ft->variant == DCAT_VARIANT_AUX, s);
+        Staged sb = stage_batch(m, batch, device,
+                                ft->variant == DCAT_VARIANT_AUX || ft->variant == DCAT_VARIANT_AUXLT, s);
         sb.in.window = ft->use_seq_module ? ft->window : 0;  // fixed-window sequence module
+        sb.in.lt_token = ft->use_seq_module && ft->variant == DCAT_VARIANT_AUXLT;
         DedupOut o = dedup_buffers(m, B);
         int t1 = mark(m, s);
         run_dedup(m, sb, o, s);

@@ -48,7 +48,7 @@ __device__ void hash_row(const DedupIn& in, int r, uint64_t seed, uint64_t mask,
             return;
         }
         if (in.pos_learned && lane == 0) {
-            const int pv = seq_kept(in, valid);  // positions used: context 0..pv-1, candidate pv
+            const int pv = seq_tokens(in, valid);  // positions used: context 0..pv-1, candidate pv
             if (pv > in.max_len) record_error(st, ERR_POS_CTX, r, pv - 1 >= in.max_len ? in.max_len : pv);
             else if (pv >= in.max_len) record_error(st, ERR_POS_CAND, r, pv);
         }
@@ -103,7 +103,7 @@ __global__ void k_span(DedupIn in, uint64_t* tkey, int32_t* tval, int64_t cap, i
         return;
     }
     if (in.pos_learned) {
-        const int pv = seq_kept(in, valid);  // positions used: context 0..pv-1, candidate pv
+        const int pv = seq_tokens(in, valid);  // positions used: context 0..pv-1, candidate pv
         if (pv > in.max_len) record_error(st, ERR_POS_CTX, r, pv - 1 >= in.max_len ? in.max_len : pv);
         else if (pv >= in.max_len) record_error(st, ERR_POS_CAND, r, pv);
     }
@@ -256,7 +256,7 @@ __global__ void k_unique_sizes(int64_t B, DedupIn in, const int32_t* first, cons
     if (u >= B) return;
     int b_u = st->b_u;
     if (u < b_u) {
-        int n = seq_kept(in, in.row_valid[first[u]]);
+        int n = seq_tokens(in, in.row_valid[first[u]]);
         int c = cnt[u];
         a_cnt[u] = c;
         a_tok[u] = n;
@@ -375,7 +375,7 @@ __global__ void k_tiles(DedupIn in, const int32_t* first, const int32_t* cnt, co
     int b_u = st->b_u;
     int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (u >= b_u) return;
-    int n = seq_kept(in, in.row_valid[first[u]]);
+    int n = seq_tokens(in, in.row_valid[first[u]]);
     int c = cnt[u];
     int64_t t0 = ctx_toff[u];
     for (int j = 0; j * tile_ctx < n; j++) {

@@ -110,11 +110,19 @@ template <typename T>
 __device__ __forceinline__ void gather_ctx_token_vec(const EmbParams& ep, const LaneCols& L, int64_t t, int i,
                                                      uint64_t item, int a, int s, T* __restrict__ E, int ldE,
                                                      int lane) {
+    const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(i) * ep.d_emb : nullptr;
+    T* out = E + t * ldE;
+    if (a < 0) {  // AuxLt learnable token: lt + pos_emb[i] (finetune.cpp:188-190); warp-uniform
+        for (int c = 4 * lane; c < ep.d_emb; c += 128) {
+            float4 v = __ldg(reinterpret_cast<const float4*>(ep.lt + c));
+            if (pe) v = add4(v, __ldg(reinterpret_cast<const float4*>(pe + c)));
+            store4<T>(out + c, v);
+        }
+        return;
+    }
     const uint32_t rows = warp_rows(ep, item, lane);
     const float* ae = ep.action_emb + static_cast<size_t>(a) * ep.d_emb;
     const float* se = ep.surface_emb + static_cast<size_t>(s) * ep.d_emb;
-    const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(i) * ep.d_emb : nullptr;
-    T* out = E + t * ldE;
 #pragma unroll
     for (int k = 0; k < kMaxSteps; k++) {
         if (128 * k >= ep.d_emb) break;
@@ -134,6 +142,15 @@ __device__ __forceinline__ void gather_ctx_token_vec(const EmbParams& ep, const 
 template <typename T, bool VEC>
 __device__ __forceinline__ void gather_ctx_token(const EmbParams& ep, int64_t t, int i, uint64_t item, int a, int s,
                                                  T* __restrict__ E, int ldE, int lane) {
+    if (a < 0) {  // AuxLt learnable token: lt + pos_emb[i] (finetune.cpp:188-190); warp-uniform
+        T* out = E + t * ldE;
+        for (int c = lane; c < ep.d_emb; c += 32) {
+            float v = ep.lt[c];
+            if (ep.pos_emb) v = v + ep.pos_emb[static_cast<size_t>(i) * ep.d_emb + c];
+            ActIO<T>::store(out + c, v);
+        }
+        return;
+    }
     {
         const uint32_t rows = warp_rows(ep, item, lane);
         const float* ae = ep.action_emb + static_cast<size_t>(a) * ep.d_emb;
@@ -182,11 +199,15 @@ __global__ void __launch_bounds__(256, 4) k_gather_ctx(DedupIn in, const int32_t
             const int64_t t = tb + lane;
             const int u = tok_unique[t];
             mi = static_cast<int>(t - tok_off[u]);
-            const int fr = first[u], rv = in.row_valid[fr];
-            const int64_t ev = in.row_offset[fr] + (rv - seq_kept(in, rv)) + mi;  // fixed window: newest events
-            mitem = in.item[ev];
-            ma = in.action[ev];
-            ms = in.surface[ev];
+            const int fr = first[u], rv = in.row_valid[fr], kept = seq_kept(in, rv);
+            if (mi < kept) {
+                const int64_t ev = in.row_offset[fr] + (rv - kept) + mi;  // fixed window: newest events
+                mitem = in.item[ev];
+                ma = in.action[ev];
+                ms = in.surface[ev];
+            } else {
+                ma = -1;  // AuxLt's learnable token after the events (finetune.cpp:186-191)
+            }
         }
         const int nt = T_ctx - tb < TOK ? static_cast<int>(T_ctx - tb) : TOK;
         for (int k = 0; k < nt; k++) {
@@ -218,7 +239,7 @@ __device__ void gather_cand_row(DedupIn in, const int32_t* __restrict__ perm, co
                                 const int32_t* __restrict__ first, const EmbParams& ep, const CandParams& cp,
                                 int64_t p, T* __restrict__ E, int ldE, T* __restrict__ feat, Status* st, int lane) {
     int i = perm[p];
-    int n = seq_kept(in, in.row_valid[first[rep[i]]]);  // candidate position (the ring's free slot)
+    int n = seq_tokens(in, in.row_valid[first[rep[i]]]);  // candidate position (after the context / lt token)
     uint64_t item = cp.candidate[i];
     const uint32_t rows = warp_rows(ep, item, lane);
     const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(n) * ep.d_emb : nullptr;
@@ -233,7 +254,7 @@ __device__ void gather_cand_row(DedupIn in, const int32_t* __restrict__ perm, co
             if (c >= ep.d_emb) continue;
             if (fo) store4<T>(fo + cp.d_model + c, raw);
             float4 v = raw;
-            if (pe) v = add4(v, __ldg(reinterpret_cast<const float4*>(pe + c)));
+            if (pe && !cp.aux_first) v = add4(v, __ldg(reinterpret_cast<const float4*>(pe + c)));
             if (aux) {
                 for (int r = 0; r < cp.d_aux; r++) {
                     float al = aux[r];
@@ -244,6 +265,7 @@ __device__ void gather_cand_row(DedupIn in, const int32_t* __restrict__ perm, co
                     v.w = __fadd_rn(v.w, __fmul_rn(al, pr.w));
                 }
             }
+            if (pe && cp.aux_first) v = add4(v, __ldg(reinterpret_cast<const float4*>(pe + c)));
             store4<T>(out + c, v);
         }
     } else {
@@ -253,10 +275,11 @@ __device__ void gather_cand_row(DedupIn in, const int32_t* __restrict__ perm, co
             if (c >= ep.d_emb) continue;
             if (fo) ActIO<T>::store(fo + cp.d_model + c, raw);
             float v = raw;
-            if (pe) v = v + pe[c];
+            if (pe && !cp.aux_first) v = v + pe[c];
             if (aux)
                 for (int r = 0; r < cp.d_aux; r++)
                     v = __fadd_rn(v, __fmul_rn(aux[r], cp.aux_proj[static_cast<size_t>(r) * ep.d_emb + c]));
+            if (pe && cp.aux_first) v = v + pe[c];
             ActIO<T>::store(out + c, v);
         }
     }

@@ -23,12 +23,17 @@ struct DedupIn {
     const uint64_t* item;
     int n_actions, n_surfaces, max_len, pos_learned;
     int window;  // fixed-window variant: keep the newest min(valid, window - 1) events (0 = off)
+    int lt_token;  // AuxLt: the learnable token is appended to every unique's context (0 / 1)
 };
 
 // Events of a row's span the sequence module uses: all of them, or the newest window - 1
 // (context_forward_fixed, dcat.cpp:301-302); `skip` = leading events dropped.
 __host__ __device__ __forceinline__ int seq_kept(const DedupIn& in, int valid) {
     return in.window > 0 ? (valid < in.window - 1 ? valid : in.window - 1) : valid;
+}
+// context tokens of a unique: its kept events, plus AuxLt's learnable token (finetune.cpp:186-191)
+__host__ __device__ __forceinline__ int seq_tokens(const DedupIn& in, int valid) {
+    return seq_kept(in, valid) + in.lt_token;
 }
 
 struct Tile {  // one attention work item: <= BM query rows of one unique
@@ -88,6 +93,7 @@ struct EmbParams {
     const float* surface_emb; // n_surfaces x d_emb
     const float* pos_emb;     // max_len x d_emb or null
     int d_emb;
+    const float* lt;          // AuxLt learnable token row (d_emb) or null
 };
 template <typename T>
 void gather_context(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const int32_t* tok_unique,
@@ -103,6 +109,8 @@ struct CandParams {
     double fresh_days, mid_days;
     int d_model;            // feat column offset of cand_emb
     int feat_ld;            // feat leading dimension (0 = no feat)
+    int aux_first;          // 1: (lookup + aux) + pos as build_input (finetune.cpp:193-203, AuxLt);
+                            // 0: (lookup + pos) + aux as the batched Aux path (finetune.cpp:468-479)
 };
 template <typename T>
 void gather_candidates(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const CandParams& cp, int64_t B,
@@ -181,5 +189,20 @@ void attention_f32(const AttnArgs& a, cudaStream_t s);
 // ---------------------------------------------------------------- head / scatter
 void scatter_outputs(const int32_t* perm, int64_t B, const float* logits_p, const float* mlog_p, const float* h_p,
                      int d, float* logits, float* mlogits, float* h_cand, cudaStream_t s);
+// Lite selectors (gather_selectors, finetune.cpp:258-274): per unique, the mean (row-order sum,
+// then one division) or the last of its token rows of H (fp32, ld d); zeros when it has none.
+void pool_selectors(const int64_t* tok_off, int b_u, const float* H, int d, int last, float* sel, cudaStream_t s);
+// row tok_off[u + 1] - 1 (a unique's last context token) of src -> dst row u
+template <typename T>
+void gather_last_rows(const int64_t* tok_off, int b_u, const T* src, int d, T* dst, cudaStream_t s);
+// candidate row p (unique-grouped order) <- selector of its unique: feat[p][col0, col0 + d) (activation
+// type) and, when hc is non-null, hc[p][0, d) (fp32)
+template <typename T>
+void broadcast_selectors(const int32_t* perm, const int32_t* rep, int64_t B, const float* sel, int d, T* feat,
+                         int ld, int col0, float* hc, cudaStream_t s);
+// module logits (crossing_forward, finetune.cpp:317-323) of the flattened selectors [sel_u | hc_p]
+// (either part may be null): sum over k ascending of s_k * mod_w[k][j], then + mod_b[j]
+void module_logits(const int32_t* perm, const int32_t* rep, int64_t B, const float* sel_u, const float* hc, int d,
+                   const float* mod_w, const float* mod_b, float* mlog, cudaStream_t s);
 
 }  // namespace dcat

@@ -358,6 +358,40 @@ def gen_rank(ref):
     np.savez_compressed(os.path.join(HERE, "rank.npz"), **out)
 
 
+def gen_variants(ref):
+    """rank_forward_batch for the remaining fusion variants (finetune.cpp:414-457): LiteMean /
+    LiteLast (one causal forward per unique, pooled selector) and AuxLt (per-example forward with
+    the learnable token; d_module = 2 d), with and without empty sequences."""
+    names_all = ["base", "aux", "aux-lt", "lite-mean", "lite-last"]
+    out = {}
+    names = []
+    rng = np.random.default_rng(77)
+    for spec, tab, L in ((ModelSpec(d_model=16, n_layers=1, n_heads=2, mlp_ratio=2, max_len=8, d_emb=8),
+                          (2, 16, 4, 52, 0.05), 4),
+                         (ModelSpec(d_model=64, n_layers=2, n_heads=4, mlp_ratio=4, max_len=34, d_emb=64),
+                          (8, 4096, 8, 7, 0.05), 32)):
+        aux_proj = (0.3 * rng.standard_normal((4, spec.d_emb))).astype(np.float32)
+        for variant in ("lite-mean", "lite-last", "aux-lt"):
+            sel = 2 if variant == "aux-lt" else 1
+            seeds = (61, 0.3, tab, 63, 8, 4, sel)
+            model_seed, tau, _, head_seed, hidden, d_aux, _ = seeds
+            w, sha = make_weights(ref, spec, model_seed, tau, tab, head_seed, hidden, d_aux, sel, 1.0, aux_proj)
+            ft = FinetuneSpec(variant=variant, max_events=L, d_aux=4)
+            for empty in (0, 1):
+                b = make_batch(4, 3, L, seed=70 + empty, layout="grouped", ragged=True, d_aux=4, empty_users=empty)
+                n = f"d{spec.d_model}_{variant}_{'empty' if empty else 'dense'}"
+                logits, mlog, probs, _ = ref.rank_forward_batch(w, ft, b)
+                names.append(n)
+                out.update(batch_fields(b, n + "."))
+                out.update({n + ".spec": spec_fields(spec)["spec"], n + ".sha": np.array(sha), n + ".logits": logits,
+                            n + ".module_logits": mlog, n + ".probs": probs, n + ".aux_proj": aux_proj,
+                            n + ".ft": np.array([names_all.index(variant), 1, L, 4]),
+                            **{n + "." + k: v for k, v in init_args(model_seed, tau, tab, head_seed, hidden, d_aux,
+                                                                    sel).items()}})
+    out["names"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "variants.npz"), **out)
+
+
 def gen_hash(ref):
     """hash_id known answers (embed.cpp:11-14)."""
     import ctypes as C
@@ -383,6 +417,7 @@ if __name__ == "__main__":
     gen_fixed(ref)
     gen_quant(ref)
     gen_files(ref)
+    gen_variants(ref)
     for f in sorted(os.listdir(HERE)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(HERE, f)))

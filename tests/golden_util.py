@@ -53,7 +53,10 @@ def apply_overrides(z, w, prefix: str = ""):
 
 def ft_from(z, prefix: str = "") -> FinetuneSpec:
     v, use, me, da = [int(x) for x in z[prefix + "ft"]]
-    return FinetuneSpec(variant=["base", "aux"][v], use_seq_module=bool(use), max_events=me, d_aux=da)
+    return FinetuneSpec(variant=VARIANT_NAMES[v], use_seq_module=bool(use), max_events=me, d_aux=da)
+
+
+VARIANT_NAMES = ["base", "aux", "aux-lt", "lite-mean", "lite-last"]  # FusionVariant order (finetune.hpp:29)
 
 
 def names(z):

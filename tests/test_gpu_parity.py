@@ -276,7 +276,8 @@ def test_errors(api, orc):
         m.rank_forward_batch(neg, ft)
     with pytest.raises(RuntimeError, match="auxiliary"):
         m.rank_forward_batch(b, FinetuneSpec(variant="aux", max_events=16))
-    with pytest.raises(RuntimeError, match="variant"):
+    # AuxLt needs a two-selector head (d_module = 2 d, finetune.cpp:251-256)
+    with pytest.raises(RuntimeError, match="d_module"):
         m.rank_forward_batch(b, FinetuneSpec(variant="aux-lt", max_events=16))
     with pytest.raises(RuntimeError, match="max_len"):
         m.rank_forward_batch(b, FinetuneSpec(max_events=19))
@@ -361,3 +362,33 @@ def test_checkpoint_and_sequence_files(api, orc):
     rl = orc.rank_forward_batch(w, FinetuneSpec(max_events=10), sb)[0]
     ls, _, _ = m.rank_forward_batch(sb, FinetuneSpec(max_events=10), precision="fp32")
     assert rel_err(ls, rl) <= 1e-4
+
+
+@pytest.mark.gpu
+def test_fusion_variants(api, orc):
+    """LiteMean / LiteLast (pooled per-unique selector, no crossing pass) and AuxLt (learnable
+    token appended to the cached context, selectors [H_lt | H_cand]) on the device: the
+    reference-pinned goldens in fp32 (1e-4, dense and with empty sequences) and a ragged d=256
+    batch in both precisions against the oracle."""
+    z = G.load("variants")
+    for n in G.names(z):
+        _, w = G.weights_from(z, orc, n + ".")
+        G.apply_overrides(z, w, n + ".")
+        b = G.batch_from(z, n + ".")
+        ft = G.ft_from(z, n + ".")
+        lf, mf, _ = api.DcatModel(w).rank_forward_batch(b, ft, precision="fp32")
+        assert rel_err(lf, z[n + ".logits"]) <= 1e-4, n
+        assert rel_err(mf, z[n + ".module_logits"]) <= 1e-4, n
+    spec = ModelSpec(d_model=256, n_layers=2, n_heads=8, mlp_ratio=4, max_len=98, d_emb=256)
+    rng = np.random.default_rng(3)
+    for variant in ("lite-mean", "lite-last", "aux-lt"):
+        w = orc.init_weights(spec, 42, table=(8, 4096, 32, 7, 0.05), head_seed=11, sel=2 if variant == "aux-lt" else 1)
+        w.head["aux_proj"][:] = (0.05 * rng.standard_normal(w.head["aux_proj"].shape)).astype(np.float32)
+        b = make_batch(4, 6, 96, seed=29, ragged=True, d_aux=16)
+        ft = FinetuneSpec(variant=variant, max_events=96)
+        rl, rm, _, _ = orc.rank_forward_batch(w, ft, b)
+        m = api.DcatModel(w)
+        lf, mf, _ = m.rank_forward_batch(b, ft, precision="fp32")
+        assert rel_err(lf, rl) <= 1e-4 and rel_err(mf, rm) <= 1e-4, variant
+        lb, mb, _ = m.rank_forward_batch(b, ft)
+        assert rel_err(lb, rl) <= 3e-2 and rel_err(mb, rm) <= 3e-2, variant

@@ -109,6 +109,22 @@ def test_rank_forward_batch_bitwise(orc):
             np.testing.assert_array_equal(h, z[n + ".h_cand"], err_msg=n)
 
 
+def test_fusion_variants_bitwise(orc):
+    """LiteMean / LiteLast (pooled per-unique selector, finetune.cpp:439-456) and AuxLt (learnable
+    token, finetune.cpp:186-191, per-example) reproduce the reference's rank_forward_batch bit
+    for bit, dense and with empty sequences (the per-example fallback)."""
+    z = G.load("variants")
+    for n in G.names(z):
+        _, w = G.weights_from(z, orc, n + ".")
+        G.apply_overrides(z, w, n + ".")
+        b = G.batch_from(z, n + ".")
+        ft = G.ft_from(z, n + ".")
+        logits, mlog, probs, _ = orc.rank_forward_batch(w, ft, b)
+        np.testing.assert_array_equal(logits, z[n + ".logits"], err_msg=n)
+        np.testing.assert_array_equal(mlog, z[n + ".module_logits"], err_msg=n)
+        np.testing.assert_array_equal(probs, z[n + ".probs"], err_msg=n)
+
+
 def test_errors_match_reference_checks(orc):
     z = G.load("rank")
     n = "tinyrank_base_dcat"
