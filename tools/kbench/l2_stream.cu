@@ -1,0 +1,132 @@
+// l2_stream.cu — TMA streaming probe (not part of the product): CTAs pull 16 KB boxes through
+// an S-stage mbarrier ring, the access pattern of the FFN weight stream.
+//   mode 0: every CTA reads the same 1 MB in the same order (the FFN's W1/W2 stream)
+//   mode 1: same 1 MB, each CTA starting at a different 16 KB block (staggered)
+//   mode 2: each CTA reads its own 1 MB region (no sharing)
+//   C > 1: clusters of C CTAs; each CTA loads 1/C of every box multicast to the whole cluster
+// Prints per-CTA bytes/clk landed in shared memory and the mean TMA issue -> full latency.
+#include <cuda.h>
+
+#include <cstdio>
+#include <cstring>
+
+#include "../../paper_2507_12704_b200/csrc/ptx.cuh"
+
+using namespace dcat;
+
+constexpr int BOX_ROWS = 128, BOX_BYTES = BOX_ROWS * 128;  // [128 x 64] bf16, SW128
+
+template <int S, int C>
+__global__ void __launch_bounds__(32, 1) k_stream(const __grid_constant__ CUtensorMap map, int mode, int iters,
+                                                 int blocks_per_region, unsigned long long* out) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[S], empty[S];
+    const uint32_t rank = C > 1 ? ptx::cluster_rank() : 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], C);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (C > 1) ptx::cluster_sync();
+    if (threadIdx.x != 0) {
+        if (C > 1) ptx::cluster_sync();
+        return;
+    }
+    const int cid = blockIdx.x / C;
+    const int region = mode == 2 ? cid : 0;
+    const int start = mode == 1 ? (cid * 7) % blocks_per_region : 0;
+    unsigned long long lat = 0, t_issue[S];
+    const unsigned long long t0 = clock64();
+    for (int it = 0; it < iters + S; it++) {
+        const int s = it % S;
+        if (it >= S) {  // consume the box issued S iterations ago, then free the slot cluster-wide
+            ptx::mbar_wait(&full[s], ((it - S) / S) & 1);
+            lat += clock64() - t_issue[s];
+            if (C > 1) {
+                for (int r = 0; r < C; r++) ptx::mbar_arrive_cl(ptx::mapa(ptx::smem_u32(&empty[s]), r));
+                ptx::mbar_wait_cl(&empty[s], ((it - S) / S) & 1);
+            }
+        }
+        if (it < iters) {
+            const int blk = (start + it) % blocks_per_region;
+            ptx::mbar_expect_tx(&full[s], BOX_BYTES);
+            t_issue[s] = clock64();
+            const int row0 = (region * blocks_per_region + blk) * BOX_ROWS;
+            if (C == 1)
+                ptx::tma_load_2d(ring + s * BOX_BYTES, &map, &full[s], 0, row0);
+            else
+                ptx::tma_load_2d_mc(ring + s * BOX_BYTES + rank * (BOX_BYTES / C), &map, &full[s], 0,
+                                    row0 + rank * (BOX_ROWS / C), static_cast<uint16_t>((1u << C) - 1));
+        }
+    }
+    const unsigned long long t1 = clock64();
+    out[2 * blockIdx.x] = t1 - t0;
+    out[2 * blockIdx.x + 1] = lat / iters;
+    if (C > 1) ptx::cluster_sync();
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <int S, int C>
+void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out) {
+    const int blocks_per_region = (1 << 20) / BOX_BYTES;  // 1 MB regions
+    const int regions = mode == 2 ? grid / C : 1;
+    CUtensorMap m;
+    cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(regions) * blocks_per_region * BOX_ROWS};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {64, BOX_ROWS / C};
+    cuuint32_t es[2] = {1, 1};
+    enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const int iters = 4096, smem = S * BOX_BYTES + 1024;
+    cudaFuncSetAttribute(k_stream<S, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(32);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    for (int rep = 0; rep < 2; rep++) cudaLaunchKernelEx(&cfg, k_stream<S, C>, m, mode, iters, blocks_per_region, d_out);
+    cudaDeviceSynchronize();
+    unsigned long long h[296];
+    cudaMemcpy(h, d_out, sizeof h, cudaMemcpyDeviceToHost);
+    double cyc = 0, lat = 0;
+    for (int i = 0; i < grid; i++) {
+        cyc += h[2 * i];
+        lat += h[2 * i + 1];
+    }
+    cyc /= grid;
+    lat /= grid;
+    std::printf(
+        "{\"mode\": %d, \"cluster\": %d, \"grid\": %d, \"stages\": %d, \"bytes_per_clk_per_cta\": %.1f, "
+        "\"latency_clk\": %.0f, \"err\": \"%s\"}\n",
+        mode, C, grid, S, static_cast<double>(iters) * BOX_BYTES / cyc, lat, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    EncodeFn enc = reinterpret_cast<EncodeFn>(fn);
+    void* buf;
+    cudaMalloc(&buf, 148ull << 20);
+    cudaMemset(buf, 0, 148ull << 20);
+    unsigned long long* d_out;
+    cudaMalloc(&d_out, 296 * sizeof(unsigned long long));
+    for (int grid : {148, 74, 37, 8}) run<6, 1>(enc, buf, 0, grid, d_out);
+    run<6, 2>(enc, buf, 0, 148, d_out);
+    run<6, 4>(enc, buf, 0, 148, d_out);
+    run<10, 2>(enc, buf, 0, 148, d_out);
+    run<6, 2>(enc, buf, 2, 148, d_out);
+    return 0;
+}
