@@ -179,6 +179,14 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
         "l"(reinterpret_cast<uint64_t>(m)), "r"(cl_bar), "r"(c0), "r"(c1)
         : "memory");
 }
+// 1-D bulk copy global -> shared (no tensor map): `bytes` (multiple of 16) land contiguously,
+// completion counted on `bar`. For operands stored pre-swizzled in global memory.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 // TMA load multicast to every CTA in `mask`: the box lands at the same shared offset in each,
 // and each one's mbarrier at `bar`'s offset receives the bytes
 __device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,

@@ -3,6 +3,7 @@
 //   mode 0: every CTA reads the same 1 MB in the same order (the FFN's W1/W2 stream)
 //   mode 1: same 1 MB, each CTA starting at a different 16 KB block (staggered)
 //   mode 2: each CTA reads its own 1 MB region (no sharing)
+//   mode 3: as mode 0 with 1-D bulk copies (no tensor map), each box as `pieces` copies
 //   C > 1: clusters of C CTAs; each CTA loads 1/C of every box multicast to the whole cluster
 // Prints per-CTA bytes/clk landed in shared memory and the mean TMA issue -> full latency.
 #include <cuda.h>
@@ -18,7 +19,8 @@ constexpr int BOX_ROWS = 128, BOX_BYTES = BOX_ROWS * 128;  // [128 x 64] bf16, S
 
 template <int S, int C>
 __global__ void __launch_bounds__(32, 1) k_stream(const __grid_constant__ CUtensorMap map, int mode, int iters,
-                                                 int blocks_per_region, unsigned long long* out) {
+                                                 int blocks_per_region, unsigned long long* out,
+                                                 const uint8_t* gsrc, int pieces) {
     extern __shared__ uint8_t raw[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
     __shared__ uint64_t full[S], empty[S];
@@ -31,10 +33,7 @@ __global__ void __launch_bounds__(32, 1) k_stream(const __grid_constant__ CUtens
         ptx::fence_barrier_init();
     }
     if (C > 1) ptx::cluster_sync();
-    if (threadIdx.x != 0) {
-        if (C > 1) ptx::cluster_sync();
-        return;
-    }
+    if (threadIdx.x == 0) {
     const int cid = blockIdx.x / C;
     const int region = mode == 2 ? cid : 0;
     const int start = mode == 1 ? (cid * 7) % blocks_per_region : 0;
@@ -55,7 +54,12 @@ __global__ void __launch_bounds__(32, 1) k_stream(const __grid_constant__ CUtens
             ptx::mbar_expect_tx(&full[s], BOX_BYTES);
             t_issue[s] = clock64();
             const int row0 = (region * blocks_per_region + blk) * BOX_ROWS;
-            if (C == 1)
+            if (mode == 3)
+                for (int p = 0; p < pieces; p++)
+                    ptx::bulk_load(ring + s * BOX_BYTES + p * (BOX_BYTES / pieces),
+                                   gsrc + static_cast<size_t>(row0) * 128 + p * (BOX_BYTES / pieces), BOX_BYTES / pieces,
+                                   &full[s]);
+            else if (C == 1)
                 ptx::tma_load_2d(ring + s * BOX_BYTES, &map, &full[s], 0, row0);
             else
                 ptx::tma_load_2d_mc(ring + s * BOX_BYTES + rank * (BOX_BYTES / C), &map, &full[s], 0,
@@ -65,7 +69,9 @@ __global__ void __launch_bounds__(32, 1) k_stream(const __grid_constant__ CUtens
     const unsigned long long t1 = clock64();
     out[2 * blockIdx.x] = t1 - t0;
     out[2 * blockIdx.x + 1] = lat / iters;
-    if (C > 1) ptx::cluster_sync();
+    }
+    __syncwarp();
+    if (C > 1) ptx::cluster_sync();  // .aligned: the whole warp, converged
 }
 
 typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -73,7 +79,7 @@ typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void
                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 template <int S, int C>
-void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out) {
+void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out, int pieces = 1) {
     const int blocks_per_region = (1 << 20) / BOX_BYTES;  // 1 MB regions
     const int regions = mode == 2 ? grid / C : 1;
     CUtensorMap m;
@@ -96,7 +102,8 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out)
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    for (int rep = 0; rep < 2; rep++) cudaLaunchKernelEx(&cfg, k_stream<S, C>, m, mode, iters, blocks_per_region, d_out);
+    for (int rep = 0; rep < 2; rep++) cudaLaunchKernelEx(&cfg, k_stream<S, C>, m, mode, iters, blocks_per_region, d_out,
+                                                   static_cast<const uint8_t*>(buf), pieces);
     cudaDeviceSynchronize();
     unsigned long long h[296];
     cudaMemcpy(h, d_out, sizeof h, cudaMemcpyDeviceToHost);
@@ -108,9 +115,10 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out)
     cyc /= grid;
     lat /= grid;
     std::printf(
-        "{\"mode\": %d, \"cluster\": %d, \"grid\": %d, \"stages\": %d, \"bytes_per_clk_per_cta\": %.1f, "
+        "{\"mode\": %d, \"pieces\": %d, \"cluster\": %d, \"grid\": %d, \"stages\": %d, \"bytes_per_clk_per_cta\": %.1f, "
         "\"latency_clk\": %.0f, \"err\": \"%s\"}\n",
-        mode, C, grid, S, static_cast<double>(iters) * BOX_BYTES / cyc, lat, cudaGetErrorString(cudaGetLastError()));
+        mode, pieces, C, grid, S, static_cast<double>(iters) * BOX_BYTES / cyc, lat, cudaGetErrorString(cudaGetLastError()));
+    std::fflush(stdout);
 }
 
 int main() {
@@ -123,10 +131,14 @@ int main() {
     cudaMemset(buf, 0, 148ull << 20);
     unsigned long long* d_out;
     cudaMalloc(&d_out, 296 * sizeof(unsigned long long));
-    for (int grid : {148, 74, 37, 8}) run<6, 1>(enc, buf, 0, grid, d_out);
-    run<6, 2>(enc, buf, 0, 148, d_out);
-    run<6, 4>(enc, buf, 0, 148, d_out);
-    run<10, 2>(enc, buf, 0, 148, d_out);
-    run<6, 2>(enc, buf, 2, 148, d_out);
+    for (int grid : {148, 8}) run<6, 1>(enc, buf, 0, grid, d_out);
+    run<4, 1>(enc, buf, 0, 148, d_out);
+    run<10, 1>(enc, buf, 0, 148, d_out);
+    for (int pieces : {1, 2, 4}) {
+        run<4, 1>(enc, buf, 3, 148, d_out, pieces);
+        run<6, 1>(enc, buf, 3, 148, d_out, pieces);
+        run<10, 1>(enc, buf, 3, 148, d_out, pieces);
+    }
+    run<6, 1>(enc, buf, 3, 8, d_out, 1);
     return 0;
 }

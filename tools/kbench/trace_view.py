@@ -9,4 +9,4 @@ ev = sorted(tuple(map(int, x.split(':'))) for x in line.split()[1:])
 t0 = ev[0][0]
 lim = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 for t, c, j in ev[:lim]:
-    print(f"{t - t0:8d} {NAMES.get(c, c):10s} {j}")
+    print(f"{t - t0:8d} {str(NAMES.get(c, c)):10s} {j}")
