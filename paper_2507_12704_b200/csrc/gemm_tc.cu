@@ -37,6 +37,7 @@
 
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "launch.h"
 #include "ptx.cuh"
@@ -730,16 +731,24 @@ struct FfnCfg {
 };
 
 #if DCAT_FFN_TRACE
-__device__ unsigned long long g_ffn_trace[8192];
-__device__ unsigned int g_ffn_trace_n;
-#define FFN_EV(code, j)                                                                       \
-    do {                                                                                      \
-        if (blockIdx.x == 0 && i < 4) {                                                       \
-            unsigned k_ = atomicAdd(&g_ffn_trace_n, 1u);                                      \
-            if (k_ < 8192)                                                                    \
-                g_ffn_trace[k_] = (static_cast<unsigned long long>(clock64()) << 16) |        \
-                                  (static_cast<unsigned>(code) << 8) | static_cast<unsigned>(j); \
-        }                                                                                     \
+// clock64 timeline of CTAs 0 and 1, first 4 tiles: one recording thread per role (producer,
+// MMA issuer, epilogue warps 0 and 15), each with its own array and a register-free shared
+// cursor, so an event costs a shared increment and a fire-and-forget global store.
+constexpr int FFN_TR_ROLES = 8, FFN_TR_CAP = 1024;
+__device__ unsigned long long g_ffn_trace[FFN_TR_ROLES * FFN_TR_CAP];
+__device__ unsigned int g_ffn_trace_n[FFN_TR_ROLES];
+#define FFN_EV(code, j)                                                                                   \
+    do {                                                                                                  \
+        if (blockIdx.x < 2 && i < 4) {                                                                    \
+            const int r_ = static_cast<int>(blockIdx.x) * 4 + (warp < 2 ? warp : (warp == 2 ? 2 : 3));    \
+            const unsigned k_ = s_tr_n[r_ & 3]++;                                                         \
+            if (k_ < FFN_TR_CAP) {                                                                        \
+                g_ffn_trace[r_ * FFN_TR_CAP + k_] = (static_cast<unsigned long long>(clock64()) << 16) | \
+                                                    (static_cast<unsigned>(code) << 8) |                  \
+                                                    static_cast<unsigned>(j);                             \
+                g_ffn_trace_n[r_] = k_ + 1;                                                               \
+            }                                                                                             \
+        }                                                                                                 \
     } while (0)
 #else
 #define FFN_EV(code, j) \
@@ -780,6 +789,10 @@ __global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
     uint64_t* rbar = acc2_empty + 1;  // residual block loads, one per epilogue warp
     uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + C::EPI_WARPS);
 
+#if DCAT_FFN_TRACE
+    __shared__ unsigned s_tr_n[4];
+    if (threadIdx.x < 4) s_tr_n[threadIdx.x] = 0;
+#endif
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = CL == 2 ? ptx::cluster_rank() : 0;
     const int units = ((M + 127) / 128 + CL - 1) / CL;  // row tiles of 128 * CL rows
@@ -1350,16 +1363,20 @@ void launch_ffn(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M,
 
 #if DCAT_FFN_TRACE
 void ffn_trace_reset() {
-    unsigned z = 0;
-    DCAT_CUDA_CHECK(cudaMemcpyToSymbol(g_ffn_trace_n, &z, sizeof(z)));
+    unsigned z[FFN_TR_ROLES] = {};
+    DCAT_CUDA_CHECK(cudaMemcpyToSymbol(g_ffn_trace_n, z, sizeof(z)));
 }
+// all roles' events, concatenated (the viewer sorts by time)
 int ffn_trace_read(unsigned long long* out, int cap) {
-    unsigned n = 0;
-    DCAT_CUDA_CHECK(cudaMemcpyFromSymbol(&n, g_ffn_trace_n, sizeof(n)));
-    if (n > 8192u) n = 8192u;
-    if (static_cast<int>(n) > cap) n = static_cast<unsigned>(cap);
-    DCAT_CUDA_CHECK(cudaMemcpyFromSymbol(out, g_ffn_trace, n * sizeof(unsigned long long)));
-    return static_cast<int>(n);
+    unsigned n[FFN_TR_ROLES];
+    DCAT_CUDA_CHECK(cudaMemcpyFromSymbol(n, g_ffn_trace_n, sizeof(n)));
+    std::vector<unsigned long long> all(FFN_TR_ROLES * FFN_TR_CAP);
+    DCAT_CUDA_CHECK(cudaMemcpyFromSymbol(all.data(), g_ffn_trace, all.size() * sizeof(unsigned long long)));
+    int m = 0;
+    for (int r = 0; r < FFN_TR_ROLES; r++)
+        for (unsigned k = 0; k < n[r] && m < cap; k++)
+            out[m++] = all[r * FFN_TR_CAP + k] + (static_cast<unsigned long long>(16 * r) << 8);  // code += 16 role
+    return m;
 }
 #endif
 

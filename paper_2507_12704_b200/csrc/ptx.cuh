@@ -148,6 +148,17 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cl(uint32_t cl_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
 }
+// relaxed forms: no release fence, for arrivals that publish no data of this thread (a
+// release.cluster arrive also waits for the thread's outstanding bulk copies, which
+// serialises a TMA producer to one copy in flight)
+__device__ __forceinline__ void mbar_arrive_cl_relaxed(uint32_t cl_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_cl_relaxed(uint32_t cl_addr, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cl_addr),
+                 "r"(bytes)
+                 : "memory");
+}
 __device__ __forceinline__ void mbar_expect_tx_cl(uint32_t cl_addr, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cl_addr),
                  "r"(bytes)

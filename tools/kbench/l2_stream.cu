@@ -4,6 +4,16 @@
 //   mode 1: same 1 MB, each CTA starting at a different 16 KB block (staggered)
 //   mode 2: each CTA reads its own 1 MB region (no sharing)
 //   mode 3: as mode 0 with 1-D bulk copies (no tensor map), each box as `pieces` copies
+//   mode 4: CTA pairs as in the pair FFN: each CTA loads its own box with the .cta_group::2 TMA,
+//           completion on the leader CTA's mbarrier (expect_tx from both); the leader frees the
+//           slot for both (remote arrive on the peer's empty barrier)
+//   mode 5: CTA pairs, each CTA loads its own box with plain TMA onto its own mbarrier; the peer
+//           forwards "my half landed" to the leader with one remote arrive per slot
+//   mode 6: as mode 4 with relaxed remote arrivals (expect_tx and the empty-slot arrivals)
+//   mode 7: clusters of 2, but each CTA streams independently (plain TMA, own barriers)
+//   mode 8: CTA pairs, plain TMA per CTA onto its own barrier; a forwarder warp in the peer
+//           relays each completed slot to a second leader barrier (relaxed remote arrive); the
+//           leader consumes when both are complete and frees the slot in both CTAs (relaxed)
 //   C > 1: clusters of C CTAs; each CTA loads 1/C of every box multicast to the whole cluster
 // Prints per-CTA bytes/clk landed in shared memory and the mean TMA issue -> full latency.
 #include <cuda.h>
@@ -18,21 +28,28 @@ using namespace dcat;
 constexpr int BOX_ROWS = 128, BOX_BYTES = BOX_ROWS * 128;  // [128 x 64] bf16, SW128
 
 template <int S, int C>
-__global__ void __launch_bounds__(32, 1) k_stream(const __grid_constant__ CUtensorMap map, int mode, int iters,
+__global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtensorMap map, int mode, int iters,
                                                  int blocks_per_region, unsigned long long* out,
                                                  const uint8_t* gsrc, int pieces) {
     extern __shared__ uint8_t raw[];
     uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t full[S], empty[S];
+    __shared__ uint64_t full[S], empty[S], fwd[S];
     const uint32_t rank = C > 1 ? ptx::cluster_rank() : 0;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; s++) {
-            ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], C);
+            ptx::mbar_init(&full[s], mode == 4 || mode == 6 || (mode == 5 && rank == 0) ? 2 : 1);
+            ptx::mbar_init(&empty[s], mode >= 4 ? 1 : C);
+            ptx::mbar_init(&fwd[s], 1);
         }
         ptx::fence_barrier_init();
     }
     if (C > 1) ptx::cluster_sync();
+    if (C == 2 && mode == 8 && rank == 1 && threadIdx.x == 32) {
+        for (int it = 0; it < iters; it++) {
+            ptx::mbar_wait(&full[it % S], (it / S) & 1);
+            ptx::mbar_arrive_cl_relaxed(ptx::mapa(ptx::smem_u32(&fwd[it % S]), 0));
+        }
+    }
     if (threadIdx.x == 0) {
     const int cid = blockIdx.x / C;
     const int region = mode == 2 ? cid : 0;
@@ -41,20 +58,65 @@ __global__ void __launch_bounds__(32, 1) k_stream(const __grid_constant__ CUtens
     const unsigned long long t0 = clock64();
     for (int it = 0; it < iters + S; it++) {
         const int s = it % S;
-        if (it >= S) {  // consume the box issued S iterations ago, then free the slot cluster-wide
+        if (C == 2 && mode == 8 && it >= S) {
+            if (rank == 0) {
+                ptx::mbar_wait(&full[s], ((it - S) / S) & 1);
+                ptx::mbar_wait(&fwd[s], ((it - S) / S) & 1);
+                lat += clock64() - t_issue[s];
+                ptx::mbar_arrive_cl_relaxed(ptx::mapa(ptx::smem_u32(&empty[s]), 0));
+                ptx::mbar_arrive_cl_relaxed(ptx::mapa(ptx::smem_u32(&empty[s]), 1));
+            }
+            ptx::mbar_wait_cl(&empty[s], ((it - S) / S) & 1);
+        } else if (C == 2 && mode == 5 && it >= S) {
+            if (rank == 0) {
+                ptx::mbar_wait(&full[s], ((it - S) / S) & 1);  // own bytes + the peer's forward
+                lat += clock64() - t_issue[s];
+                ptx::mbar_arrive_cl(ptx::mapa(ptx::smem_u32(&empty[s]), 0));
+                ptx::mbar_arrive_cl(ptx::mapa(ptx::smem_u32(&empty[s]), 1));
+            } else {
+                ptx::mbar_wait(&full[s], ((it - S) / S) & 1);
+                ptx::mbar_arrive_cl(ptx::mapa(ptx::smem_u32(&full[s]), 0));
+            }
+            ptx::mbar_wait_cl(&empty[s], ((it - S) / S) & 1);
+        } else if (C == 2 && (mode == 4 || mode == 6) && it >= S) {  // pair: the leader consumes both halves and frees the slot in both CTAs
+            if (rank == 0) {
+                ptx::mbar_wait(&full[s], ((it - S) / S) & 1);
+                lat += clock64() - t_issue[s];
+                if (mode == 6) {
+                    ptx::mbar_arrive_cl_relaxed(ptx::mapa(ptx::smem_u32(&empty[s]), 0));
+                    ptx::mbar_arrive_cl_relaxed(ptx::mapa(ptx::smem_u32(&empty[s]), 1));
+                } else {
+                    ptx::mbar_arrive_cl(ptx::mapa(ptx::smem_u32(&empty[s]), 0));
+                    ptx::mbar_arrive_cl(ptx::mapa(ptx::smem_u32(&empty[s]), 1));
+                }
+            }
+            ptx::mbar_wait_cl(&empty[s], ((it - S) / S) & 1);
+        } else if (it >= S) {  // consume the box issued S iterations ago, then free the slot cluster-wide
             ptx::mbar_wait(&full[s], ((it - S) / S) & 1);
             lat += clock64() - t_issue[s];
-            if (C > 1) {
+            if (C > 1 && mode != 7) {
                 for (int r = 0; r < C; r++) ptx::mbar_arrive_cl(ptx::mapa(ptx::smem_u32(&empty[s]), r));
                 ptx::mbar_wait_cl(&empty[s], ((it - S) / S) & 1);
             }
         }
         if (it < iters) {
-            const int blk = (start + it) % blocks_per_region;
+            // pair modes: the peer streams the other half of the region, as the pair FFN's halves
+            const int half = (mode >= 4 && rank == 1) ? blocks_per_region / 2 : 0;
+            const int blk = (start + it + half) % blocks_per_region;
+            const int row0 = (region * blocks_per_region + blk) * BOX_ROWS;
+            if (C == 2 && (mode == 4 || mode == 6)) {
+                const uint32_t lead_full = ptx::mapa(ptx::smem_u32(&full[s]), 0);
+                if (mode == 6) ptx::mbar_expect_tx_cl_relaxed(lead_full, BOX_BYTES);
+                else ptx::mbar_expect_tx_cl(lead_full, BOX_BYTES);
+                t_issue[s] = clock64();
+                ptx::tma_load_2d_pair(ptx::smem_u32(ring + s * BOX_BYTES), &map, lead_full, 0, row0);
+                continue;
+            }
             ptx::mbar_expect_tx(&full[s], BOX_BYTES);
             t_issue[s] = clock64();
-            const int row0 = (region * blocks_per_region + blk) * BOX_ROWS;
-            if (mode == 3)
+            if ((C == 2 && (mode == 5 || mode == 8)) || mode == 7)
+                ptx::tma_load_2d(ring + s * BOX_BYTES, &map, &full[s], 0, row0);
+            else if (mode == 3)
                 for (int p = 0; p < pieces; p++)
                     ptx::bulk_load(ring + s * BOX_BYTES + p * (BOX_BYTES / pieces),
                                    gsrc + static_cast<size_t>(row0) * 128 + p * (BOX_BYTES / pieces), BOX_BYTES / pieces,
@@ -85,7 +147,7 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out,
     CUtensorMap m;
     cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(regions) * blocks_per_region * BOX_ROWS};
     cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {64, BOX_ROWS / C};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(mode >= 4 ? BOX_ROWS : BOX_ROWS / C)};
     cuuint32_t es[2] = {1, 1};
     enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -93,7 +155,7 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out,
     cudaFuncSetAttribute(k_stream<S, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(32);
+    cfg.blockDim = dim3(64);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -108,12 +170,15 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out,
     unsigned long long h[296];
     cudaMemcpy(h, d_out, sizeof h, cudaMemcpyDeviceToHost);
     double cyc = 0, lat = 0;
+    int nm = 0;
     for (int i = 0; i < grid; i++) {
+        if (mode >= 4 && mode != 7 && (i & 1)) continue;  // latency is measured by the leader
         cyc += h[2 * i];
         lat += h[2 * i + 1];
+        nm++;
     }
-    cyc /= grid;
-    lat /= grid;
+    cyc /= nm;
+    lat /= nm;
     std::printf(
         "{\"mode\": %d, \"pieces\": %d, \"cluster\": %d, \"grid\": %d, \"stages\": %d, \"bytes_per_clk_per_cta\": %.1f, "
         "\"latency_clk\": %.0f, \"err\": \"%s\"}\n",
@@ -131,14 +196,11 @@ int main() {
     cudaMemset(buf, 0, 148ull << 20);
     unsigned long long* d_out;
     cudaMalloc(&d_out, 296 * sizeof(unsigned long long));
-    for (int grid : {148, 8}) run<6, 1>(enc, buf, 0, grid, d_out);
     run<4, 1>(enc, buf, 0, 148, d_out);
-    run<10, 1>(enc, buf, 0, 148, d_out);
-    for (int pieces : {1, 2, 4}) {
-        run<4, 1>(enc, buf, 3, 148, d_out, pieces);
-        run<6, 1>(enc, buf, 3, 148, d_out, pieces);
-        run<10, 1>(enc, buf, 3, 148, d_out, pieces);
-    }
-    run<6, 1>(enc, buf, 3, 8, d_out, 1);
+    run<6, 1>(enc, buf, 0, 148, d_out);
+    run<6, 2>(enc, buf, 6, 148, d_out);
+    run<6, 2>(enc, buf, 7, 148, d_out);
+    run<6, 2>(enc, buf, 8, 148, d_out);
+    run<10, 2>(enc, buf, 8, 148, d_out);
     return 0;
 }
