@@ -68,8 +68,14 @@ struct EpiMaps {
     CUtensorMap resid, xout, ln, o[3], out2;
 };
 
-template <int BN, int MODE>
+// RB (resident B): EPI_BIAS with BN = 256 and K <= 256 only. The CTA keeps its 256-column weight
+// slice in shared memory for the whole launch (the grid is a multiple of the N-slice count, so
+// every tile of a CTA has the same n0) and streams only A: per 128 x 256 tile the TMA moves
+// 64 KB instead of 192 KB (a per-SM TMA ingress of ~27 B/clk is the bound of these small-K
+// GEMMs; profiles/r01_ffn.md).
+template <int BN, int MODE, bool RB = false>
 struct Cfg {
+    static_assert(!RB || (MODE == EPI_BIAS && BN == 256), "resident B: EPI_BIAS, BN = 256");
     static constexpr bool FULL = MODE == EPI_RESID_LN || MODE == EPI_L2NORM;
     static constexpr int CG = BN == 64 ? 2 : (FULL ? (BN == 512 ? 1 : 2) : 4);  // epilogue warps per lane quadrant
     static constexpr int EPI_WARPS = 4 * CG;
@@ -81,15 +87,18 @@ struct Cfg {
     static constexpr int N_HALVES = BN / MMA_N;
     static constexpr int ACC_BUFS = BN <= 256 ? 2 : 1;
     static constexpr int TMEM_COLS = BN * ACC_BUFS < 32 ? 32 : BN * ACC_BUFS;
-    static constexpr int STAGES = BN == 64 ? (FULL ? 4 : 6) : BN == 128 ? (FULL ? 3 : 4) : BN == 256 ? (FULL ? 2 : 3) : 2;
+    static constexpr int STAGES =
+        RB ? 4 : BN == 64 ? (FULL ? 4 : 6) : BN == 128 ? (FULL ? 3 : 4) : BN == 256 ? (FULL ? 2 : 3) : 2;
     static constexpr int B_BYTES = BN * BK * 2;
-    static constexpr int RING = STAGES * (A_BYTES + B_BYTES);
-    static constexpr int EW = FULL ? 2 * F_BYTES + 2 * H_BYTES : (MODE == EPI_BIAS ? 2 * H_BYTES : 0);  // per warp
+    static constexpr int KB_RES = 4;  // resident B: k-blocks (K <= 256)
+    static constexpr int RING = RB ? STAGES * A_BYTES + KB_RES * B_BYTES : STAGES * (A_BYTES + B_BYTES);
+    static constexpr int HBUF = RB ? 1 : 2;  // bf16 staging buffers per epilogue warp
+    static constexpr int EW = FULL ? 2 * F_BYTES + 2 * H_BYTES : (MODE == EPI_BIAS ? HBUF * H_BYTES : 0);  // per warp
     static constexpr int EPI_SMEM = EW * EPI_WARPS;
     static constexpr int RED = MODE == EPI_BIAS ? 0 : 4 * 3 * CG * 32 * 4;  // [quadrant][value][cg][lane]
     // smem params: EPI_BIAS keeps the whole bias (N <= 4096, every N tile of a persistent CTA);
     // full-row / head modes: bias | ln_g | ln_b | mod_w/w2 | mod_b/b2 of one row (d <= 512)
-    static constexpr int PARAM_FLOATS = MODE == EPI_BIAS ? 4096 : BN == 512 ? 3088 : 1600;
+    static constexpr int PARAM_FLOATS = RB ? BN : MODE == EPI_BIAS ? 4096 : BN == 512 ? 3088 : 1600;
     static constexpr int SMEM = RING + EPI_SMEM + RED + PARAM_FLOATS * 4 + 1024 + 512;
 };
 
@@ -303,11 +312,11 @@ struct EpiWarp {
     uint32_t hb;       // next bf16 staging buffer (alternates on every bf16 store)
 };
 
-template <int BN, int MODE>
+template <int BN, int MODE, bool RB>
 __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, uint32_t tacc, EpiWarp& W,
                                               uint32_t red, uint32_t sp, int q, int cg, int lane, int m0, int n0,
                                               int M, int N, int nvalid, int t, int tiles) {
-    using C = Cfg<BN, MODE>;
+    using C = Cfg<BN, MODE, RB>;
     const ParamLayout PL = param_layout(N);
     const int row_base = m0 + q * 32;
     const int row = row_base + lane;
@@ -322,7 +331,7 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
             if (c >= nvalid) break;
             const int nc = min(32, nvalid - c);
             tmem_load32(tacc + c, v);
-            lds32(sp, n0 + c, p);
+            lds32(sp, (RB ? 0 : n0) + c, p);  // resident B: the smem bias holds this CTA's slice
             if (e.act) {
 #pragma unroll
                 for (int i = 0; i < 32; i++) v[i] = gelu_fast(v[i] + p[i]);
@@ -334,8 +343,8 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
             const int seg = g0 / e.seg_cols;
             if (tma_ok) {
                 const uint32_t buf = W.ew + W.hb * H_BYTES;
-                W.hb ^= 1;
-                staging_free<1>(lane);
+                if constexpr (C::HBUF == 2) W.hb ^= 1;
+                staging_free<C::HBUF - 1>(lane);
                 if (e.out_trans[seg]) {  // V^T: this lane's row becomes column `lane` of a [dims][rows] block
                     write_bf16_col(buf, lane, v);
                     store_block(&mp.o[seg], buf, row_base, g0 - seg * e.seg_cols, lane);
@@ -537,11 +546,11 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
     }
 }
 
-template <int BN, int MODE>
-__global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
+template <int BN, int MODE, bool RB>
+__global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
               const __grid_constant__ Epi e, const __grid_constant__ EpiMaps mp) {
-    using C = Cfg<BN, MODE>;
+    using C = Cfg<BN, MODE, RB>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -554,7 +563,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* rbars = tempty + 2;  // 2 per epilogue warp
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(rbars + 2 * C::EPI_WARPS);
+    uint64_t* b_full = rbars + 2 * C::EPI_WARPS;  // resident B loaded
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(b_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (K + BK - 1) / BK;
@@ -573,10 +583,20 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
             ptx::mbar_init(&tempty[b], C::EPI_WARPS);
         }
         for (int b = 0; b < 2 * C::EPI_WARPS; b++) ptx::mbar_init(&rbars[b], 1);
+        ptx::mbar_init(b_full, 1);
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc(tslot, C::TMEM_COLS);
-    if (warp >= 4) load_params<MODE>(e, s_par, N, threadIdx.x - 128, C::EPI_THREADS);
+    // resident B: every tile of this CTA has n0 = n_res (grid is a multiple of num_n)
+    const int n_res = static_cast<int>(blockIdx.x % num_n) * BN;
+    if (warp >= 4) {
+        if constexpr (RB) {
+            for (int i = threadIdx.x - 128; i < BN; i += C::EPI_THREADS)
+                sts1(s_par + 4u * i, n_res + i < N ? e.bias[n_res + i] : 0.f);
+        } else {
+            load_params<MODE>(e, s_par, N, threadIdx.x - 128, C::EPI_THREADS);
+        }
+    }
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -585,17 +605,26 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
     if (warp == 0) {
         if (lane == 0) {
             uint32_t it = 0;
+            if constexpr (RB) {  // the CTA's weight slice, once
+                ptx::mbar_expect_tx(b_full, nk * C::B_BYTES);
+                for (int kb = 0; kb < nk; kb++)
+#pragma unroll
+                    for (int h = 0; h < C::N_HALVES; h++)
+                        ptx::tma_load_2d(sB + kb * C::B_BYTES + h * C::MMA_N * 128, &tmB, b_full, kb * BK,
+                                         n_res + h * C::MMA_N);
+            }
             for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
                 const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
                 for (int kb = 0; kb < nk; kb++, it++) {
                     const int s = it % C::STAGES;
                     ptx::mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
-                    ptx::mbar_expect_tx(&full[s], A_BYTES + C::B_BYTES);
+                    ptx::mbar_expect_tx(&full[s], RB ? A_BYTES : A_BYTES + C::B_BYTES);
                     ptx::tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], kb * BK, m0);
+                    if constexpr (!RB)
 #pragma unroll
-                    for (int h = 0; h < C::N_HALVES; h++)
-                        ptx::tma_load_2d(sB + s * C::B_BYTES + h * C::MMA_N * 128, &tmB, &full[s], kb * BK,
-                                         n0 + h * C::MMA_N);
+                        for (int h = 0; h < C::N_HALVES; h++)
+                            ptx::tma_load_2d(sB + s * C::B_BYTES + h * C::MMA_N * 128, &tmB, &full[s], kb * BK,
+                                             n0 + h * C::MMA_N);
                 }
             }
         }
@@ -603,6 +632,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_bf16(BM, C::MMA_N);
             uint32_t it = 0, i = 0;
+            if constexpr (RB) ptx::mbar_wait(b_full, 0);
             for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
                 const int buf = i % C::ACC_BUFS;
                 ptx::mbar_wait(&tempty[buf], ((i / C::ACC_BUFS) & 1) ^ 1);
@@ -613,7 +643,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
                     ptx::mbar_wait(&full[s], (it / C::STAGES) & 1);
                     ptx::tc_fence_after();
                     const uint32_t a_base = ptx::smem_u32(sA + s * A_BYTES);
-                    const uint32_t b_base = ptx::smem_u32(sB + s * C::B_BYTES);
+                    const uint32_t b_base = ptx::smem_u32(sB + (RB ? kb : s) * C::B_BYTES);
 #pragma unroll
                     for (int k = 0; k < BK / 16; k++) {
                         const uint64_t ad = ptx::sdesc_sw128(a_base + k * 32);
@@ -661,7 +691,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE>::THREADS, 1)
             ptx::mbar_wait(&tfull[buf], (i / C::ACC_BUFS) & 1);
             ptx::tc_fence_after();
             const uint32_t tacc = tmem + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
-            epilogue_tile<BN, MODE>(e, mp, tacc, W, s_red, s_par, q, cg, lane, m0, n0, M, N, min(BN, N - n0), t,
+            epilogue_tile<BN, MODE, RB>(e, mp, tacc, W, s_red, s_par, q, cg, lane, m0, n0, M, N, min(BN, N - n0), t,
                                     tiles);
             ptx::tc_fence_before();
             __syncwarp();
@@ -1278,26 +1308,33 @@ int num_sms() {
     return n;
 }
 
-template <int BN, int MODE>
+template <int BN, int MODE, bool RB = false>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e, cudaStream_t s) {
-    using C = Cfg<BN, MODE>;
+    using C = Cfg<BN, MODE, RB>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
     static std::once_flag once;
     std::call_once(once, [] {
-        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tc<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tc<BN, MODE, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM));
     });
     {
         const int npad = (N + 31) & ~31;
-        const int need = MODE == EPI_BIAS ? npad : MODE == EPI_HEAD ? 4 * npad + 3 : 6 * npad + 3;
+        const int need = RB ? BN : MODE == EPI_BIAS ? npad : MODE == EPI_HEAD ? 4 * npad + 3 : 6 * npad + 3;
         if (need > C::PARAM_FLOATS)
             throw InvalidArg("gemm_tc: epilogue parameters of N=" + std::to_string(N) + " exceed the smem staging");
     }
     const EpiMaps mp = make_maps(e, M, N);
-    int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+    const int num_n = (N + BN - 1) / BN;
+    int tiles = ((M + BM - 1) / BM) * num_n;
     int grid = tiles < num_sms() ? tiles : num_sms();
-    k_gemm_tc<BN, MODE><<<grid, C::THREADS, C::SMEM, s>>>(ta, tb, M, N, K, e, mp);
+    if constexpr (RB) grid = grid / num_n * num_n;  // a fixed N slice per CTA (tiles >= num_sms here)
+    k_gemm_tc<BN, MODE, RB><<<grid, C::THREADS, C::SMEM, s>>>(ta, tb, M, N, K, e, mp);
     DCAT_LAUNCH_CHECK();
+}
+
+bool resident_b_disabled() {  // A/B switch for measurements: DCAT_NO_RESIDENT_B=1
+    static const bool off = getenv("DCAT_NO_RESIDENT_B") != nullptr;
+    return off;
 }
 
 template <int MODE>
@@ -1306,7 +1343,16 @@ void launch_mode(int BN, const CUtensorMap& ta, const CUtensorMap& tb, int M, in
     switch (BN) {
         case 64: launch<64, MODE>(ta, tb, M, N, K, e, s); break;
         case 128: launch<128, MODE>(ta, tb, M, N, K, e, s); break;
-        case 256: launch<256, MODE>(ta, tb, M, N, K, e, s); break;
+        case 256:
+            // resident weight slice: large M (every CTA gets many tiles of its slice), K <= 256
+            if constexpr (MODE == EPI_BIAS)
+                if (K <= 64 * Cfg<256, EPI_BIAS, true>::KB_RES && !resident_b_disabled() &&
+                    static_cast<long>((M + BM - 1) / BM) * ((N + 255) / 256) >= 4L * num_sms()) {
+                    launch<256, MODE, true>(ta, tb, M, N, K, e, s);
+                    break;
+                }
+            launch<256, MODE>(ta, tb, M, N, K, e, s);
+            break;
         case 512:
             if constexpr (MODE == EPI_RESID_LN || MODE == EPI_L2NORM) {
                 launch<512, MODE>(ta, tb, M, N, K, e, s);

@@ -14,6 +14,7 @@
 //   mode 8: CTA pairs, plain TMA per CTA onto its own barrier; a forwarder warp in the peer
 //           relays each completed slot to a second leader barrier (relaxed remote arrive); the
 //           leader consumes when both are complete and frees the slot in both CTAs (relaxed)
+//   mode 9: as mode 0 with C > 1 (multicast) but relaxed cross-CTA slot release
 //   C > 1: clusters of C CTAs; each CTA loads 1/C of every box multicast to the whole cluster
 // Prints per-CTA bytes/clk landed in shared memory and the mean TMA issue -> full latency.
 #include <cuda.h>
@@ -38,7 +39,7 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; s++) {
             ptx::mbar_init(&full[s], mode == 4 || mode == 6 || (mode == 5 && rank == 0) ? 2 : 1);
-            ptx::mbar_init(&empty[s], mode >= 4 ? 1 : C);
+            ptx::mbar_init(&empty[s], mode >= 4 && mode <= 8 ? 1 : C);
             ptx::mbar_init(&fwd[s], 1);
         }
         ptx::fence_barrier_init();
@@ -95,13 +96,16 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
             ptx::mbar_wait(&full[s], ((it - S) / S) & 1);
             lat += clock64() - t_issue[s];
             if (C > 1 && mode != 7) {
-                for (int r = 0; r < C; r++) ptx::mbar_arrive_cl(ptx::mapa(ptx::smem_u32(&empty[s]), r));
+                for (int r = 0; r < C; r++) {
+                    if (mode == 9) ptx::mbar_arrive_cl_relaxed(ptx::mapa(ptx::smem_u32(&empty[s]), r));
+                    else ptx::mbar_arrive_cl(ptx::mapa(ptx::smem_u32(&empty[s]), r));
+                }
                 ptx::mbar_wait_cl(&empty[s], ((it - S) / S) & 1);
             }
         }
         if (it < iters) {
             // pair modes: the peer streams the other half of the region, as the pair FFN's halves
-            const int half = (mode >= 4 && rank == 1) ? blocks_per_region / 2 : 0;
+            const int half = (mode >= 4 && mode <= 8 && rank == 1) ? blocks_per_region / 2 : 0;
             const int blk = (start + it + half) % blocks_per_region;
             const int row0 = (region * blocks_per_region + blk) * BOX_ROWS;
             if (C == 2 && (mode == 4 || mode == 6)) {
@@ -147,7 +151,7 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out,
     CUtensorMap m;
     cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(regions) * blocks_per_region * BOX_ROWS};
     cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(mode >= 4 ? BOX_ROWS : BOX_ROWS / C)};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(mode >= 4 && mode <= 8 ? BOX_ROWS : BOX_ROWS / C)};
     cuuint32_t es[2] = {1, 1};
     enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -172,7 +176,7 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out,
     double cyc = 0, lat = 0;
     int nm = 0;
     for (int i = 0; i < grid; i++) {
-        if (mode >= 4 && mode != 7 && (i & 1)) continue;  // latency is measured by the leader
+        if (mode >= 4 && mode <= 8 && mode != 7 && (i & 1)) continue;  // latency is measured by the leader
         cyc += h[2 * i];
         lat += h[2 * i + 1];
         nm++;
@@ -198,9 +202,9 @@ int main() {
     cudaMalloc(&d_out, 296 * sizeof(unsigned long long));
     run<4, 1>(enc, buf, 0, 148, d_out);
     run<6, 1>(enc, buf, 0, 148, d_out);
-    run<6, 2>(enc, buf, 6, 148, d_out);
-    run<6, 2>(enc, buf, 7, 148, d_out);
-    run<6, 2>(enc, buf, 8, 148, d_out);
-    run<10, 2>(enc, buf, 8, 148, d_out);
+    run<6, 2>(enc, buf, 9, 148, d_out);
+    run<10, 2>(enc, buf, 9, 148, d_out);
+    run<6, 4>(enc, buf, 9, 148, d_out);
+    run<10, 4>(enc, buf, 9, 148, d_out);
     return 0;
 }
