@@ -58,21 +58,42 @@ def gemm_flops(cfg, U, C, L):
 
 
 def gemm_bytes(cfg, U, C, L):
-    """Algorithmic HBM bytes of all GEMM launches of one step (bf16 activations,
-    fp32 residual stream): per context token phi_in 1K+2K, per full layer
-    qkv 2K + o 3K + ffn1 2.5K + ffn2 4.5K (d=256 units scale with d), last-layer
-    kv 1.5K; per candidate phi_in 3K, 4 layers x 12K, phi_out 2K, head 1.2K.
-    Written generally: A read + outputs written + residual read/written."""
+    """Algorithmic HBM bytes of all tcgen05 GEMM-class launches of one step, as the fused
+    kernels move them (bf16 activations, fp32 residual stream; weights are L2-resident):
+    per row phi_in1 (E in, h1 out) + phi_in2 (h1 in, x + LN1 rows out); per full layer
+    qkv (2d in, 6d out) + the fused layer tail (attention rows 2d + x 4d in, x 4d + next-LN
+    rows 2d out; x_mid, LN2 rows and the d_ff-wide hidden never reach HBM); last context
+    layer kv (2d in, 4d out); per candidate phi_out and the ranking head."""
     s = cfg["spec"]
-    d, de, nl, F = s.d_model, s.d_emb, s.n_layers, s.d_ff
+    d, de, nl = s.d_model, s.d_emb, s.n_layers
     b2, b4 = 2, 4
     phi_in = (de * b2 + d * b2) + (d * b2 + d * b4 + d * b2)
-    layer = (d * b2 + 3 * d * b2) + (d * b2 + 2 * d * b4 + d * b2) + (d * b2 + F * b2) + (F * b2 + 2 * d * b4 + d * b2)
+    layer = (d * b2 + 3 * d * b2) + tail_row_bytes(cfg)
     kv = d * b2 + 2 * d * b2
     kh = (d + de + 8 + 63) // 64 * 64
     per_user = L * (phi_in + (nl - 1) * layer + kv)
     per_cand = phi_in + nl * layer + (d * b2 + d * b2) + (d * b2 + d * b2 + 12) + (kh * b2 + 12)
     return U * per_user + U * C * per_cand
+
+
+def tail_row_bytes(cfg):
+    """Fused layer tail, HBM bytes per row: attention output (bf16) and x (fp32) in, x and the
+    next LN1 rows (bf16) out = 12 d."""
+    d = cfg["spec"].d_model
+    return d * 2 + d * 4 + d * 4 + d * 2
+
+
+def tail_rows(cfg, U, C, L):
+    """Rows through the layer tail per step: L - 1 full context layers per unique user, L
+    crossing layers per candidate (valid = L synthetic sequences)."""
+    nl = cfg["spec"].n_layers
+    return U * L * (nl - 1) + U * C * nl
+
+
+def tail_flops(cfg, U, C, L):
+    """Fused layer tail FLOPs per step: output projection 2 d^2 + FFN 4 d d_ff per row."""
+    s = cfg["spec"]
+    return tail_rows(cfg, U, C, L) * (2 * s.d_model * s.d_model + 4 * s.d_model * s.d_ff)
 
 
 def attn_flops(cfg, U, C, L):
@@ -270,26 +291,33 @@ def run_ours(args, rank, world, local_rank):
     ms_step = ms_dev / K
     value = B_total / (ms_step / 1e3)
     hbm, tf_burst, tf_sus, peak_kind = peaks()
-    # dominant kernel class: the tcgen05 GEMMs (all launches of k_gemm_tc)
+    # GEMM class: every tcgen05 GEMM-class launch (k_gemm_tc + the fused layer tail)
     gemm_ms = sum(v for n, v in stage_tot.items() if n.startswith("gemm.")) / K
     U_loc = B // C  # unique users of this rank (rank 0 reports)
     gf = gemm_flops(cfg, U_loc, C, L)
     gb = gemm_bytes(cfg, U_loc, C, L)
     achieved = gf / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    # dominant kernel: the fused layer tail (k_ffn_tc<d, 1, true>), all its launches of a step
+    tail_ms = sum(v for n, v in stage_tot.items() if n.endswith(".tail")) / K
+    n_tail = 2 * cfg["spec"].n_layers - 1  # tail launches per step: L - 1 context + L crossing layers
+    tf_tail = tail_flops(cfg, U_loc, C, L)
+    tb_tail = tail_rows(cfg, U_loc, C, L) * tail_row_bytes(cfg)
     ctx_f, cross_f = attn_flops(cfg, U, C, L)
     attn_ctx_ms = stage_tot.get("attn.ctx", 0.0) / K
     attn_cross_ms = stage_tot.get("attn.cross", 0.0) / K
     s = spec
     kv_bytes = s.n_layers * 4 * U * L * s.d_model + B * s.n_layers * 8 * s.d_model
-    # measured DRAM bytes (dram__bytes_read + write) of the same GEMM launches from the
-    # committed ncu --set full capture (profiles/), per step of this workload
-    traffic = None
+    # measured DRAM bytes (dram__bytes_read + write) of the same launches from the committed
+    # ncu --set full capture (profiles/gemm_traffic.json, tools/traffic_from_ncu.py), per step
+    traffic = tail_traffic = None
     tp = os.path.join(ROOT, "profiles", "gemm_traffic.json")
     if os.path.exists(tp) and args.config == "pinfm-base" and U_loc == CONFIGS["pinfm-base"]["U"]:
         try:
-            traffic = json.load(open(tp)).get("dram_bytes_per_step")
+            tj = json.load(open(tp))
+            traffic = tj.get("dram_bytes_per_step")
+            tail_traffic = tj.get("tail", {}).get("dram_bytes_per_step")
         except Exception:
-            traffic = None
+            traffic = tail_traffic = None
     stages = {n: round(v / K, 4) for n, v in sorted(stage_tot.items())}
     line = {
         "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -305,18 +333,30 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": round(B_total / (e2e_ms / K / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms / K, 4)},
         "gpu_launches": int(stats["kernel_launches"]) * K,
-        # dominant kernel class: the tcgen05 GEMMs with fused epilogues. At d=256 their
-        # arithmetic intensity (gf / gb ~ 130 flop/B) is below the B200 ridge
-        # (1348.6 TF/s / 6545.6 GB/s ~ 206 flop/B), so the bound is HBM.
-        "roofline": {"bound": "hbm", "kernel": "k_gemm_tc (all tcgen05 GEMM launches of a step, fused epilogues)",
-                     "achieved": round(gb / (gemm_ms / 1e3) / 1e9, 1) if gemm_ms else None, "peak": hbm,
-                     "unit": "GB/s", "frac": round(gb / (gemm_ms / 1e3) / 1e9 / hbm, 4) if gemm_ms else None,
-                     "peak_kind": f"{peak_kind} copy bandwidth", "traffic": traffic,
-                     "algorithmic_bytes_per_step": gb, "gemm_ms_per_step": round(gemm_ms, 4),
-                     "gemm_share_of_step": round(gemm_ms / ms_step, 3),
-                     "tensor": {"achieved_tflops": round(achieved, 1) if achieved else None, "peak": tf_sus,
-                                "frac": round(achieved / tf_sus, 4) if achieved else None,
-                                "flops_per_step": gf, "intensity_flop_per_byte": round(gf / gb, 1)}},
+        # dominant kernel: the fused layer tail (output projection + residual + LN2 + FFN +
+        # residual + next LN1), ~45 % of the step. Per HBM byte it does 2 d^2 + 4 d d_ff flops over
+        # 12 d bytes (~380 flop/B at d = 256), above the B200 ridge (1348.6 TF/s / 6545.6 GB/s
+        # ~ 206 flop/B): tensor bound by the roofline. What binds it in practice is the per-SM
+        # L2 -> SM interface that streams the 1.1 MB of weights per 128-row tile
+        # (profiles/r01_ffn.md: ~27 B/clk per SM, loads and stores together).
+        "roofline": {"bound": "tensor", "kernel": "k_ffn_tc<d, 1, TAIL> (fused layer tail, all launches of a step)",
+                     "achieved": round(tf_tail / (tail_ms / 1e3) / 1e12, 1) if tail_ms else None,
+                     "peak": tf_sus, "unit": "TFLOP/s",
+                     "frac": round(tf_tail / (tail_ms / 1e3) / 1e12 / tf_sus, 4) if tail_ms else None,
+                     "peak_kind": "sustained dense bf16 (MEASURED_PEAKS.json)",
+                     "traffic": round(tail_traffic / n_tail) if tail_traffic else None,
+                     "traffic_note": "ncu dram bytes per launch, mean over the step's tail launches",
+                     "algorithmic_bytes_per_launch": round(tb_tail / n_tail), "flops_per_step": tf_tail,
+                     "ms_per_step": round(tail_ms, 4), "share_of_step": round(tail_ms / ms_step, 3),
+                     "hbm": {"achieved_gbs": round(tb_tail / (tail_ms / 1e3) / 1e9, 1) if tail_ms else None,
+                             "frac": round(tb_tail / (tail_ms / 1e3) / 1e9 / hbm, 4) if tail_ms else None}},
+        "gemm_class": {"kernels": "k_gemm_tc + layer tail (all tcgen05 GEMM launches of a step, fused epilogues)",
+                       "ms_per_step": round(gemm_ms, 4), "share_of_step": round(gemm_ms / ms_step, 3),
+                       "hbm_achieved_gbs": round(gb / (gemm_ms / 1e3) / 1e9, 1) if gemm_ms else None,
+                       "hbm_frac": round(gb / (gemm_ms / 1e3) / 1e9 / hbm, 4) if gemm_ms else None,
+                       "algorithmic_bytes_per_step": gb, "dram_traffic_per_step": traffic,
+                       "tensor_achieved_tflops": round(achieved, 1) if achieved else None,
+                       "tensor_frac": round(achieved / tf_sus, 4) if achieved else None, "flops_per_step": gf},
         "kernels": {
             "attn.ctx": {"ms": round(attn_ctx_ms, 4), "tflops": round(ctx_f / (attn_ctx_ms / 1e3) / 1e12, 1)
                          if attn_ctx_ms else None},

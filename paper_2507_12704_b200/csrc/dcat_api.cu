@@ -410,6 +410,63 @@ void ffn(dcat_model* m, const char* pass, const T* a, const LayerW& L, int M, Ep
     gemm<T>(m, ctx ? "gemm.ctx.ffn2" : "gemm.cross.ffn2", f1, F, L.f2, 0, d, M, fin, tmp, s);
 }
 
+// The rest of a layer after attention (layer_forward model.cpp:378-397, cross_forward's tail
+// dcat.cpp:80-86): x += attn_out . Wo + bo; x += FFN(LN2(x)); a = next LN1(x) (or a copy of x).
+// bf16: one fused tcgen05 kernel (layer_tail_tc; DCAT_NO_TAIL_FUSION=1 selects the two-kernel
+// path); otherwise the o-projection GEMM (writes x and LN2(x)) followed by ffn().
+template <typename T>
+void layer_tail(dcat_model* m, const char* pass, const T* attn_out, const LayerW& L, int l, int M, float* x, T* a,
+                const float* next_g, const float* next_b, T* f1, float* tmp, cudaStream_t s) {
+    const int d = m->cfg.d_model, F = d * m->cfg.mlp_ratio;
+    const bool ctx = pass[0] == 'c' && pass[1] == 't';
+    if constexpr (std::is_same<T, bf16>::value) {
+        // read per call (a handful per pass) so tests can compare both paths in one process
+        const bool two_kernels = getenv("DCAT_NO_TAIL_FUSION") != nullptr || getenv("DCAT_NO_FUSED_FFN") != nullptr;
+        if (!two_kernels && layer_tail_tc_supported(d, F)) {
+            if (M <= 0) return;
+            int t0 = mark(m, s);
+            Epi e = base_epi(m, EPI_RESID_LN, l);
+            e.bias = L.f1.bias;
+            e.b2 = L.f2.bias;
+            e.o_bias = L.o.bias;
+            e.ln2_g = L.ln2_g;
+            e.ln2_b = L.ln2_b;
+            e.resid = x;
+            e.x_out = x;
+            e.ld_x = d;
+            e.ln_g = next_g;
+            e.ln_b = next_b;
+            e.ln_out = a;
+            e.ln_ld = d;
+            layer_tail_tc(attn_out, d, L.o.wt, L.f1.wt, L.f2.wt, M, d, F, e, s);
+            m->stats.kernel_launches += 1;
+            m->stats.gemm_launches += 1;
+            m->stats.gemm_flops += 2.0 * M * d * d + 4.0 * M * F * d;
+            span(m, ctx ? "gemm.ctx.tail" : "gemm.cross.tail", t0, mark(m, s));
+            return;
+        }
+    }
+    Epi e = base_epi(m, EPI_RESID_LN, l);
+    e.bias = L.o.bias;
+    e.resid = x;
+    e.x_out = x;
+    e.ld_x = d;
+    e.ln_g = L.ln2_g;
+    e.ln_b = L.ln2_b;
+    e.ln_out = a;
+    e.ln_ld = d;
+    gemm<T>(m, ctx ? "gemm.ctx.o" : "gemm.cross.o", attn_out, d, L.o, 0, d, M, e, tmp, s);
+    e = base_epi(m, EPI_RESID_LN, l);  // cross_tail's finite check (dcat.cpp:85-86)
+    e.resid = x;
+    e.x_out = x;
+    e.ld_x = d;
+    e.ln_g = next_g;
+    e.ln_b = next_b;
+    e.ln_out = a;
+    e.ln_ld = d;
+    ffn<T>(m, pass, a, L, M, e, f1, tmp, s);
+}
+
 template <typename T>
 void attn(dcat_model* m, const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t s) {
     int t0 = mark(m, s);
@@ -539,25 +596,8 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             AttnArgs aa{A.q,     d,  K_l(l), V_l(l), d, ldvt, nullptr, nullptr, 0, A.ctx, d, ctx_tiles, st.ctx_tiles,
                         H,       dh, scale,  1,      c.max_len + 1};
             attn<T>(m, aa, Rr, Tp, s);
-            e = base_epi(m, EPI_RESID_LN, l);
-            e.bias = L.o.bias;
-            e.resid = A.x;
-            e.x_out = A.x;
-            e.ld_x = d;
-            e.ln_g = L.ln2_g;
-            e.ln_b = L.ln2_b;
-            e.ln_out = A.a;
-            e.ln_ld = d;
-            gemm<T>(m, "gemm.ctx.o", A.ctx, d, L.o, 0, d, M, e, A.tmp, s);
-            e = base_epi(m, EPI_RESID_LN, l);
-            e.resid = A.x;
-            e.x_out = A.x;
-            e.ld_x = d;
-            e.ln_g = l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr;  // emitted hidden rows: plain copy
-            e.ln_b = l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr;
-            e.ln_out = A.a;
-            e.ln_ld = d;
-            ffn<T>(m, "ctx", A.a, L, M, e, A.f1, A.tmp, s);
+            layer_tail<T>(m, "ctx", A.ctx, L, l, M, A.x, A.a, l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr,
+                          l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // emitted rows: copy
         }
     }
     // per-unique selector rows (fp32 b_u x d): Lite pools phi_out(H) over a unique's tokens,
@@ -651,25 +691,8 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         AttnArgs aa{A.q, d,     K_l(l), V_l(l), d, ldvt, A.kself, A.vself, d, A.ctx, d, cross_tiles, st.cross_tiles,
                     H,   dh,    scale,  0,      c.max_len + 1};
         attn<T>(m, aa, Rr, std::max<int64_t>(Tp, 1), s);
-        e = base_epi(m, EPI_RESID_LN, l);
-        e.bias = L.o.bias;
-        e.resid = A.x;
-        e.x_out = A.x;
-        e.ld_x = d;
-        e.ln_g = L.ln2_g;
-        e.ln_b = L.ln2_b;
-        e.ln_out = A.a;
-        e.ln_ld = d;
-        gemm<T>(m, "gemm.cross.o", A.ctx, d, L.o, 0, d, M, e, A.tmp, s);
-        e = base_epi(m, EPI_RESID_LN, l);  // cross_tail's finite check (dcat.cpp:85-86)
-        e.resid = A.x;
-        e.x_out = A.x;
-        e.ld_x = d;
-        e.ln_g = l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr;  // last layer: plain copy for phi_out
-        e.ln_b = l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr;
-        e.ln_out = A.a;
-        e.ln_ld = d;
-        ffn<T>(m, "cross", A.a, L, M, e, A.f1, A.tmp, s);
+        layer_tail<T>(m, "cross", A.ctx, L, l, M, A.x, A.a, l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr,
+                      l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // last: copy for phi_out
     }
     // phi_out (dcat.cpp:266) + module head (finetune.cpp:317-323)
     e = base_epi(m, EPI_BIAS);

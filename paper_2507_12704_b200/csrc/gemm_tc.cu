@@ -718,8 +718,14 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
 // TMEM accumulators (double-buffered), one group of 8 epilogue warps per buffer applies
 // bias + GELU and writes the chunk as the next MMA's K-major A operand, FFN2 accumulates all chunks into a
 // D-column TMEM accumulator; the residual / LayerNorm epilogue then runs on it.
-template <int D, int CL>
+// TAIL: the layer tail (layer_forward model.cpp:378-397, cross_tail dcat.cpp:80-86) in the same
+// kernel: acc2 <- x rows (tcgen05.cp), acc2 += A_o . Wo^T (the attention output projection),
+// then x_mid = acc2 + bo stays in acc2 as the FFN residual and LN2(x_mid) is written by the
+// epilogue warps straight into the A tile as the FFN1 operand. x_mid and LN2(x_mid) never
+// reach HBM: 384 KB less traffic per 128-row tile than the o-projection GEMM + FFN pair.
+template <int D, int CL, bool TAIL = false>
 struct FfnCfg {
+    static_assert(!TAIL || (CL == 1 && D >= 128), "fused layer tail: single CTA, D = 128 or 256");
     static constexpr int CH = 128;                        // hidden columns per chunk
     static constexpr int KB1 = D / 64;                    // k-blocks of the A tile
     // Weight blocks this CTA loads: CL = 1 the whole block, CL = 2 its half of the N rows
@@ -750,7 +756,8 @@ struct FfnCfg {
     static constexpr int CGF = D >= 128 ? 4 : 2;  // final-epilogue warps per quadrant
     static constexpr int FCOLS = D / CGF;         // final-epilogue columns per warp
     static constexpr int STG = 4096;              // final-epilogue staging per warp (in the H buffers)
-    static constexpr int PARAM_FLOATS = 1024 + 3 * 256 + 32;  // b1 (d_ff <= 1024) | b2 | ln_g | ln_b
+    // b1 (d_ff <= 1024) | b2 | ln_g | ln_b [| bo | ln2_g | ln2_b]
+    static constexpr int PARAM_FLOATS = 1024 + (TAIL ? 6 : 3) * 256 + 32;
     static constexpr int RED = 4 * 3 * CGF * 32 * 4;
     static constexpr int SMEM = A_TILE + 2 * H_BUF + STAGES * SLOT + PARAM_FLOATS * 4 + RED + 1024 + 512;
     static_assert(EPI_WARPS * STG <= 2 * H_BUF, "final-epilogue staging lives in the H buffers");
@@ -792,12 +799,12 @@ __device__ unsigned int g_ffn_trace_n[FFN_TR_ROLES];
 // weight bytes per row. Every barrier the MMA issuer waits on lives in the leader
 // (peer producers / epilogue warps arrive remotely); MMA completions are multicast to
 // the same barrier in both CTAs.
-template <int D, int CL>
-__global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
+template <int D, int CL, bool TAIL>
+__global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
     k_ffn_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmW1,
-             const __grid_constant__ CUtensorMap tmW2, int M, int F, const __grid_constant__ Epi e,
-             const __grid_constant__ EpiMaps mp) {
-    using C = FfnCfg<D, CL>;
+             const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmWo, int M, int F,
+             const __grid_constant__ Epi e, const __grid_constant__ EpiMaps mp) {
+    using C = FfnCfg<D, CL, TAIL>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -817,7 +824,9 @@ __global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
     uint64_t* acc2_full = h_empty + 2;
     uint64_t* acc2_empty = acc2_full + 1;
     uint64_t* rbar = acc2_empty + 1;  // residual block loads, one per epilogue warp
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(rbar + C::EPI_WARPS);
+    uint64_t* o_full = rbar + C::EPI_WARPS;  // TAIL: residual + A_o . Wo^T complete in acc2
+    uint64_t* a2_full = o_full + 1;          // TAIL: LN2 rows in the A tile, x_mid in acc2
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(a2_full + 1);
 
 #if DCAT_FFN_TRACE
     __shared__ unsigned s_tr_n[4];
@@ -829,6 +838,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
     const int unit0 = blockIdx.x / CL, ustride = gridDim.x / CL;
     const int nch = F / C::CH;
     const int P_B2 = 1024, P_G = 1024 + 256, P_BB = 1024 + 512;
+    const int P_BO = 1024 + 768, P_G2 = 1024 + 1024, P_BB2 = 1024 + 1280;  // TAIL
     // MMA issue order F1_0 .. F1_{LA-1}, then F1_j, F2_{j-LA}: FFN1 runs LA chunks ahead, so a
     // chunk's GELU overlaps ~2 LA chunk-MMAs and F1_j only needs GELU_{j-2}'s TMEM read.
     constexpr int LA = 2;
@@ -872,6 +882,8 @@ __global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
         }
         ptx::mbar_init(acc2_full, 1);
         ptx::mbar_init(acc2_empty, CL * 4 * C::CGF);
+        ptx::mbar_init(o_full, 1);
+        ptx::mbar_init(a2_full, 4 * C::CGF);
         for (int w = 0; w < C::EPI_WARPS; w++) ptx::mbar_init(&rbar[w], 1);
         ptx::fence_barrier_init();
     }
@@ -886,6 +898,11 @@ __global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
             sts1(s_par + 4u * (P_B2 + i), i < D ? e.b2[i] : 0.f);
             sts1(s_par + 4u * (P_G + i), (e.ln_g && i < D) ? e.ln_g[i] : 0.f);
             sts1(s_par + 4u * (P_BB + i), (e.ln_b && i < D) ? e.ln_b[i] : 0.f);
+            if constexpr (TAIL) {
+                sts1(s_par + 4u * (P_BO + i), i < D ? e.o_bias[i] : 0.f);
+                sts1(s_par + 4u * (P_G2 + i), i < D ? e.ln2_g[i] : 0.f);
+                sts1(s_par + 4u * (P_BB2 + i), i < D ? e.ln2_b[i] : 0.f);
+            }
         }
     }
     ptx::tc_fence_before();
@@ -933,15 +950,14 @@ __global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
                     ptx::mbar_expect_tx(a_full, C::A_TILE);
                     for (int kb = 0; kb < C::KB1; kb++) ptx::tma_load_2d(sA + kb * 16384, &tmA, a_full, kb * 64, t * 128);
                 }
-                // the next tile's A rows and residual rows stream into L2 while this tile's MMAs
-                // run, so its A load and residual slots are L2 hits
-                if (u + ustride < units) {
-                    const int tn = (u + ustride) * CL + static_cast<int>(rank);
-                    for (int kb = 0; kb < C::KB1; kb++) ptx::tma_prefetch_l2(&tmA, kb * 64, tn * 128);
-                    for (int cc = 0; cc < D; cc += 32) ptx::tma_prefetch_l2(&mp.resid, cc, tn * 128);
+                // No L2 prefetch of the next tile's rows: issued a tile (~36 us, ~230 MB of DRAM
+                // traffic) ahead, it is evicted from the 126 MB L2 before use (ncu: +190-250 MB of
+                // DRAM reads per context launch, and 368 vs 378 us in tools/kbench without it).
+                if constexpr (TAIL) {  // x rows (acc2's initial value), then Wo^T [NW2 x 64] blocks
+                    for (int cc = 0; cc < D; cc += 32) push(&mp.resid, cc, t * 128, 1, C::SLOT);
+                    for (int kb = 0; kb < C::KB1; kb++)
+                        for (int nh = 0; nh < D / C::NW2; nh++) push(&tmWo, kb * 64, nh * C::NW2, 1, C::SLOT);
                 }
-                if (i == 0)
-                    for (int cc = 0; cc < D; cc += 32) ptx::tma_prefetch_l2(&mp.resid, cc, t * 128);
                 for (int j = 0; j < nch + LA; j++) {  // same order as the MMA issuer
                     if (j < nch)
                         for (int p = 0; p < C::S1; p++)
@@ -949,7 +965,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
                                  C::W1_PER_SLOT, C::W1_BLK);
                     if (j >= LA) {
                         const int jj = j - LA;
-                        if (jj == 0)  // residual [128 x 32] fp32 blocks: the initial value of acc2
+                        if (!TAIL && jj == 0)  // residual [128 x 32] fp32 blocks: the initial value of acc2
                             for (int cc = 0; cc < D; cc += 32) push(&mp.resid, cc, t * 128, 1, C::SLOT);
                         if constexpr (CL == 1 && C::NW2 < D) {  // single CTA, D = 256: N halves per slot
                             for (int kb2 = 0; kb2 < 2; kb2++)
@@ -984,9 +1000,41 @@ __global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
                 ptx::tc_fence_after();
                 return static_cast<uint32_t>(s);
             };
+            // acc2 <- residual rows: [128 x 32] fp32 ring slots copied into TMEM (tcgen05.cp is ordered
+            // before the MMAs that accumulate onto it)
+            auto resid_to_acc2 = [&]() {
+                wait_lead(acc2_empty, (i & 1) ^ 1);
+                ptx::tc_fence_after();
+                for (int cc = 0; cc < D; cc += 32, it++) {
+                    const uint32_t s = next_slot();
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const uint64_t sd = ptx::sdesc_sw128(r_base + s * C::SLOT + k * 32);
+                        if constexpr (CL == 2) ptx::tmem_cp_128x256b_pair(T_ACC2 + cc + 8 * k, sd);
+                        else ptx::tmem_cp_128x256b(T_ACC2 + cc + 8 * k, sd);
+                    }
+                    commit(&empty[s]);
+                }
+            };
             for (int u = unit0; u < units; u += ustride, i++) {
                 wait_lead(a_full, i & 1);
                 ptx::tc_fence_after();
+                if constexpr (TAIL) {  // acc2 = x + A_o . Wo^T, then the epilogue's x_mid / LN2 hand-off
+                    resid_to_acc2();
+                    ptx::tc_fence_after();
+                    for (int kb = 0; kb < C::KB1; kb++)
+                        for (int nh = 0; nh < D / C::NW2; nh++, it++) {
+                            const uint32_t s = next_slot();
+#pragma unroll
+                            for (int k = 0; k < 4; k++)
+                                mma(T_ACC2 + nh * C::NW2, a_base + kb * 16384 + k * 32, r_base + s * C::SLOT + k * 32,
+                                    idesc2, 1u);
+                            commit(&empty[s]);
+                        }
+                    commit(o_full);
+                    ptx::mbar_wait(a2_full, i & 1);
+                    ptx::tc_fence_after();
+                }
                 for (int j = 0; j < nch + LA; j++) {
                     if (j < nch) {  // FFN1 chunk j -> acc1[b]
                         const int b = c1 & 1;
@@ -1013,20 +1061,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
                         const int hb = c2 & 1;
                         wait_lead(&h_full[hb], (c2 >> 1) & 1);
                         FFN_EV(2, jj);
-                        if (jj == 0) {  // acc2 <- residual rows (tcgen05.cp, ordered before the MMAs)
-                            wait_lead(acc2_empty, (i & 1) ^ 1);
-                            ptx::tc_fence_after();
-                            for (int cc = 0; cc < D; cc += 32, it++) {
-                                const uint32_t s = next_slot();
-#pragma unroll
-                                for (int k = 0; k < 4; k++) {
-                                    const uint64_t sd = ptx::sdesc_sw128(r_base + s * C::SLOT + k * 32);
-                                    if constexpr (CL == 2) ptx::tmem_cp_128x256b_pair(T_ACC2 + cc + 8 * k, sd);
-                                    else ptx::tmem_cp_128x256b(T_ACC2 + cc + 8 * k, sd);
-                                }
-                                commit(&empty[s]);
-                            }
-                        }
+                        if (!TAIL && jj == 0) resid_to_acc2();
                         ptx::tc_fence_after();
                         if constexpr (CL == 1 && C::NW2 < D) {
                             for (int kb2 = 0; kb2 < 2; kb2++)
@@ -1069,6 +1104,79 @@ __global__ void __launch_bounds__(FfnCfg<D, CL>::THREADS, 1)
         for (int u = unit0; u < units; u += ustride, i++) {
             const int t = u * CL + static_cast<int>(rank);
             const int m0 = t * 128, row_base = m0 + q * 32, row = row_base + lane;
+            if constexpr (TAIL) {
+                // ---- x_mid = acc2 + bo (acc2 = x + A_o . Wo^T) back into acc2 as the FFN residual;
+                // LN2(x_mid) (model.cpp:386) -> row r of the A tile, bf16, SW128 K-major
+                const bool live = row < M;
+                const uint32_t tacc = T_ACC2 + (static_cast<uint32_t>(q * 32) << 16) + c0;
+                const uint32_t a_row = ptx::smem_u32(sA) + r * 128;
+                float v[32];
+                float s1[1] = {0.f};
+                bool bad = false;
+                ptx::mbar_wait(o_full, i & 1);
+                ptx::tc_fence_after();
+#pragma unroll 1
+                for (int h = 0; h < C::FCOLS; h += 32) {
+                    tmem_load32(tacc + h, v);
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const float4 bb = lds4(s_par + 4u * (P_BO + c0 + h + 4 * j));
+                        float* w = v + 4 * j;
+                        w[0] += bb.x;
+                        w[1] += bb.y;
+                        w[2] += bb.z;
+                        w[3] += bb.w;
+                    }
+#pragma unroll
+                    for (int k = 0; k < 32; k++) {
+                        bad |= !isfinite(v[k]);
+                        s1[0] += v[k];
+                    }
+                    tmem_store32(tacc + h, v);
+                }
+                if (bad && live && e.layer_idx >= 0) atomicMax(&e.st->nonfinite_layer, e.layer_idx + 1);
+                quad_reduce<C::CGF, 1>(s_red, s1, cg, lane, q);
+                const float dn = static_cast<float>(D);
+                const float mu = s1[0] / dn;
+                float var[1] = {0.f};
+#pragma unroll 1
+                for (int h = 0; h < C::FCOLS; h += 32) {
+                    tmem_load32(tacc + h, v);
+#pragma unroll
+                    for (int k = 0; k < 32; k++) {
+                        const float d0 = v[k] - mu;
+                        var[0] += d0 * d0;
+                    }
+                }
+                quad_reduce<C::CGF, 1>(s_red, var, cg, lane, q);
+                const float rs = 1.0f / sqrtf(var[0] / dn + 1e-5f);
+#pragma unroll 1
+                for (int h = 0; h < C::FCOLS; h += 32) {
+                    tmem_load32(tacc + h, v);
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const float4 gg = lds4(s_par + 4u * (P_G2 + c0 + h + 4 * j));
+                        const float4 bb = lds4(s_par + 4u * (P_BB2 + c0 + h + 4 * j));
+                        float* w = v + 4 * j;
+                        w[0] = gg.x * ((w[0] - mu) * rs) + bb.x;
+                        w[1] = gg.y * ((w[1] - mu) * rs) + bb.y;
+                        w[2] = gg.z * ((w[2] - mu) * rs) + bb.z;
+                        w[3] = gg.w * ((w[3] - mu) * rs) + bb.w;
+                    }
+                    // columns col .. col + 31: k-block col / 64, 16-byte chunks (col % 64) / 8 + k
+                    const int col = c0 + h;
+                    const uint32_t rowa = a_row + (col >> 6) * 16384;
+#pragma unroll
+                    for (int k = 0; k < 4; k++)
+                        sts4u(rowa + (((((col & 63) >> 3) + k) ^ (r & 7)) << 4), pack_bf16(v[8 * k], v[8 * k + 1]),
+                              pack_bf16(v[8 * k + 2], v[8 * k + 3]), pack_bf16(v[8 * k + 4], v[8 * k + 5]),
+                              pack_bf16(v[8 * k + 6], v[8 * k + 7]));
+                }
+                fence_async_smem();  // the A tile is read by the FFN1 MMAs (async proxy)
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(a2_full);
+            }
             // ---- GELU chunks: group cg >> 1 takes the chunks in acc1 buffer cg >> 1; this warp
             // owns columns [64 (cg & 1), +64) of them = H k-block cg & 1, all eight 16-byte chunks
             const int grp = cg >> 1, sub = cg & 1;
@@ -1366,14 +1474,15 @@ void launch_mode(int BN, const CUtensorMap& ta, const CUtensorMap& tb, int M, in
 }  // namespace
 
 namespace {
-template <int D, int CL>
+template <int D, int CL, bool TAIL = false>
 void launch_ffn(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M, int F, const Epi& e,
-                const EpiMaps& mp, cudaStream_t s) {
-    using C = FfnCfg<D, CL>;
+                const EpiMaps& mp, cudaStream_t s, const bf16* Wot = nullptr) {
+    using C = FfnCfg<D, CL, TAIL>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
     static std::once_flag once;
     std::call_once(once, [] {
-        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_ffn_tc<D, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        DCAT_CUDA_CHECK(
+            cudaFuncSetAttribute(k_ffn_tc<D, CL, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     });
     const CUtensorMap ta = tmap_bf16(A, static_cast<uint64_t>(D), static_cast<uint64_t>(M),
                                      static_cast<uint64_t>(lda) * 2, 128);
@@ -1381,13 +1490,17 @@ void launch_ffn(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M,
                                      static_cast<uint64_t>(D) * 2, static_cast<uint32_t>(C::W1_ROWS));
     const CUtensorMap t2 = tmap_bf16(W2t, static_cast<uint64_t>(F), static_cast<uint64_t>(D),
                                      static_cast<uint64_t>(F) * 2, static_cast<uint32_t>(C::W2_ROWS));
+    // TAIL: Wo^T [D x D] (K-major) in [NW2 x 64] ring-slot blocks
+    const CUtensorMap to = TAIL ? tmap_bf16(Wot, static_cast<uint64_t>(D), static_cast<uint64_t>(D),
+                                            static_cast<uint64_t>(D) * 2, static_cast<uint32_t>(C::NW2))
+                                : t2;
     EpiMaps mpf = mp;  // residual in [128 x 32] fp32 blocks: one ring slot each, copied into acc2
     mpf.resid = tmap_epi(e.resid, true, static_cast<uint64_t>(D), static_cast<uint64_t>(M), e.ld_x, 128);
     const int units = ((M + 127) / 128 + CL - 1) / CL;
     const int per = num_sms() / CL;
     const int grid = CL * (units < per ? units : per);
     if constexpr (CL == 1) {
-        k_ffn_tc<D, 1><<<grid, C::THREADS, C::SMEM, s>>>(ta, t1, t2, M, F, e, mpf);
+        k_ffn_tc<D, 1, TAIL><<<grid, C::THREADS, C::SMEM, s>>>(ta, t1, t2, to, M, F, e, mpf);
         DCAT_LAUNCH_CHECK();
     } else {
         cudaLaunchConfig_t cfg = {};
@@ -1402,7 +1515,7 @@ void launch_ffn(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M,
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        DCAT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_ffn_tc<D, CL>, ta, t1, t2, M, F, e, mpf));
+        DCAT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k_ffn_tc<D, CL, TAIL>, ta, t1, t2, to, M, F, e, mpf));
     }
 }
 }  // namespace
@@ -1449,6 +1562,20 @@ void ffn_tc(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M, int
             else launch_ffn<256, 2>(A, lda, W1t, W2t, M, F, e, mp, s);
             break;
     }
+}
+
+bool layer_tail_tc_supported(int D, int F) { return (D == 128 || D == 256) && F % 128 == 0 && F <= 1024; }
+
+void layer_tail_tc(const bf16* A_o, int lda, const bf16* Wot, const bf16* W1t, const bf16* W2t, int M, int D, int F,
+                   const Epi& e, cudaStream_t s) {
+    if (M <= 0) return;
+    if (!layer_tail_tc_supported(D, F)) throw InvalidArg("layer_tail_tc: unsupported shape");
+    if (!e.o_bias || !e.ln2_g || !e.ln2_b) throw InvalidArg("layer_tail_tc: o_bias / ln2_g / ln2_b required");
+    Epi em = e;
+    em.mode = EPI_RESID_LN;
+    const EpiMaps mp = make_maps(em, M, D);
+    if (D == 128) launch_ffn<128, 1, true>(A_o, lda, W1t, W2t, M, F, e, mp, s, Wot);
+    else launch_ffn<256, 1, true>(A_o, lda, W1t, W2t, M, F, e, mp, s, Wot);
 }
 
 void gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K, const Epi& e, cudaStream_t s) {

@@ -149,6 +149,9 @@ struct Epi {
     float* logits;           // [M x 3]
     Status* st;
     int layer_idx;           // for non-finite reporting (-1: no check)
+    const float* o_bias;     // layer_tail_tc: attention output projection bias [d]
+    const float* ln2_g;      // layer_tail_tc: LN2 (pre-FFN) gain / bias [d]
+    const float* ln2_b;
 };
 
 // bf16 tensor-core GEMM (tcgen05 + TMEM + TMA): C[M x N] = A[M x K] . W^T,
@@ -158,6 +161,13 @@ void gemm_tc(const bf16* A, int lda, const bf16* W, int ldw, int M, int N, int K
 // (e.bias = b1 [F], e.b2 = b2 [D], resid / x_out / ld_x / ln_g / ln_b / ln_out / ln_ld as EPI_RESID_LN).
 // W1t = W1^T [F x D], W2t = W2^T [D x F] (bf16, K-major).
 bool ffn_tc_supported(int D, int F);
+// Fused layer tail (tcgen05, one kernel): x_mid = x + (A_o . Wot^T + o_bias); h = LN2(x_mid);
+// x_out = x_mid + gelu(h . W1t^T + bias) . W2t^T + b2; ln_out = LN(x_out) (next LN1) or a copy.
+// e as for ffn_tc (resid = x) plus o_bias / ln2_g / ln2_b; Wot = Wo^T [D x D] (K-major).
+// x_mid and h stay on the SM.
+bool layer_tail_tc_supported(int D, int F);
+void layer_tail_tc(const bf16* A_o, int lda, const bf16* Wot, const bf16* W1t, const bf16* W2t, int M, int D, int F,
+                   const Epi& e, cudaStream_t s);
 void ffn_tc(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M, int D, int F, const Epi& e,
             cudaStream_t s);
 // fp32 parity path: SIMT GEMM (W in reference in x out layout, ldw) + row epilogue.

@@ -165,6 +165,27 @@ def test_bf16_pinfm_base_sample_vs_oracle(api, orc):
     assert rel_err(lf, rl) <= 1e-4
 
 
+@pytest.mark.parametrize("d", [128, 256])
+def test_fused_layer_tail(api, orc, d, monkeypatch):
+    """The fused layer tail (o-projection + residual + LN2 + FFN + residual + next LN1 in one
+    tcgen05 kernel, layer_tail_tc) against the oracle and against the two-kernel path
+    (o-projection GEMM, then the fused FFN) on ragged users, for both d the kernel supports."""
+    spec = ModelSpec(d_model=d, n_layers=2, n_heads=d // 32, mlp_ratio=4, max_len=130, d_emb=d)
+    w = orc.init_weights(spec, 42, table=(8, 4096, d // 8, 7, 0.05), head_seed=11)
+    b = make_batch(5, 7, 128, seed=12, ragged=True, layout="grouped")
+    ft = FinetuneSpec(max_events=128)
+    m = api.DcatModel(w)
+    lf, mf, hf = m.rank_forward_batch(b, ft, want_h=True)
+    monkeypatch.setenv("DCAT_NO_TAIL_FUSION", "1")
+    l2, m2, h2 = m.rank_forward_batch(b, ft, want_h=True)
+    rl, rm, _, rh = orc.rank_forward_batch(w, ft, b)
+    for h, lg, mg in ((hf, lf, mf), (h2, l2, m2)):
+        assert float(np.abs(h - rh).max()) <= 3e-2 and cos_min(h, rh) >= 0.999
+        assert rel_err(lg, rl) <= 3e-2 and rel_err(mg, rm) <= 3e-2
+    # the two bf16 paths differ only in rounding order (residual added in TMEM before the bias)
+    assert float(np.abs(hf - h2).max()) <= 2e-2 and cos_min(hf, h2) >= 0.9995
+
+
 @pytest.mark.parametrize("impl", ["pipe", "tcgen05", "flash"])
 def test_bf16_attention_impls_and_kv_cache(api, orc, impl, monkeypatch):
     """Every bf16 attention kernel (the mma.sync flash default with the row-major cache, the
