@@ -20,7 +20,9 @@ import numpy as np
 from .abi import (Batch, BatchC, CallStatsC, FLAG_INPUT_DEVICE, FLAG_PRECISION_FP32, FLAG_PROFILE,
                   FinetuneConfigC, FinetuneSpec, HeadC, ModelConfigC, ParamsC, TableC, Weights)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libdcat_b200.so")
+# DCAT_LIB_PATH: an alternative build of the same library (kernel variant experiments, tools/)
+LIB_PATH = os.environ.get("DCAT_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                           "libdcat_b200.so")
 
 _lib = None
 

@@ -15,6 +15,9 @@
 //           relays each completed slot to a second leader barrier (relaxed remote arrive); the
 //           leader consumes when both are complete and frees the slot in both CTAs (relaxed)
 //   mode 9: as mode 0 with C > 1 (multicast) but relaxed cross-CTA slot release
+//   mode 10: CTA pairs, .cta_group::2 TMA of both CTAs onto the leader's barrier, ONLY the leader
+//           arrives (expect_tx of both boxes, local); the peer issues its copy with no arrival
+//           (the CUTLASS 2-SM pattern); the leader frees the slot in both CTAs (relaxed)
 //   C > 1: clusters of C CTAs; each CTA loads 1/C of every box multicast to the whole cluster
 // Prints per-CTA bytes/clk landed in shared memory and the mean TMA issue -> full latency.
 #include <cuda.h>
@@ -39,7 +42,7 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; s++) {
             ptx::mbar_init(&full[s], mode == 4 || mode == 6 || (mode == 5 && rank == 0) ? 2 : 1);
-            ptx::mbar_init(&empty[s], mode >= 4 && mode <= 8 ? 1 : C);
+            ptx::mbar_init(&empty[s], (mode >= 4 && mode <= 8) || mode == 10 ? 1 : C);
             ptx::mbar_init(&fwd[s], 1);
         }
         ptx::fence_barrier_init();
@@ -79,11 +82,11 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
                 ptx::mbar_arrive_cl(ptx::mapa(ptx::smem_u32(&full[s]), 0));
             }
             ptx::mbar_wait_cl(&empty[s], ((it - S) / S) & 1);
-        } else if (C == 2 && (mode == 4 || mode == 6) && it >= S) {  // pair: the leader consumes both halves and frees the slot in both CTAs
+        } else if (C == 2 && (mode == 4 || mode == 6 || mode == 10) && it >= S) {  // pair: the leader consumes both halves and frees the slot in both CTAs
             if (rank == 0) {
                 ptx::mbar_wait(&full[s], ((it - S) / S) & 1);
                 lat += clock64() - t_issue[s];
-                if (mode == 6) {
+                if (mode == 6 || mode == 10) {
                     ptx::mbar_arrive_cl_relaxed(ptx::mapa(ptx::smem_u32(&empty[s]), 0));
                     ptx::mbar_arrive_cl_relaxed(ptx::mapa(ptx::smem_u32(&empty[s]), 1));
                 } else {
@@ -105,9 +108,16 @@ __global__ void __launch_bounds__(64, 1) k_stream(const __grid_constant__ CUtens
         }
         if (it < iters) {
             // pair modes: the peer streams the other half of the region, as the pair FFN's halves
-            const int half = (mode >= 4 && mode <= 8 && rank == 1) ? blocks_per_region / 2 : 0;
+            const int half = (((mode >= 4 && mode <= 8) || mode == 10) && rank == 1) ? blocks_per_region / 2 : 0;
             const int blk = (start + it + half) % blocks_per_region;
             const int row0 = (region * blocks_per_region + blk) * BOX_ROWS;
+            if (C == 2 && mode == 10) {
+                const uint32_t lead_full = ptx::mapa(ptx::smem_u32(&full[s]), 0);
+                if (rank == 0) ptx::mbar_expect_tx(&full[s], 2 * BOX_BYTES);
+                t_issue[s] = clock64();
+                ptx::tma_load_2d_pair(ptx::smem_u32(ring + s * BOX_BYTES), &map, lead_full, 0, row0);
+                continue;
+            }
             if (C == 2 && (mode == 4 || mode == 6)) {
                 const uint32_t lead_full = ptx::mapa(ptx::smem_u32(&full[s]), 0);
                 if (mode == 6) ptx::mbar_expect_tx_cl_relaxed(lead_full, BOX_BYTES);
@@ -151,7 +161,7 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out,
     CUtensorMap m;
     cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(regions) * blocks_per_region * BOX_ROWS};
     cuuint64_t strides[1] = {128};
-    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(mode >= 4 && mode <= 8 ? BOX_ROWS : BOX_ROWS / C)};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>((mode >= 4 && mode <= 8) || mode == 10 ? BOX_ROWS : BOX_ROWS / C)};
     cuuint32_t es[2] = {1, 1};
     enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -176,7 +186,7 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out,
     double cyc = 0, lat = 0;
     int nm = 0;
     for (int i = 0; i < grid; i++) {
-        if (mode >= 4 && mode <= 8 && mode != 7 && (i & 1)) continue;  // latency is measured by the leader
+        if (((mode >= 4 && mode <= 8 && mode != 7) || mode == 10) && (i & 1)) continue;  // latency is measured by the leader
         cyc += h[2 * i];
         lat += h[2 * i + 1];
         nm++;
@@ -202,9 +212,10 @@ int main() {
     cudaMalloc(&d_out, 296 * sizeof(unsigned long long));
     run<4, 1>(enc, buf, 0, 148, d_out);
     run<6, 1>(enc, buf, 0, 148, d_out);
-    run<6, 2>(enc, buf, 9, 148, d_out);
-    run<10, 2>(enc, buf, 9, 148, d_out);
-    run<6, 4>(enc, buf, 9, 148, d_out);
-    run<10, 4>(enc, buf, 9, 148, d_out);
+    run<6, 2>(enc, buf, 6, 148, d_out);
+    run<4, 2>(enc, buf, 10, 148, d_out);
+    run<6, 2>(enc, buf, 10, 148, d_out);
+    run<10, 2>(enc, buf, 10, 148, d_out);
+    run<6, 2>(enc, buf, 7, 148, d_out);
     return 0;
 }
