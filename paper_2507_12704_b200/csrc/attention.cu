@@ -92,6 +92,9 @@ struct FlashCfg {
 #ifndef DCAT_XRT
 #define DCAT_XRT 2
 #endif
+#ifndef DCAT_FLASH_ABLATE  // kernel experiments only (tools/build_variant.sh): 1 no exp, 2 no PV, 4 no QK, 8 no K/V loads
+#define DCAT_FLASH_ABLATE 0
+#endif
 #ifndef DCAT_CRT
 #define DCAT_CRT 2
 #endif
@@ -141,6 +144,7 @@ __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS
             bool ok = key < tile.nkv;
             size_t off = static_cast<size_t>(tile.kv0 + (ok ? key : 0)) * p.ldkv + hc + c * 8;
             uint32_t so = 2 * (buf * C::KV_ELEMS + r * LD + c * 8);
+            if (DCAT_FLASH_ABLATE & 8) continue;
             cp_async16(sK0 + so, K + off, ok);
             cp_async16(sV0 + so, V + off, ok);
         }
@@ -260,6 +264,7 @@ __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS
                     int key = 8 * (j + (lane >> 4)) + (lane & 7);
                     int col = kk * 16 + 8 * ((lane >> 3) & 1);
                     ldsm_x4(b, kb + 2 * (key * LD + col));
+                    if (DCAT_FLASH_ABLATE & 4) { s[0][j][0] += __uint_as_float(b[0]); continue; }
 #pragma unroll
                     for (int t = 0; t < RT; t++) {
                         mma16816(s[t][j], qf[t][kk], b[0], b[1]);
@@ -325,8 +330,14 @@ __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS
                 const float u1 = m1 == -INFINITY ? 0.f : -m1 * sl2;
 #pragma unroll
                 for (int j = 0; j < NJ; j++) {
-                    float p0 = ex2(fmaf(s[t][j][0], sl2, u0)), p1 = ex2(fmaf(s[t][j][1], sl2, u0));
-                    float p2 = ex2(fmaf(s[t][j][2], sl2, u1)), p3 = ex2(fmaf(s[t][j][3], sl2, u1));
+                    float p0, p1, p2, p3;
+                    if (DCAT_FLASH_ABLATE & 1) {
+                        p0 = fmaf(s[t][j][0], sl2, u0), p1 = fmaf(s[t][j][1], sl2, u0);
+                        p2 = fmaf(s[t][j][2], sl2, u1), p3 = fmaf(s[t][j][3], sl2, u1);
+                    } else {
+                        p0 = ex2(fmaf(s[t][j][0], sl2, u0)), p1 = ex2(fmaf(s[t][j][1], sl2, u0));
+                        p2 = ex2(fmaf(s[t][j][2], sl2, u1)), p3 = ex2(fmaf(s[t][j][3], sl2, u1));
+                    }
                     pf[t][j >> 1][(j & 1) * 2 + 0] = pack_bf16(p0, p1);
                     pf[t][j >> 1][(j & 1) * 2 + 1] = pack_bf16(p2, p3);
                 }
@@ -340,6 +351,7 @@ __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS
                 for (int j = 0; j < NT; j += 2) {
                     uint32_t b[4];
                     ldsm_x4_t(b, vb + 2 * (key * LD + 8 * (j + (lane >> 4))));
+                    if (DCAT_FLASH_ABLATE & 2) { o[0][j][0] += __uint_as_float(b[0] ^ pf[0][kk][0]); continue; }
 #pragma unroll
                     for (int t = 0; t < RT; t++) {
                         mma16816(o[t][j], pf[t][kk], b[0], b[1]);
@@ -362,10 +374,10 @@ __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS
             int c = hc + j * 8 + 2 * t4;
             if (r0 < tile.nq)
                 *reinterpret_cast<uint32_t*>(O + static_cast<size_t>(tile.q0 + r0) * p.ldo + c) =
-                    pack_bf16(o[t][j][0] * i0, o[t][j][1] * i0);
+                    DCAT_FLASH_ABLATE ? 0u : pack_bf16(o[t][j][0] * i0, o[t][j][1] * i0);
             if (r1 < tile.nq)
                 *reinterpret_cast<uint32_t*>(O + static_cast<size_t>(tile.q0 + r1) * p.ldo + c) =
-                    pack_bf16(o[t][j][2] * i1, o[t][j][3] * i1);
+                    DCAT_FLASH_ABLATE ? 0u : pack_bf16(o[t][j][2] * i1, o[t][j][3] * i1);
         }
     }
 }

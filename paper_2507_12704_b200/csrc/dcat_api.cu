@@ -280,7 +280,7 @@ DedupOut dedup_buffers(dcat_model* m, int64_t B) {
     o.list = m->b_dd[6].get<int32_t>(B);
     o.list_n = m->b_dd[7].get<int32_t>(1);
     o.scan_tmp = m->b_dd[8].get<int64_t>(n1);
-    o.scan_blk = m->b_dd[9].get<int64_t>(4097);
+    o.scan_blk = m->b_dd[9].get<int64_t>(4 * 4097);  // four arrays' block sums
     o.uid = m->b_dd[10].get<int64_t>(n1);
     o.rep = m->b_dd[11].get<int32_t>(B);
     o.first = m->b_dd[12].get<int32_t>(B);
@@ -323,12 +323,12 @@ void run_dedup(dcat_model* m, const Staged& sb, const DedupOut& o, cudaStream_t 
     uint64_t mask = debug_hash_mask();
     const int kTileCtx = m->tile_ctx, kTileCross = m->tile_cross;
     dedup_plan(sb.in, o, mask, kTileCtx, kTileCross, s);
-    m->stats.kernel_launches += 27;
+    m->stats.kernel_launches += 18;
     DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
     DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
     if (m->st_host->collisions > 0 && m->st_host->err_bits == 0) {
         dedup_repair(sb.in, o, m->st_host->collisions, kTileCtx, kTileCross, mask, s);
-        m->stats.kernel_launches += 5 * 5 + 20;
+        m->stats.kernel_launches += 5 * 5 + 11;
         DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
         DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
     }

@@ -311,7 +311,16 @@ __device__ int64_t block_exclusive_scan(int64_t v, int64_t* total) {
     return base + x - v;
 }
 
-__global__ void k_scan_sums(const int64_t* in, int64_t n, int64_t* blk) {
+// Up to 4 independent exclusive scans of n items in one launch sequence: blockIdx.y picks the
+// array, each with its own block-sum row in blk (stride kScanTile + 1).
+struct ScanSet {
+    const int64_t* in[4];
+    int64_t* out[4];
+};
+
+__global__ void k_scan_sums(ScanSet x, int64_t n, int64_t* blk) {
+    const int64_t* in = x.in[blockIdx.y];
+    blk += blockIdx.y * (kScanTile + 1);
     int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
     int64_t s = 0;
 #pragma unroll
@@ -323,7 +332,8 @@ __global__ void k_scan_sums(const int64_t* in, int64_t n, int64_t* blk) {
 }
 
 __global__ void k_scan_top(int64_t* blk, int64_t nb) {
-    // single block; nb <= kScanTile
+    // one block per array; nb <= kScanTile
+    blk += blockIdx.x * (kScanTile + 1);
     int64_t v[kScanItems];
     int64_t s = 0;
 #pragma unroll
@@ -343,7 +353,10 @@ __global__ void k_scan_top(int64_t* blk, int64_t nb) {
     if (threadIdx.x == 0) blk[nb] = tot;
 }
 
-__global__ void k_scan_apply(const int64_t* in, int64_t n, const int64_t* blk, int64_t nb, int64_t* out) {
+__global__ void k_scan_apply(ScanSet x, int64_t n, const int64_t* blk, int64_t nb) {
+    const int64_t* in = x.in[blockIdx.y];
+    int64_t* out = x.out[blockIdx.y];
+    blk += blockIdx.y * (kScanTile + 1);
     int64_t base = static_cast<int64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
     int64_t v[kScanItems];
     int64_t s = 0;
@@ -412,14 +425,24 @@ inline unsigned warp_grid(int64_t rows) {
 
 }  // namespace
 
-void scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* blk, cudaStream_t s) {
+// exclusive scans (out[n] = total) of `count` arrays of n items; in place when in == out (each
+// thread of k_scan_apply reads only the items it writes). blk: count * (kScanTile + 1) items.
+static void scan_multi(const ScanSet& x, int count, int64_t n, int64_t* blk, cudaStream_t s) {
     int64_t nb = (n + kScanTile - 1) / kScanTile;
     if (nb == 0) nb = 1;
     if (nb > kScanTile) throw InvalidArg("scan: batch too large (max 16M rows)");
-    k_scan_sums<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, blk);
-    k_scan_top<<<1, kScanThreads, 0, s>>>(blk, nb);
-    k_scan_apply<<<static_cast<unsigned>(nb), kScanThreads, 0, s>>>(in, n, blk, nb, out);
+    const dim3 grid(static_cast<unsigned>(nb), static_cast<unsigned>(count));
+    k_scan_sums<<<grid, kScanThreads, 0, s>>>(x, n, blk);
+    k_scan_top<<<count, kScanThreads, 0, s>>>(blk, nb);
+    k_scan_apply<<<grid, kScanThreads, 0, s>>>(x, n, blk, nb);
     DCAT_LAUNCH_CHECK();
+}
+
+void scan_i64(const int64_t* in, int64_t* out, int64_t n, int64_t* blk, cudaStream_t s) {
+    ScanSet x{};
+    x.in[0] = in;
+    x.out[0] = out;
+    scan_multi(x, 1, n, blk, s);
 }
 
 // uid / rep / groups / offsets from head[]. Scans run in place (each thread
@@ -433,10 +456,8 @@ static void finish_plan(const DedupIn& in, const DedupOut& o, int tile_ctx, int 
     k_rep<<<grid_for(B, 256), 256, 0, s>>>(B, o.head, o.uid, o.rep, o.first, o.cnt, o.st);
     k_unique_sizes<<<grid_for(B, 256), 256, 0, s>>>(B, in, o.first, o.cnt, o.st, tile_ctx, tile_cross, o.goff,
                                                     o.tok_off, o.ctx_toff, o.cross_toff);
-    scan_i64(o.goff, o.goff, B, o.scan_blk, s);
-    scan_i64(o.tok_off, o.tok_off, B, o.scan_blk, s);
-    scan_i64(o.ctx_toff, o.ctx_toff, B, o.scan_blk, s);
-    scan_i64(o.cross_toff, o.cross_toff, B, o.scan_blk, s);
+    ScanSet x{{o.goff, o.tok_off, o.ctx_toff, o.cross_toff}, {o.goff, o.tok_off, o.ctx_toff, o.cross_toff}};
+    scan_multi(x, 4, B, o.scan_blk, s);  // the four per-unique offset arrays, one launch sequence
     k_totals<<<1, 1, 0, s>>>(B, o.tok_off, o.ctx_toff, o.cross_toff, o.cnt, o.st);
     k_perm<<<grid_for(B, 256), 256, 0, s>>>(B, o.rep, o.goff, o.cursor, o.perm);
     DCAT_LAUNCH_CHECK();
