@@ -104,6 +104,7 @@ struct dcat_model {
     uint64_t* seed_mix = nullptr;
     int J = 0, R = 0, d_sub = 0;
     float *action_emb = nullptr, *surface_emb = nullptr, *pos_emb = nullptr;
+    float* cmb = nullptr;  // (action + surface) + pos rows for the bf16 context gather, or null
     Lin phi_in1, phi_in2, phi_out1, phi_out2;
     std::vector<LayerW> layers;
     // ranking head
@@ -540,7 +541,8 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     m->last_Tp = Tp;
 
     EmbParams ep{m->table, m->qtable,     m->qbits,       m->qrow_bytes, m->qcode_bytes, m->seed_mix, m->J,
-                 m->R,     m->d_sub,      m->action_emb,  m->surface_emb, m->pos_emb,    de,          m->lt};
+                 m->R,     m->d_sub,      m->action_emb,  m->surface_emb, m->pos_emb,    de,          m->lt,
+                 f32 ? nullptr : m->cmb, m->cfg.n_surfaces, m->cfg.max_len};
     const float scale = 1.0f / std::sqrt(static_cast<float>(dh));
     auto K_l = [&](int l) { return A.kv + static_cast<size_t>(2 * l) * Tp * d; };
     auto V_l = [&](int l) { return A.kv + static_cast<size_t>(2 * l + 1) * Tp * d; };
@@ -748,7 +750,7 @@ void run_head_only(dcat_model* m, const Staged& sb, const DedupOut& o, const dca
     float* tmp = f32 ? m->b_act[13].get<float>(Bp * m->hidden) : nullptr;
     EmbParams ep{m->table, m->qtable, m->qbits, m->qrow_bytes, m->qcode_bytes, m->seed_mix, m->J, m->R, m->d_sub,
                  m->action_emb, m->surface_emb, m->pos_emb,
-                 m->cfg.d_emb, m->lt};
+                 m->cfg.d_emb, m->lt, nullptr, m->cfg.n_surfaces, m->cfg.max_len};
     CandParams cp{sb.candidate, sb.age, nullptr, m->aux_proj, 0, 0, ft.max_events, ft.fresh_days, ft.mid_days,
                   0, kh, 0};
     gather_candidates<T>(sb.in, o, ep, cp, B, E, m->cfg.d_emb, feat, s);
@@ -857,6 +859,14 @@ int dcat_model_create(const dcat_model_config* cfg, const dcat_params* params, c
         m->action_emb = m->mem.upload(t[k++], static_cast<size_t>(c.n_actions) * c.d_emb);
         m->surface_emb = m->mem.upload(t[k++], static_cast<size_t>(c.n_surfaces) * c.d_emb);
         m->pos_emb = c.pos_learned ? m->mem.upload(t[k++], static_cast<size_t>(c.max_len) * c.d_emb) : nullptr;
+        const size_t n_cmb = static_cast<size_t>(c.n_actions) * c.n_surfaces * c.max_len * c.d_emb;
+        if (m->pos_emb && c.d_emb % 4 == 0 && n_cmb * 4 <= (64u << 20)) {  // <= 64 MB (7.4 MB at PinFM-base)
+            DCAT_CUDA_CHECK(cudaMalloc(&m->cmb, n_cmb * 4));
+            m->mem.ptrs.push_back(m->cmb);
+            build_combined_emb(m->action_emb, m->surface_emb, m->pos_emb, c.n_actions, c.n_surfaces, c.max_len,
+                               c.d_emb, m->cmb, nullptr);
+            DCAT_CUDA_CHECK(cudaDeviceSynchronize());
+        }
         int d = c.d_model, F = d * c.mlp_ratio;
         m->phi_in1 = make_lin(m->mem, t[k], t[k + 1], c.d_emb, d);
         m->phi_in2 = make_lin(m->mem, t[k + 2], t[k + 3], d, d);

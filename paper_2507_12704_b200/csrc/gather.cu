@@ -11,8 +11,14 @@
 // (crossing_forward finetune.cpp:303-308, ctx_features :212-226).
 // One warp per row, 128-bit loads of the fp32 table rows (4 MB at PinFM-base,
 // L2-resident), additions in the reference's order, output bf16 (or fp32 in
-// the parity path).
+// the parity path). The bf16 context gather reads one precombined
+// (action + surface) + pos row (EmbParams::cmb, 7.4 MB at PinFM-base) instead of
+// three: the sum is associated differently from the reference's
+// ((lookup + action) + surface) + pos, a last-bit fp32 difference before the
+// bf16 rounding; the fp32 parity path keeps the reference's order.
 #include <cuda_fp16.h>
+
+#include <type_traits>
 
 #include "launch.h"
 
@@ -121,6 +127,18 @@ __device__ __forceinline__ void gather_ctx_token_vec(const EmbParams& ep, const 
         return;
     }
     const uint32_t rows = warp_rows(ep, item, lane);
+    if (ep.cmb != nullptr) {  // bf16 path: lookup + ((action + surface) + pos), one row read instead of three
+        const float* ce = ep.cmb + (static_cast<size_t>(a * ep.n_surf + s) * ep.max_len + i) * ep.d_emb;
+#pragma unroll
+        for (int k = 0; k < kMaxSteps; k++) {
+            if (128 * k >= ep.d_emb) break;
+            const int c = 128 * k + 4 * lane;
+            const uint32_t r = __shfl_sync(0xffffffffu, rows, L.j[k] & 31);
+            if (c < ep.d_emb)
+                store4<T>(out + c, add4(sub4(ep, L.j[k], r, L.cc[k]), __ldg(reinterpret_cast<const float4*>(ce + c))));
+        }
+        return;
+    }
     const float* ae = ep.action_emb + static_cast<size_t>(a) * ep.d_emb;
     const float* se = ep.surface_emb + static_cast<size_t>(s) * ep.d_emb;
 #pragma unroll
@@ -220,6 +238,59 @@ __global__ void __launch_bounds__(256, 4) k_gather_ctx(DedupIn in, const int32_t
     }
 }
 
+// bf16 context gather, 4 tokens per warp: lane group g (8 lanes) owns token tb + g. Each lane
+// resolves its group's token metadata (same addresses within a group: broadcast loads), lane
+// j < J of a group hashes sub-table row j once, and the group writes the row as 8 x 16-byte
+// chunks per 128 columns: lookup + cmb, cmb = (action + surface) + pos (EmbParams::cmb).
+// Needs J <= 8, d_sub % 4 == 0, d_emb % 32 == 0, the fp32 table and cmb.
+__global__ void __launch_bounds__(256) k_gather_ctx_g8(DedupIn in, const int32_t* __restrict__ first,
+                                                      const int64_t* __restrict__ tok_off, EmbParams ep,
+                                                      const int32_t* __restrict__ tok_unique, int64_t T_ctx,
+                                                      bf16* __restrict__ E, int ldE) {
+    const int lane = threadIdx.x & 31, grp = lane >> 3, l8 = lane & 7;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t tb = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * 4; tb < T_ctx;
+         tb += nw * 4) {
+        const int64_t t = tb + grp;
+        const bool live = t < T_ctx;
+        int i = 0, a = 0, sf = 0;
+        uint64_t item = 0;
+        if (live) {
+            const int u = tok_unique[t];
+            i = static_cast<int>(t - tok_off[u]);
+            const int fr = first[u], rv = in.row_valid[fr], kept = seq_kept(in, rv);
+            if (i < kept) {
+                const int64_t ev = in.row_offset[fr] + (rv - kept) + i;  // fixed window: newest events
+                item = in.item[ev];
+                a = in.action[ev];
+                sf = in.surface[ev];
+            } else {
+                a = -1;  // AuxLt's learnable token after the events (finetune.cpp:186-191)
+            }
+        }
+        const uint32_t row_j = (live && a >= 0 && l8 < ep.J) ? table_row(ep, item, l8) : 0u;
+        if (!live) continue;  // groups are independent from here (8-lane shuffles only)
+        bf16* out = E + t * ldE;
+        if (a < 0) {  // lt + pos_emb[i] (finetune.cpp:188-190)
+            for (int c = 4 * l8; c < ep.d_emb; c += 32) {
+                float4 v = __ldg(reinterpret_cast<const float4*>(ep.lt + c));
+                if (ep.pos_emb) v = add4(v, __ldg(reinterpret_cast<const float4*>(ep.pos_emb + static_cast<size_t>(i) * ep.d_emb + c)));
+                store4<bf16>(out + c, v);
+            }
+            continue;
+        }
+        const float* ce = ep.cmb + (static_cast<size_t>(a * ep.n_surf + sf) * ep.max_len + i) * ep.d_emb;
+        const unsigned gmask = 0xffu << (grp * 8);
+        for (int c = 4 * l8; c < ep.d_emb; c += 32) {
+            const int j = c / ep.d_sub;  // the 8 lanes share one sub-table row when d_sub >= 32
+            const uint32_t r = __shfl_sync(gmask, row_j, j, 8);
+            const float4 v = __ldg(reinterpret_cast<const float4*>(ep.table + (static_cast<size_t>(j) * ep.R + r) * ep.d_sub +
+                                                                   (c - j * ep.d_sub)));
+            store4<bf16>(out + c, add4(v, __ldg(reinterpret_cast<const float4*>(ce + c))));
+        }
+    }
+}
+
 // ctx_features (finetune.cpp:212-226)
 __device__ float ctx_feature(int k, double age, int valid, int last_surface, int max_events, double fresh,
                              double mid) {
@@ -234,13 +305,45 @@ __device__ float ctx_feature(int k, double age, int valid, int last_surface, int
     return (valid > 0 && k - 4 == last_surface) ? 1.0f : 0.0f;
 }
 
+// per-row metadata of a candidate, resolved by one lane (8 rows per warp step in parallel)
+struct CandMeta {
+    int i, n, valid, last_s;
+    uint64_t item;
+    double age;
+};
+__device__ __forceinline__ CandMeta cand_meta(const DedupIn& in, const int32_t* __restrict__ perm,
+                                              const int32_t* __restrict__ rep, const int32_t* __restrict__ first,
+                                              const CandParams& cp, bool want_feat, int64_t p) {
+    CandMeta m;
+    m.i = perm[p];
+    m.n = seq_tokens(in, in.row_valid[first[rep[m.i]]]);  // candidate position (after the context / lt token)
+    m.item = cp.candidate[m.i];
+    m.valid = 0;
+    m.last_s = -1;
+    m.age = 0.0;
+    if (want_feat) {
+        m.age = cp.age[m.i];
+        m.valid = in.row_valid[m.i];
+        m.last_s = m.valid > 0 ? in.surface[in.row_offset[m.i] + m.valid - 1] : -1;
+    }
+    return m;
+}
+__device__ __forceinline__ CandMeta shfl_meta(const CandMeta& m, int k) {
+    CandMeta r;
+    r.i = __shfl_sync(0xffffffffu, m.i, k);
+    r.n = __shfl_sync(0xffffffffu, m.n, k);
+    r.valid = __shfl_sync(0xffffffffu, m.valid, k);
+    r.last_s = __shfl_sync(0xffffffffu, m.last_s, k);
+    r.item = __shfl_sync(0xffffffffu, m.item, k);
+    r.age = __shfl_sync(0xffffffffu, m.age, k);
+    return r;
+}
+
 template <typename T>
-__device__ void gather_cand_row(DedupIn in, const int32_t* __restrict__ perm, const int32_t* __restrict__ rep,
-                                const int32_t* __restrict__ first, const EmbParams& ep, const CandParams& cp,
-                                int64_t p, T* __restrict__ E, int ldE, T* __restrict__ feat, Status* st, int lane) {
-    int i = perm[p];
-    int n = seq_tokens(in, in.row_valid[first[rep[i]]]);  // candidate position (after the context / lt token)
-    uint64_t item = cp.candidate[i];
+__device__ void gather_cand_row(const EmbParams& ep, const CandParams& cp, const CandMeta& m, int64_t p,
+                                T* __restrict__ E, int ldE, T* __restrict__ feat, Status* st, int lane) {
+    const int i = m.i, n = m.n;
+    const uint64_t item = m.item;
     const uint32_t rows = warp_rows(ep, item, lane);
     const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(n) * ep.d_emb : nullptr;
     const float* aux = cp.variant_aux ? cp.aux + static_cast<size_t>(i) * cp.d_aux : nullptr;
@@ -284,13 +387,12 @@ __device__ void gather_cand_row(DedupIn in, const int32_t* __restrict__ perm, co
         }
     }
     if (fo) {
-        double age = cp.age[i];
+        const double age = m.age;
         if (lane == 0 && age < 0.0) {
             atomicOr(&st->err_bits, ERR_AGE);
             atomicMin(&st->err_row, i);
         }
-        int valid = in.row_valid[i];
-        int last_s = valid > 0 ? in.surface[in.row_offset[i] + valid - 1] : -1;
+        const int valid = m.valid, last_s = m.last_s;
         int c0 = cp.d_model + ep.d_emb;
         for (int c = c0 + lane; c < cp.feat_ld; c += 32) {
             int k = c - c0;
@@ -304,10 +406,17 @@ template <typename T>
 __global__ void k_gather_cand(DedupIn in, const int32_t* __restrict__ perm, const int32_t* __restrict__ rep,
                               const int32_t* __restrict__ first, EmbParams ep, CandParams cp, int64_t B,
                               T* __restrict__ E, int ldE, T* __restrict__ feat, Status* st) {
+    constexpr int TOK = 8;  // rows per warp step: lanes 0..7 resolve their metadata chains in parallel
     const int lane = threadIdx.x & 31;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t p = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; p < B; p += nw)
-        gather_cand_row(in, perm, rep, first, ep, cp, p, E, ldE, feat, st, lane);
+    for (int64_t pb = ((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5) * TOK; pb < B;
+         pb += nw * TOK) {
+        CandMeta mine{};
+        if (lane < TOK && pb + lane < B) mine = cand_meta(in, perm, rep, first, cp, feat != nullptr, pb + lane);
+        const int nt = B - pb < TOK ? static_cast<int>(B - pb) : TOK;
+        for (int k = 0; k < nt; k++)
+            gather_cand_row(ep, cp, shfl_meta(mine, k), pb + k, E, ldE, feat, st, lane);
+    }
 }
 
 // grid for the grid-stride warp-per-row kernels (256 threads): <= 8 resident blocks per SM
@@ -316,13 +425,43 @@ inline unsigned warp_grid(int64_t rows) {
     return static_cast<unsigned>(g < 148 * 8 ? (g > 0 ? g : 1) : 148 * 8);
 }
 
+__global__ void k_build_cmb(const float* __restrict__ ae, const float* __restrict__ se, const float* __restrict__ pe,
+                            int n_surf, int max_len, int d_emb, int64_t n, float* __restrict__ cmb) {
+    for (int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
+         x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(x % d_emb);
+        const int64_t row = x / d_emb;
+        const int i = static_cast<int>(row % max_len);
+        const int as = static_cast<int>(row / max_len);
+        const int a = as / n_surf, s = as % n_surf;
+        cmb[x] = (ae[static_cast<size_t>(a) * d_emb + c] + se[static_cast<size_t>(s) * d_emb + c]) +
+                 pe[static_cast<size_t>(i) * d_emb + c];
+    }
+}
+
 }  // namespace
+
+void build_combined_emb(const float* action_emb, const float* surface_emb, const float* pos_emb, int n_act,
+                        int n_surf, int max_len, int d_emb, float* cmb, cudaStream_t s) {
+    const int64_t n = static_cast<int64_t>(n_act) * n_surf * max_len * d_emb;
+    if (n <= 0) return;
+    k_build_cmb<<<1184, 256, 0, s>>>(action_emb, surface_emb, pos_emb, n_surf, max_len, d_emb, n, cmb);
+    DCAT_LAUNCH_CHECK();
+}
 
 template <typename T>
 void gather_context(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const int32_t* tok_unique,
                     int64_t T_ctx, T* E, int ldE, cudaStream_t s) {
     if (T_ctx <= 0) return;
     const unsigned g = warp_grid(T_ctx);
+    if constexpr (std::is_same<T, bf16>::value) {
+        if (ep.cmb && ep.q == nullptr && ep.J <= 8 && ep.d_sub % 4 == 0 && ep.d_emb % 32 == 0 && ldE % 4 == 0) {
+            k_gather_ctx_g8<<<warp_grid((T_ctx + 3) / 4), 256, 0, s>>>(in, o.first, o.tok_off, ep, tok_unique, T_ctx, E,
+                                                                        ldE);
+            DCAT_LAUNCH_CHECK();
+            return;
+        }
+    }
     if ((ep.d_sub % 4) == 0 && (ep.d_emb % 4) == 0 && (ldE % 4) == 0 && ep.d_emb <= 128 * 8 && ep.J <= 32)
         k_gather_ctx<T, true><<<g, 256, 0, s>>>(in, o.first, o.tok_off, ep, tok_unique, T_ctx, E, ldE);
     else

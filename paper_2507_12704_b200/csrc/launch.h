@@ -94,7 +94,14 @@ struct EmbParams {
     const float* pos_emb;     // max_len x d_emb or null
     int d_emb;
     const float* lt;          // AuxLt learnable token row (d_emb) or null
+    // bf16 path: (action_emb[a] + surface_emb[s]) + pos_emb[i] precombined, row (a * n_surf + s) *
+    // max_len + i, or null (fp32 parity path, no learned positions)
+    const float* cmb;
+    int n_surf, max_len;
 };
+// the precombined action / surface / position rows of EmbParams::cmb (n_act * n_surf * max_len x d_emb)
+void build_combined_emb(const float* action_emb, const float* surface_emb, const float* pos_emb, int n_act,
+                        int n_surf, int max_len, int d_emb, float* cmb, cudaStream_t s);
 template <typename T>
 void gather_context(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const int32_t* tok_unique,
                     int64_t T_ctx, T* E, int ldE, cudaStream_t s);
