@@ -13,7 +13,9 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -104,6 +106,7 @@ struct dcat_model {
     uint64_t* seed_mix = nullptr;
     int J = 0, R = 0, d_sub = 0;
     float *action_emb = nullptr, *surface_emb = nullptr, *pos_emb = nullptr;
+    int t_dedup_end = 0;   // profiling mark after the plan read-back
     float* cmb = nullptr;  // (action + surface) + pos rows for the bf16 context gather, or null
     Lin phi_in1, phi_in2, phi_out1, phi_out2;
     std::vector<LayerW> layers;
@@ -129,6 +132,7 @@ struct dcat_model {
     bool last_vt = false;
     void* last_kv = nullptr;
     std::vector<int64_t> last_tok_off;
+    const int64_t* last_tok_off_dev = nullptr;  // the last call's context token offsets (read lazily)
     dcat_call_stats stats{};
     std::vector<std::pair<const char*, float>> stage_ms;
     std::vector<cudaEvent_t> ev_pool;
@@ -145,6 +149,11 @@ struct dcat_model {
 namespace {
 
 // ---------------------------------------------------------------- profiling
+bool host_timing() {  // DCAT_HOST_TIMING=1: host-side phase times of each call on stderr (tools)
+    static const bool on = getenv("DCAT_HOST_TIMING") != nullptr;
+    return on;
+}
+
 int mark(dcat_model* m, cudaStream_t s) {
     if (!m->profiling) return -1;
     if (m->ev_next >= static_cast<int>(m->ev_pool.size())) {
@@ -323,10 +332,13 @@ bool use_tc_attention(const dcat_model* m, bool f32) {
 void run_dedup(dcat_model* m, const Staged& sb, const DedupOut& o, cudaStream_t s) {
     uint64_t mask = debug_hash_mask();
     const int kTileCtx = m->tile_ctx, kTileCross = m->tile_cross;
+    const int t0 = mark(m, s);
     dedup_plan(sb.in, o, mask, kTileCtx, kTileCross, s);
     m->stats.kernel_launches += 18;
+    const int t1 = mark(m, s);
     DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
     DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+    span(m, "dedup.kernels", t0, t1);
     if (m->st_host->collisions > 0 && m->st_host->err_bits == 0) {
         dedup_repair(sb.in, o, m->st_host->collisions, kTileCtx, kTileCross, mask, s);
         m->stats.kernel_launches += 5 * 5 + 11;
@@ -509,6 +521,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     const bool full_last = lite || auxlt;  // the context pass must emit the final hidden rows
 
     int t_stage0 = mark(m, s);
+    span(m, "host.after_sync", m->t_dedup_end, t_stage0);
     // tiles + token map
     Tile* ctx_tiles = m->b_dd[20].get<Tile>(std::max(st.ctx_tiles, 1));
     Tile* cross_tiles = m->b_dd[21].get<Tile>(std::max(st.cross_tiles, 1));
@@ -979,6 +992,7 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
                             float* module_logits, float* h_cand, int32_t flags, void* stream) {
     if (!m || !batch || !ft || !logits || !module_logits) return set_err(DCAT_EINVAL, "null argument");
     return guarded(m, [&]() -> int {
+        const auto h_entry = std::chrono::steady_clock::now();
         int rc = validate_ft(m, ft, batch);
         if (rc) return rc;
         cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1001,8 +1015,10 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         sb.in.lt_token = ft->use_seq_module && ft->variant == DCAT_VARIANT_AUXLT;
         DedupOut o = dedup_buffers(m, B);
         int t1 = mark(m, s);
+        const double h_pre = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h_entry).count();
         run_dedup(m, sb, o, s);
         int t2 = mark(m, s);
+        m->t_dedup_end = t2;
         Status st = *m->st_host;
         if (!ft->use_seq_module) st.err_bits &= ~(ERR_ACTION | ERR_SURFACE | ERR_POS_CTX | ERR_POS_CAND);
         if (st.err_bits) {
@@ -1040,6 +1056,7 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
         int t4 = mark(m, s);
         DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+        const auto h_sync = std::chrono::steady_clock::now();
         if (m->profiling) {
             span(m, "h2d", t0, t1);
             span(m, "dedup", t1, t2);
@@ -1055,11 +1072,13 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         if (fin.err_bits & ERR_AGE) return set_err(DCAT_EINVAL, "candidate age must be non-negative");
         if (fin.nonfinite_layer > 0)
             return set_err(DCAT_ENONFINITE, "non-finite activation in layer " + std::to_string(fin.nonfinite_layer - 1));
-        if (ft->use_seq_module) {
-            // keep the context token offsets for dcat_debug_kv
-            m->last_tok_off.resize(static_cast<size_t>(st.b_u) + 1);
-            DCAT_CUDA_CHECK(cudaMemcpy(m->last_tok_off.data(), o.tok_off, sizeof(int64_t) * (st.b_u + 1),
-                                       cudaMemcpyDeviceToHost));
+        // the context token offsets stay on the device until the next call; dcat_debug_kv reads them
+        m->last_tok_off.clear();
+        m->last_tok_off_dev = ft->use_seq_module ? o.tok_off : nullptr;
+        if (host_timing()) {
+            const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h_entry).count();
+            std::fprintf(stderr, "[dcat host] entry->dedup launch %.1f us, final sync->return (incl.) %.1f us, total %.1f us\n",
+                         h_pre, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - h_sync).count(), us);
         }
         return DCAT_OK;
     });
@@ -1068,6 +1087,11 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
 int dcat_debug_kv(dcat_model* m, int32_t layer, int32_t unique, float* k, float* v, int32_t* n) {
     if (!m || !n) return set_err(DCAT_EINVAL, "null argument");
     return guarded(m, [&]() -> int {
+        if (m->last_tok_off.empty() && m->last_tok_off_dev && m->last_bu >= 0) {
+            m->last_tok_off.resize(static_cast<size_t>(m->last_bu) + 1);
+            DCAT_CUDA_CHECK(cudaMemcpy(m->last_tok_off.data(), m->last_tok_off_dev,
+                                       sizeof(int64_t) * (static_cast<size_t>(m->last_bu) + 1), cudaMemcpyDeviceToHost));
+        }
         if (unique < 0 || unique >= m->last_bu || layer < 0 || layer >= m->cfg.n_layers ||
             m->last_tok_off.size() < static_cast<size_t>(unique) + 2)
             return set_err(DCAT_EINVAL, "no such unique / layer in the last call");
