@@ -15,8 +15,13 @@ import sys
 
 rep = sys.argv[1]
 n_layers = int(sys.argv[2]) if len(sys.argv) > 2 else 4
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.endswith(".csv"):  # an exported `ncu -i ... --page raw --csv` (any launches; non-GEMM ones are skipped)
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
+while rows and "Kernel Name" not in rows[0]:
+    rows = rows[1:]
 h = rows[0]
 col = {n: i for i, n in enumerate(h)}
 labels = ["ctx.phi_in1", "ctx.phi_in2"]
@@ -37,7 +42,9 @@ def f(r, name, scale=1.0):
 
 launches = []
 for k, r in enumerate(rows[2:]):
-    if not r or not r[col["Kernel Name"]]:
+    if not r or len(r) != len(h) or not r[col["Kernel Name"]]:
+        continue
+    if not any(x in r[col["Kernel Name"]] for x in ("k_gemm_tc", "k_ffn_tc")):
         continue
     rd, wr = f(r, "dram__bytes_read.sum"), f(r, "dram__bytes_write.sum")
     launches.append({
