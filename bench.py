@@ -179,7 +179,7 @@ def run_ours(args, rank, world, local_rank):
     # the request batch of the whole job: U users per GPU; each rank keeps the
     # user-disjoint shard of its content hash (sharding.py), scores it, and the
     # scores are gathered to rank 0 in the global row order (one NCCL gather)
-    from paper_2507_12704_b200.sharding import gather_scores as gather_rows
+    from paper_2507_12704_b200.sharding import ScoreGather
     from paper_2507_12704_b200.sharding import local_batch, shard_rows
     glob = make_batch(U * world, C, L, seed=1, layout="interleaved", shared_storage=not args.private_rows)
     shards = shard_rows(glob, world)
@@ -194,10 +194,12 @@ def run_ours(args, rank, world, local_rank):
     out_dev = (torch.empty((B, 3), device=dev), torch.empty((B, 3), device=dev), None)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
+    sg = ScoreGather(shards, B_total, (3, 3), dev) if world > 1 else None
+
     def gather_scores(lg, ml):
         if world == 1:
             return
-        gather_rows(torch.cat([lg, ml], dim=1), shards, B_total)
+        sg(lg, ml)
 
     def step_device(profile=False):
         lg, ml, _ = model.rank_forward_batch(dbatch, ft, stream=sp, out=out_dev, profile=profile)
@@ -287,9 +289,28 @@ def run_ours(args, rank, world, local_rank):
         priv = pms / max(1, args.steps // 2)
         del pbd
 
-    t = torch.tensor([ms_dev, e2e_ms, priv or 0.0], device=dev, dtype=torch.float64)
+    # N > 1 diagnostics: every rank's own device ms per step, and the score gather timed alone
+    per_rank = [ms_dev / args.steps]
+    gather_ms = None
+    if world > 1:
+        lg0, ml0 = out_dev[0], out_dev[1]
+        dist.barrier()
+        torch.cuda.synchronize()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            gather_scores(lg0, ml0)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gather_ms = g0.elapsed_time(g1) / args.steps
+        pr = torch.zeros(world, device=dev, dtype=torch.float64)
+        pr[rank] = ms_dev / args.steps
+        dist.all_reduce(pr)
+        per_rank = [round(float(x), 4) for x in pr.tolist()]
+    t = torch.tensor([ms_dev, e2e_ms, priv or 0.0, gather_ms or 0.0], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gather_ms = float(t[3])
     ms_dev, e2e_ms, priv = float(t[0]), float(t[1]), (float(t[2]) if priv is not None else None)
     if rank != 0:
         return None
@@ -377,6 +398,9 @@ def run_ours(args, rank, world, local_rank):
     }
     if priv:
         line["value_private_rows"] = round(B_total / (priv / 1e3), 1)
+    if world > 1:
+        line["per_rank_ms_per_step"] = per_rank
+        line["score_gather_ms"] = round(gather_ms, 4)
     if world == 1 and not args.no_cpu:
         line["cpu_baseline"], line["parity"] = cpu_baseline(args, w, host, ft, model)
     return line

@@ -97,6 +97,46 @@ def local_batch(b: Batch, rows: np.ndarray) -> Batch:
                  None if b.aux is None else np.ascontiguousarray(b.aux[rows]))
 
 
+class ScoreGather:
+    """gather_scores with everything that does not change between calls prepared once: the
+    padded send buffer, one receive buffer on dst, and the source index of every output row
+    (rank r's local row i sits at r * cap + i of the receive buffer). One call is two copies
+    into the send buffer, one NCCL gather and one index_select on dst."""
+
+    def __init__(self, rows: List[np.ndarray], n_rows: int, widths, device, dtype=None, group=None, dst: int = 0):
+        import torch
+        import torch.distributed as dist
+        self.group, self.dst = group, dst
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.widths = list(widths)
+        width = sum(self.widths)
+        dtype = dtype or torch.float32
+        self.cap = max(len(r) for r in rows)
+        self.n_local = len(rows[self.rank])
+        self.send = torch.zeros((self.cap, width), dtype=dtype, device=device)
+        self.recv = None
+        if self.rank == dst:
+            self.recv = torch.empty((self.world * self.cap, width), dtype=dtype, device=device)
+            src = np.empty(n_rows, np.int64)
+            for r in range(self.world):
+                src[rows[r]] = r * self.cap + np.arange(len(rows[r]), dtype=np.int64)
+            self.src = torch.from_numpy(src).to(device)
+
+    def __call__(self, *parts):
+        import torch
+        import torch.distributed as dist
+        c = 0
+        for t, w in zip(parts, self.widths):
+            self.send[: self.n_local, c:c + w].copy_(t[: self.n_local])
+            c += w
+        chunks = list(self.recv.chunk(self.world)) if self.recv is not None else None
+        dist.gather(self.send, chunks, dst=self.dst, group=self.group)
+        if self.recv is None:
+            return None
+        return torch.index_select(self.recv, 0, self.src)
+
+
 def gather_scores(local: "torch.Tensor", rows: List[np.ndarray], n_rows: int, group=None, dst: int = 0):
     """Gather each rank's [n_local, k] score tensor to `dst` and return the
     [n_rows, k] result in original row order on dst (None elsewhere). Ranks pad

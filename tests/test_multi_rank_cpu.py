@@ -37,8 +37,16 @@ def _worker(rank, world, port, out_path):
     logits, mlog, _, _ = orc.rank_forward_batch(w, ft, b.take(rows[rank]))
     local = torch.from_numpy(np.concatenate([logits, mlog], 1))
     full = gather_scores(local, rows, b.n_rows)
+    # the bench's cached form: logits and module logits as two parts, called twice
+    from paper_2507_12704_b200.sharding import ScoreGather
+    sg = ScoreGather(rows, b.n_rows, (3, 3), "cpu")
+    for _ in range(2):
+        full2 = sg(torch.from_numpy(logits), torch.from_numpy(mlog))
     if rank == 0:
+        np.testing.assert_array_equal(full2.numpy(), full.numpy())
         np.save(out_path, full.numpy())
+    else:
+        assert full2 is None
     dist.barrier()
     dist.destroy_process_group()
 
