@@ -1002,43 +1002,50 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
             };
             // acc2 <- residual rows: [128 x 32] fp32 ring slots copied into TMEM (tcgen05.cp is ordered
             // before the MMAs that accumulate onto it)
-            auto resid_to_acc2 = [&]() {
-                wait_lead(acc2_empty, (i & 1) ^ 1);
+            // TAIL: x rows + A_o . Wo^T accumulate in the acc1 columns (free once the previous
+            // tile's last two GELU chunks are read), so this phase overlaps the previous tile's
+            // final epilogue on acc2; the LN2 epilogue then moves x_mid into acc2.
+            auto resid_to = [&](uint32_t t_dst) {
+                if constexpr (!TAIL) wait_lead(acc2_empty, (i & 1) ^ 1);
                 ptx::tc_fence_after();
                 for (int cc = 0; cc < D; cc += 32, it++) {
                     const uint32_t s = next_slot();
 #pragma unroll
                     for (int k = 0; k < 4; k++) {
                         const uint64_t sd = ptx::sdesc_sw128(r_base + s * C::SLOT + k * 32);
-                        if constexpr (CL == 2) ptx::tmem_cp_128x256b_pair(T_ACC2 + cc + 8 * k, sd);
-                        else ptx::tmem_cp_128x256b(T_ACC2 + cc + 8 * k, sd);
+                        if constexpr (CL == 2) ptx::tmem_cp_128x256b_pair(t_dst + cc + 8 * k, sd);
+                        else ptx::tmem_cp_128x256b(t_dst + cc + 8 * k, sd);
                     }
                     commit(&empty[s]);
                 }
             };
+            auto resid_to_acc2 = [&]() { resid_to(T_ACC2); };
             for (int u = unit0; u < units; u += ustride, i++) {
                 wait_lead(a_full, i & 1);
                 ptx::tc_fence_after();
-                if constexpr (TAIL) {  // acc2 = x + A_o . Wo^T, then the epilogue's x_mid / LN2 hand-off
-                    resid_to_acc2();
+                if constexpr (TAIL) {  // acc1 cols = x + A_o . Wo^T, then the epilogue's x_mid / LN2 hand-off
+                    // both acc1 buffers free: the waits the next two FFN1 chunks would do
+                    wait_lead(&acc1_empty[c1 & 1], ((c1 >> 1) & 1) ^ 1);
+                    wait_lead(&acc1_empty[(c1 + 1) & 1], (((c1 + 1) >> 1) & 1) ^ 1);
+                    resid_to(T_ACC1);
                     ptx::tc_fence_after();
                     for (int kb = 0; kb < C::KB1; kb++)
                         for (int nh = 0; nh < D / C::NW2; nh++, it++) {
                             const uint32_t s = next_slot();
 #pragma unroll
                             for (int k = 0; k < 4; k++)
-                                mma(T_ACC2 + nh * C::NW2, a_base + kb * 16384 + k * 32, r_base + s * C::SLOT + k * 32,
+                                mma(T_ACC1 + nh * C::NW2, a_base + kb * 16384 + k * 32, r_base + s * C::SLOT + k * 32,
                                     idesc2, 1u);
                             commit(&empty[s]);
                         }
                     commit(o_full);
-                    ptx::mbar_wait(a2_full, i & 1);
+                    ptx::mbar_wait(a2_full, i & 1);  // x_mid in acc2, LN2 rows in the A tile, acc1 free
                     ptx::tc_fence_after();
                 }
                 for (int j = 0; j < nch + LA; j++) {
                     if (j < nch) {  // FFN1 chunk j -> acc1[b]
                         const int b = c1 & 1;
-                        wait_lead(&acc1_empty[b], ((c1 >> 1) & 1) ^ 1);
+                        if (!TAIL || j >= 2) wait_lead(&acc1_empty[b], ((c1 >> 1) & 1) ^ 1);
                         FFN_EV(1, j);
                         ptx::tc_fence_after();
                         for (int p = 0; p < C::S1; p++, it++) {
@@ -1109,6 +1116,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                 // LN2(x_mid) (model.cpp:386) -> row r of the A tile, bf16, SW128 K-major
                 const bool live = row < M;
                 const uint32_t tacc = T_ACC2 + (static_cast<uint32_t>(q * 32) << 16) + c0;
+                const uint32_t tsrc = T_ACC1 + (static_cast<uint32_t>(q * 32) << 16) + c0;  // x + A_o . Wo^T
                 const uint32_t a_row = ptx::smem_u32(sA) + r * 128;
                 float v[32];
                 float s1[1] = {0.f};
@@ -1117,7 +1125,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                 ptx::tc_fence_after();
 #pragma unroll 1
                 for (int h = 0; h < C::FCOLS; h += 32) {
-                    tmem_load32(tacc + h, v);
+                    tmem_load32(tsrc + h, v);
 #pragma unroll
                     for (int j = 0; j < 8; j++) {
                         const float4 bb = lds4(s_par + 4u * (P_BO + c0 + h + 4 * j));
