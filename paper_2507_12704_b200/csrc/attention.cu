@@ -250,6 +250,8 @@ __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS
             constexpr int NJ = SUB / 8;                // n-tiles of S
             const int kbase = blk * BKV + sub * SUB;
             if (kbase >= tile.nkv) break;  // uniform across the CTA
+            // causal: keys past this warp's last query row are masked for all its rows (warp-uniform)
+            if (CAUSAL && kbase > tile.qloc + rw[RT - 1] + 15) continue;
             float s[RT][NJ][4];
 #pragma unroll
             for (int t = 0; t < RT; t++)
