@@ -1006,7 +1006,7 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         int64_t B = batch->n_rows;
         if (B == 0) return DCAT_OK;
         m->vt = use_tc_attention(m, f32);
-        m->tile_ctx = m->vt ? 128 : 64;
+        m->tile_ctx = m->vt ? 128 : kCtxTile;
         m->tile_cross = 128;
         int t0 = mark(m, s);
         Staged sb = stage_batch(m, batch, device,

@@ -36,6 +36,12 @@ __host__ __device__ __forceinline__ int seq_tokens(const DedupIn& in, int valid)
     return seq_kept(in, valid) + in.lt_token;
 }
 
+// query rows per context-attention tile of the mma.sync flash kernel (attention.cu)
+#ifndef DCAT_CTX_BQ
+#define DCAT_CTX_BQ 64
+#endif
+constexpr int kCtxTile = DCAT_CTX_BQ;
+
 struct Tile {  // one attention work item: <= BM query rows of one unique
     int q0, nq;     // first query row, number of query rows
     int kv0, nkv;   // first context K/V row, number of keys visible to the tile
