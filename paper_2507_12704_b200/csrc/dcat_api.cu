@@ -139,10 +139,18 @@ struct dcat_model {
     std::vector<std::pair<const char*, std::pair<int, int>>> ev_marks;
     bool profiling = false;
     int ev_next = 0;
+    // host batches: the candidate-side arrays (candidate, age, aux) are copied on a side stream
+    // after the dedup inputs, overlapping the dedup and context kernels (they are first read by
+    // the candidate gather, which waits on cand_ready)
+    cudaStream_t side = nullptr;
+    cudaEvent_t side_start = nullptr, cand_ready = nullptr;
 
     ~dcat_model() {
         if (st_host) cudaFreeHost(st_host);
         for (auto e : ev_pool) cudaEventDestroy(e);
+        if (side_start) cudaEventDestroy(side_start);
+        if (cand_ready) cudaEventDestroy(cand_ready);
+        if (side) cudaStreamDestroy(side);
     }
 };
 
@@ -229,7 +237,12 @@ struct Staged {
     const uint64_t* candidate;
     const double* age;
     const float* aux;
+    cudaEvent_t cand_ready = nullptr;  // side-stream copy of candidate / age / aux, or null
 };
+// the stream waits for the side-stream candidate copies (before the first candidate gather)
+void wait_cand(const Staged& sb, cudaStream_t s) {
+    if (sb.cand_ready) DCAT_CUDA_CHECK(cudaStreamWaitEvent(s, sb.cand_ready, 0));
+}
 
 template <typename T>
 const T* stage(Buf& b, const T* src, size_t n, bool device, cudaStream_t s, int64_t* h2d) {
@@ -240,7 +253,8 @@ const T* stage(Buf& b, const T* src, size_t n, bool device, cudaStream_t s, int6
     return d;
 }
 
-Staged stage_batch(dcat_model* m, const dcat_batch* b, bool device, bool aux_needed, cudaStream_t s) {
+Staged stage_batch(dcat_model* m, const dcat_batch* b, bool device, bool aux_needed, cudaStream_t s,
+                   bool side_cand = false) {
     Staged st;
     int64_t h2d = 0;
     int64_t B = b->n_rows, E = b->n_events;
@@ -266,11 +280,26 @@ Staged stage_batch(dcat_model* m, const dcat_batch* b, bool device, bool aux_nee
     st.in.pos_learned = m->cfg.pos_learned;
     st.in.window = 0;
     st.in.lt_token = 0;
-    st.candidate = stage(m->b_in[6], b->candidate, B, device, s, &h2d);
-    st.age = stage(m->b_in[7], b->age_seconds, B, device, s, &h2d);
+    cudaStream_t cs = s;
+    if (side_cand && !device) {  // queued behind the dedup inputs, on the side stream
+        if (!m->side) {
+            DCAT_CUDA_CHECK(cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking));
+            DCAT_CUDA_CHECK(cudaEventCreateWithFlags(&m->side_start, cudaEventDisableTiming));
+            DCAT_CUDA_CHECK(cudaEventCreateWithFlags(&m->cand_ready, cudaEventDisableTiming));
+        }
+        DCAT_CUDA_CHECK(cudaEventRecord(m->side_start, s));
+        DCAT_CUDA_CHECK(cudaStreamWaitEvent(m->side, m->side_start, 0));
+        cs = m->side;
+    }
+    st.candidate = stage(m->b_in[6], b->candidate, B, device, cs, &h2d);
+    st.age = stage(m->b_in[7], b->age_seconds, B, device, cs, &h2d);
     st.aux = nullptr;
     if (aux_needed && b->aux) {
-        st.aux = stage(m->b_aux, b->aux, static_cast<size_t>(B) * b->d_aux, device, s, &h2d);
+        st.aux = stage(m->b_aux, b->aux, static_cast<size_t>(B) * b->d_aux, device, cs, &h2d);
+    }
+    if (cs != s) {
+        DCAT_CUDA_CHECK(cudaEventRecord(m->cand_ready, cs));
+        st.cand_ready = m->cand_ready;
     }
     return st;
 }
@@ -650,6 +679,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     if (lite) {  // candidate-independent selector: no crossing pass (finetune.cpp:439-456)
         CandParams cp{sb.candidate, sb.age, sb.aux, m->aux_proj, m->d_aux, 0, ft.max_events, ft.fresh_days,
                       ft.mid_days, m->d_module, kh, 0};
+        wait_cand(sb, s);
         gather_candidates<T>(sb.in, o, ep, cp, B, A.E, de, A.feat, s);
         broadcast_selectors<T>(o.perm, o.rep, B, sel, d, A.feat, kh, 0, h_cand ? A.hc : nullptr, s);
         module_logits(o.perm, o.rep, B, sel, nullptr, d, m->mod_w, m->mod_b, A.mlog_p, s);
@@ -675,6 +705,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     CandParams cp{sb.candidate, sb.age, sb.aux, m->aux_proj, m->d_aux,
                   ft.variant == DCAT_VARIANT_AUX || ft.variant == DCAT_VARIANT_AUXLT,
                   ft.max_events, ft.fresh_days, ft.mid_days, m->d_module, kh, auxlt ? 1 : 0};
+    wait_cand(sb, s);
     gather_candidates<T>(sb.in, o, ep, cp, B, A.E, de, A.feat, s);
     m->stats.kernel_launches += 1;
     Epi e = base_epi(m, EPI_BIAS);
@@ -766,6 +797,7 @@ void run_head_only(dcat_model* m, const Staged& sb, const DedupOut& o, const dca
                  m->cfg.d_emb, m->lt, nullptr, m->cfg.n_surfaces, m->cfg.max_len};
     CandParams cp{sb.candidate, sb.age, nullptr, m->aux_proj, 0, 0, ft.max_events, ft.fresh_days, ft.mid_days,
                   0, kh, 0};
+    wait_cand(sb, s);
     gather_candidates<T>(sb.in, o, ep, cp, B, E, m->cfg.d_emb, feat, s);
     m->stats.kernel_launches += 1;
     Epi e = base_epi(m, EPI_HEAD);
@@ -1010,7 +1042,14 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         m->tile_cross = 128;
         int t0 = mark(m, s);
         Staged sb = stage_batch(m, batch, device,
-                                ft->variant == DCAT_VARIANT_AUX || ft->variant == DCAT_VARIANT_AUXLT, s);
+                                ft->variant == DCAT_VARIANT_AUX || ft->variant == DCAT_VARIANT_AUXLT, s, true);
+        // every exit (errors included) leaves no copy of the borrowed host arrays in flight
+        struct SideDone {
+            cudaEvent_t e;
+            ~SideDone() {
+                if (e) cudaEventSynchronize(e);
+            }
+        } side_done{sb.cand_ready};
         sb.in.window = ft->use_seq_module ? ft->window : 0;  // fixed-window sequence module
         sb.in.lt_token = ft->use_seq_module && ft->variant == DCAT_VARIANT_AUXLT;
         DedupOut o = dedup_buffers(m, B);
