@@ -144,6 +144,16 @@ struct dcat_model {
     // the candidate gather, which waits on cand_ready)
     cudaStream_t side = nullptr;
     cudaEvent_t side_start = nullptr, cand_ready = nullptr;
+    // the dedup / plan launch sequence as a CUDA graph, re-captured when its arguments change
+    struct DedupKey {
+        DedupIn in;
+        DedupOut o;
+        uint64_t mask;
+        int tile_ctx, tile_cross;
+    };
+    DedupKey dd_key;
+    cudaGraphExec_t dd_exec = nullptr;
+    cudaStream_t cap = nullptr;
 
     ~dcat_model() {
         if (st_host) cudaFreeHost(st_host);
@@ -151,6 +161,8 @@ struct dcat_model {
         if (side_start) cudaEventDestroy(side_start);
         if (cand_ready) cudaEventDestroy(cand_ready);
         if (side) cudaStreamDestroy(side);
+        if (dd_exec) cudaGraphExecDestroy(dd_exec);
+        if (cap) cudaStreamDestroy(cap);
     }
 };
 
@@ -256,6 +268,7 @@ const T* stage(Buf& b, const T* src, size_t n, bool device, cudaStream_t s, int6
 Staged stage_batch(dcat_model* m, const dcat_batch* b, bool device, bool aux_needed, cudaStream_t s,
                    bool side_cand = false) {
     Staged st;
+    std::memset(&st.in, 0, sizeof st.in);  // padding too: the dedup graph cache compares it bytewise
     int64_t h2d = 0;
     int64_t B = b->n_rows, E = b->n_events;
     st.in.B = B;
@@ -306,6 +319,7 @@ Staged stage_batch(dcat_model* m, const dcat_batch* b, bool device, bool aux_nee
 
 DedupOut dedup_buffers(dcat_model* m, int64_t B) {
     DedupOut o;
+    std::memset(&o, 0, sizeof o);  // padding too: the dedup graph cache compares it bytewise
     int64_t cap = 1024;
     while (cap < 2 * B) cap <<= 1;
     size_t n1 = static_cast<size_t>(B) + 1;
@@ -362,7 +376,33 @@ void run_dedup(dcat_model* m, const Staged& sb, const DedupOut& o, cudaStream_t 
     uint64_t mask = debug_hash_mask();
     const int kTileCtx = m->tile_ctx, kTileCross = m->tile_cross;
     const int t0 = mark(m, s);
-    dedup_plan(sb.in, o, mask, kTileCtx, kTileCross, s);
+    static const bool no_graph = getenv("DCAT_NO_DEDUP_GRAPH") != nullptr;
+    if (no_graph) {
+        dedup_plan(sb.in, o, mask, kTileCtx, kTileCross, s);
+    } else {  // ~27 small launches replayed as one graph (captured on a private stream)
+        dcat_model::DedupKey k;
+        std::memset(&k, 0, sizeof k);
+        k.in = sb.in;
+        k.o = o;
+        k.mask = mask;
+        k.tile_ctx = kTileCtx;
+        k.tile_cross = kTileCross;
+        if (!m->dd_exec || std::memcmp(&k, &m->dd_key, sizeof k) != 0) {
+            if (!m->cap) DCAT_CUDA_CHECK(cudaStreamCreateWithFlags(&m->cap, cudaStreamNonBlocking));
+            if (m->dd_exec) {
+                DCAT_CUDA_CHECK(cudaGraphExecDestroy(m->dd_exec));
+                m->dd_exec = nullptr;
+            }
+            cudaGraph_t g = nullptr;
+            DCAT_CUDA_CHECK(cudaStreamBeginCapture(m->cap, cudaStreamCaptureModeThreadLocal));
+            dedup_plan(sb.in, o, mask, kTileCtx, kTileCross, m->cap);
+            DCAT_CUDA_CHECK(cudaStreamEndCapture(m->cap, &g));
+            DCAT_CUDA_CHECK(cudaGraphInstantiate(&m->dd_exec, g, 0));
+            DCAT_CUDA_CHECK(cudaGraphDestroy(g));
+            m->dd_key = k;
+        }
+        DCAT_CUDA_CHECK(cudaGraphLaunch(m->dd_exec, s));
+    }
     m->stats.kernel_launches += 18;
     const int t1 = mark(m, s);
     DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
