@@ -13,6 +13,7 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -43,6 +44,10 @@ uint64_t host_mix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 
+// bumped whenever a work buffer is (re)allocated: a cached graph of the scoring pass is only
+// replayed while every buffer it captured still exists
+std::atomic<uint64_t> g_alloc_epoch{0};
+
 struct Buf {
     void* p = nullptr;
     size_t cap = 0;
@@ -59,6 +64,7 @@ struct Buf {
             c = (c + 4095) & ~size_t(4095);
             DCAT_CUDA_CHECK(cudaMalloc(&p, c));
             cap = c;
+            g_alloc_epoch++;
         }
         return static_cast<T*>(p);
     }
@@ -154,6 +160,13 @@ struct dcat_model {
     DedupKey dd_key;
     cudaGraphExec_t dd_exec = nullptr;
     cudaStream_t cap = nullptr;
+    // the scoring pass after the plan read-back (run_dcat) as a CUDA graph: a call whose sizes,
+    // pointers and settings equal the previous call's is captured, and replayed while they repeat
+    std::vector<uint64_t> run_seen, run_key;
+    cudaGraphExec_t run_exec = nullptr;
+    dcat_call_stats run_stats{};
+    void* run_last_kv = nullptr;  // host bookkeeping run_dcat sets, restored on replay
+    int64_t run_last_Tp = 0;
 
     ~dcat_model() {
         if (st_host) cudaFreeHost(st_host);
@@ -162,6 +175,7 @@ struct dcat_model {
         if (cand_ready) cudaEventDestroy(cand_ready);
         if (side) cudaStreamDestroy(side);
         if (dd_exec) cudaGraphExecDestroy(dd_exec);
+        if (run_exec) cudaGraphExecDestroy(run_exec);
         if (cap) cudaStreamDestroy(cap);
     }
 };
@@ -1060,6 +1074,45 @@ int dcat_dedup(dcat_model* m, const dcat_batch* batch, int32_t* rep, int32_t* fi
     });
 }
 
+namespace {
+// everything run_dcat's launches depend on: sizes, every pointer, settings, the buffer epoch
+std::vector<uint64_t> run_key(const dcat_model* m, const Staged& sb, const DedupOut& o,
+                              const dcat_finetune_config& ft, const Status& st, const float* dl, const float* dm,
+                              const float* dh, bool f32) {
+    std::vector<uint64_t> k;
+    auto add_bytes = [&](const void* p, size_t n) {
+        const uint8_t* b = static_cast<const uint8_t*>(p);
+        for (size_t i = 0; i < n; i += 8) {
+            uint64_t v = 0;
+            std::memcpy(&v, b + i, std::min<size_t>(8, n - i));
+            k.push_back(v);
+        }
+    };
+    add_bytes(&sb.in, sizeof sb.in);  // zero-padded (stage_batch)
+    add_bytes(&o, sizeof o);          // zero-padded (dedup_buffers)
+    k.push_back(reinterpret_cast<uintptr_t>(sb.candidate));
+    k.push_back(reinterpret_cast<uintptr_t>(sb.age));
+    k.push_back(reinterpret_cast<uintptr_t>(sb.aux));
+    k.push_back(static_cast<uint64_t>(st.b_u));
+    k.push_back(static_cast<uint64_t>(st.ctx_tokens));
+    k.push_back(static_cast<uint64_t>(st.ctx_tiles));
+    k.push_back(static_cast<uint64_t>(st.cross_tiles));
+    k.push_back(reinterpret_cast<uintptr_t>(dl));
+    k.push_back(reinterpret_cast<uintptr_t>(dm));
+    k.push_back(reinterpret_cast<uintptr_t>(dh));
+    k.push_back(static_cast<uint64_t>(ft.variant) | static_cast<uint64_t>(ft.use_seq_module) << 8 |
+                static_cast<uint64_t>(static_cast<uint32_t>(ft.window)) << 16 | static_cast<uint64_t>(f32) << 48 |
+                static_cast<uint64_t>(m->vt) << 49);
+    k.push_back(static_cast<uint64_t>(static_cast<uint32_t>(ft.max_events)) |
+                static_cast<uint64_t>(static_cast<uint32_t>(ft.d_aux)) << 32);
+    add_bytes(&ft.fresh_days, sizeof ft.fresh_days);
+    add_bytes(&ft.mid_days, sizeof ft.mid_days);
+    k.push_back(static_cast<uint64_t>(m->tile_ctx) | static_cast<uint64_t>(m->tile_cross) << 32);
+    k.push_back(g_alloc_epoch.load());
+    return k;
+}
+}  // namespace
+
 int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_finetune_config* ft, float* logits,
                             float* module_logits, float* h_cand, int32_t flags, void* stream) {
     if (!m || !batch || !ft || !logits || !module_logits) return set_err(DCAT_EINVAL, "null argument");
@@ -1118,8 +1171,51 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
             dh = h_cand ? m->b_out[2].get<float>(B * m->cfg.d_model) : nullptr;
         }
         if (ft->use_seq_module) {
-            if (f32) run_dcat<float>(m, sb, o, *ft, dl, dm, dh, s);
-            else run_dcat<bf16>(m, sb, o, *ft, dl, dm, dh, s);
+            auto run = [&](const Staged& b, cudaStream_t rs) {
+                if (f32) run_dcat<float>(m, b, o, *ft, dl, dm, dh, rs);
+                else run_dcat<bf16>(m, b, o, *ft, dl, dm, dh, rs);
+            };
+            static const bool no_graph = getenv("DCAT_NO_RUN_GRAPH") != nullptr;
+            if (no_graph || m->profiling) {
+                run(sb, s);
+            } else {
+                wait_cand(sb, s);  // outside any capture: the graph has no external dependency
+                Staged gb = sb;
+                gb.cand_ready = nullptr;
+                std::vector<uint64_t> key = run_key(m, gb, o, *ft, st, dl, dm, dh, f32);
+                if (m->run_exec && key == m->run_key) {  // replay
+                    DCAT_CUDA_CHECK(cudaGraphLaunch(m->run_exec, s));
+                    const dcat_call_stats keep = m->stats;
+                    m->stats = m->run_stats;
+                    m->stats.b_u = keep.b_u;
+                    m->stats.ctx_tokens = keep.ctx_tokens;
+                    m->stats.kernel_launches += keep.kernel_launches;
+                    m->last_kv = m->run_last_kv;
+                    m->last_Tp = m->run_last_Tp;
+                } else if (key == m->run_seen) {  // second call with this shape: capture it
+                    if (!m->cap) DCAT_CUDA_CHECK(cudaStreamCreateWithFlags(&m->cap, cudaStreamNonBlocking));
+                    if (m->run_exec) {
+                        DCAT_CUDA_CHECK(cudaGraphExecDestroy(m->run_exec));
+                        m->run_exec = nullptr;
+                    }
+                    const dcat_call_stats before = m->stats;
+                    cudaGraph_t g = nullptr;
+                    DCAT_CUDA_CHECK(cudaStreamBeginCapture(m->cap, cudaStreamCaptureModeRelaxed));
+                    run(gb, m->cap);
+                    DCAT_CUDA_CHECK(cudaStreamEndCapture(m->cap, &g));
+                    DCAT_CUDA_CHECK(cudaGraphInstantiate(&m->run_exec, g, 0));
+                    DCAT_CUDA_CHECK(cudaGraphDestroy(g));
+                    DCAT_CUDA_CHECK(cudaGraphLaunch(m->run_exec, s));
+                    m->run_key = run_key(m, gb, o, *ft, st, dl, dm, dh, f32);
+                    m->run_stats = m->stats;  // the pass's own counters, replayed with the graph
+                    m->run_stats.kernel_launches -= before.kernel_launches;
+                    m->run_last_kv = m->last_kv;
+                    m->run_last_Tp = m->last_Tp;
+                } else {
+                    run(gb, s);
+                    m->run_seen = run_key(m, gb, o, *ft, st, dl, dm, dh, f32);
+                }
+            }
         } else {
             if (f32) run_head_only<float>(m, sb, o, *ft, dl, dm, s);
             else run_head_only<bf16>(m, sb, o, *ft, dl, dm, s);

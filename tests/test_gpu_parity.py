@@ -273,6 +273,39 @@ def test_device_resident_io_matches_host(api, orc):
 
 # ------------------------------------------------------------------ errors (reference SEQFM_CHECKs)
 
+def test_scoring_graph_replay(api, orc):
+    """Repeated calls with the same sizes and buffers replay a captured CUDA graph of the scoring
+    pass (third call on): results must equal the stream-launched pass, also when the data in the
+    same device buffers changes between calls."""
+    import torch
+    spec, w, b = _base_setup(orc, 24, 6, 48, seed=9, ragged=True)
+    ft = FinetuneSpec(max_events=48)
+    m = api.DcatModel(w)
+    bd = b.to(lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int64) if a.dtype == np.uint64 else a).cuda())
+    out = (torch.empty((b.n_rows, 3), device="cuda"), torch.empty((b.n_rows, 3), device="cuda"), None)
+    runs = []
+    for _ in range(4):  # stream, capture + launch, replay, replay
+        lg, ml, _ = m.rank_forward_batch(bd, ft, out=out)
+        torch.cuda.synchronize()
+        runs.append((lg.cpu().numpy().copy(), ml.cpu().numpy().copy()))
+    for lg, ml in runs[1:]:
+        np.testing.assert_array_equal(lg, runs[0][0])
+        np.testing.assert_array_equal(ml, runs[0][1])
+    # new candidates in the same buffers (same plan, same sizes): the replay sees the new data
+    new_c = np.random.default_rng(3).integers(0, 1_000_000, b.n_rows).astype(np.uint64)
+    bd.candidate.copy_(torch.from_numpy(new_c.view(np.int64)))
+    lg, ml, _ = m.rank_forward_batch(bd, ft, out=out)
+    torch.cuda.synchronize()
+    b2 = b.take(np.arange(b.n_rows))
+    b2.candidate = new_c
+    fresh = api.DcatModel(w)  # its first call launches on the stream (no graph yet)
+    lr, mr, _ = fresh.rank_forward_batch(b2, ft)
+    np.testing.assert_array_equal(lg.cpu().numpy(), lr)
+    np.testing.assert_array_equal(ml.cpu().numpy(), mr)
+    rl, rm, _, _ = orc.rank_forward_batch(w, ft, b2)
+    assert rel_err(lr, rl) <= 3e-2
+
+
 def test_errors(api, orc):
     spec = ModelSpec(d_model=64, n_layers=2, n_heads=4, mlp_ratio=4, max_len=20, d_emb=64)
     w = orc.init_weights(spec, 3, table=(8, 128, 8, 7, 0.05))
