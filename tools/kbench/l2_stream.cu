@@ -178,10 +178,21 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    for (int rep = 0; rep < 2; rep++) cudaLaunchKernelEx(&cfg, k_stream<S, C>, m, mode, iters, blocks_per_region, d_out,
-                                                   static_cast<const uint8_t*>(buf), pieces);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int rep = 0; rep < 2; rep++) {
+        if (rep == 1) cudaEventRecord(e0);
+        cudaLaunchKernelEx(&cfg, k_stream<S, C>, m, mode, iters, blocks_per_region, d_out,
+                           static_cast<const uint8_t*>(buf), pieces);
+    }
+    cudaEventRecord(e1);
     cudaDeviceSynchronize();
-    unsigned long long h[296];
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    // whole-kernel rate: every CTA's bytes over the wall time (co-resident CTAs add up per SM)
+    const double tot_gbs = static_cast<double>(grid) * iters * BOX_BYTES / (ms * 1e-3) / 1e9;
+    unsigned long long h[1024];
     cudaMemcpy(h, d_out, sizeof h, cudaMemcpyDeviceToHost);
     double cyc = 0, lat = 0;
     int nm = 0;
@@ -195,8 +206,66 @@ void run(EncodeFn enc, void* buf, int mode, int grid, unsigned long long* d_out,
     lat /= nm;
     std::printf(
         "{\"mode\": %d, \"pieces\": %d, \"cluster\": %d, \"grid\": %d, \"stages\": %d, \"bytes_per_clk_per_cta\": %.1f, "
-        "\"latency_clk\": %.0f, \"err\": \"%s\"}\n",
-        mode, pieces, C, grid, S, static_cast<double>(iters) * BOX_BYTES / cyc, lat, cudaGetErrorString(cudaGetLastError()));
+        "\"latency_clk\": %.0f, \"kernel_GBps\": %.0f, \"per_SM_GBps\": %.1f, \"err\": \"%s\"}\n",
+        mode, pieces, C, grid, S, static_cast<double>(iters) * BOX_BYTES / cyc, lat, tot_gbs, tot_gbs / 148,
+        cudaGetErrorString(cudaGetLastError()));
+    std::fflush(stdout);
+}
+
+
+// P producer warps in ONE CTA, each with its own S-stage ring and mbarriers, all streaming the
+// same 1 MB: is the ~27 B/clk per CTA a per-CTA or a per-issuing-thread limit?
+template <int S, int P>
+__global__ void __launch_bounds__(32 * P, 1) k_stream_multi(const __grid_constant__ CUtensorMap map, int iters,
+                                                          int blocks_per_region) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[P][S];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        for (int s = 0; s < S; s++) ptx::mbar_init(&full[w][s], 1);
+        ptx::fence_barrier_init();
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) != 0) return;
+    uint8_t* my = ring + static_cast<size_t>(w) * S * BOX_BYTES;
+    const int n = iters / P;
+    for (int it = 0; it < n + S; it++) {
+        const int s = it % S;
+        if (it >= S) ptx::mbar_wait(&full[w][s], ((it - S) / S) & 1);
+        if (it < n) {
+            const int blk = (it * P + w) % blocks_per_region;
+            ptx::mbar_expect_tx(&full[w][s], BOX_BYTES);
+            ptx::tma_load_2d(my + s * BOX_BYTES, &map, &full[w][s], 0, blk * BOX_ROWS);
+        }
+    }
+}
+
+template <int S, int P>
+void run_multi(EncodeFn enc, void* buf, int grid) {
+    const int blocks_per_region = (1 << 20) / BOX_BYTES;
+    CUtensorMap m;
+    cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(blocks_per_region) * BOX_ROWS};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(BOX_ROWS)};
+    cuuint32_t es[2] = {1, 1};
+    enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const int iters = 4096, smem = P * S * BOX_BYTES + 1024;
+    cudaFuncSetAttribute(k_stream_multi<S, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_stream_multi<S, P><<<grid, 32 * P, smem>>>(m, iters, blocks_per_region);
+    cudaEventRecord(e0);
+    k_stream_multi<S, P><<<grid, 32 * P, smem>>>(m, iters, blocks_per_region);
+    cudaEventRecord(e1);
+    cudaDeviceSynchronize();
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double gbs = static_cast<double>(grid) * iters * BOX_BYTES / (ms * 1e-3) / 1e9;
+    std::printf("{\"multi_producer\": %d, \"stages_each\": %d, \"grid\": %d, \"kernel_GBps\": %.0f, \"per_SM_GBps\": %.1f, \"err\": \"%s\"}\n",
+                P, S, grid, gbs, gbs / 148, cudaGetErrorString(cudaGetLastError()));
     std::fflush(stdout);
 }
 
@@ -206,16 +275,20 @@ int main() {
     cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
     EncodeFn enc = reinterpret_cast<EncodeFn>(fn);
     void* buf;
-    cudaMalloc(&buf, 148ull << 20);
-    cudaMemset(buf, 0, 148ull << 20);
+    cudaMalloc(&buf, 448ull << 20);
+    cudaMemset(buf, 0, 448ull << 20);
     unsigned long long* d_out;
-    cudaMalloc(&d_out, 296 * sizeof(unsigned long long));
+    cudaMalloc(&d_out, 1024 * sizeof(unsigned long long));
     run<4, 1>(enc, buf, 0, 148, d_out);
     run<6, 1>(enc, buf, 0, 148, d_out);
-    run<6, 2>(enc, buf, 6, 148, d_out);
-    run<4, 2>(enc, buf, 10, 148, d_out);
-    run<6, 2>(enc, buf, 10, 148, d_out);
-    run<10, 2>(enc, buf, 10, 148, d_out);
-    run<6, 2>(enc, buf, 7, 148, d_out);
+    // two CTAs per SM (296 CTAs, 6 x 16 KB each): is ~27 B/clk a per-SM or a per-issuer limit?
+    run<6, 1>(enc, buf, 0, 296, d_out);
+    run<4, 1>(enc, buf, 0, 444, d_out);
+    run<6, 1>(enc, buf, 2, 296, d_out);
+    run_multi<8, 1>(enc, buf, 148);
+    run_multi<4, 2>(enc, buf, 148);
+    run_multi<6, 2>(enc, buf, 148);
+    run_multi<3, 4>(enc, buf, 148);
+    run_multi<2, 4>(enc, buf, 148);
     return 0;
 }
