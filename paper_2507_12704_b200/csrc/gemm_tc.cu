@@ -740,7 +740,10 @@ struct FfnCfg {
     static constexpr int W2_PER_SLOT = SLOT / W2_BLK;
     static constexpr int S1 = KB1 / W1_PER_SLOT;          // slots per FFN1 chunk
     static constexpr int S2 = 2 / W2_PER_SLOT;            // slots per FFN2 chunk (2 k-blocks of 64)
-    static constexpr int STAGES = D == 256 ? 5 : 7;       // weight blocks in flight (L2 latency)
+#ifndef DCAT_FFN_STAGES256
+#define DCAT_FFN_STAGES256 5
+#endif
+    static constexpr int STAGES = D == 256 ? DCAT_FFN_STAGES256 : 7;  // weight blocks in flight (L2 latency)
     static constexpr int A_TILE = KB1 * 16384;
     static constexpr int H_BUF = 2 * 16384;  // [128 x CH] bf16 = 2 SW128 k-blocks
     // warp 0: TMA producer + TMEM allocator, warp 1: MMA issuer (leader CTA), warps 2..17:
