@@ -5,6 +5,9 @@ product):
     ncu -i call.ncu-rep --page raw --csv > call_raw.csv
     python tools/kernel_table.py call_raw.csv > profiles/r01_kernels.md
 
+With `--calls 3` the last complete call is tabulated (the second one: captured into the cached
+graph and launched from it).
+
 One row per launch: ncu duration (serialised, cold L2: compare shares, not absolutes), DRAM bytes,
 achieved DRAM GB/s and its fraction of the measured HBM peak, tensor-pipe utilisation, issue
 utilisation. Launch labels follow run_dcat's order (PinFM-base, 4 layers)."""
@@ -21,6 +24,13 @@ while "Kernel Name" not in raw[i]:
 h = raw[i]
 rows = [r for r in raw[i + 2:] if len(r) == len(h) and r[h.index("Kernel Name")]]
 col = {n: k for k, n in enumerate(h)}
+# several calls in the capture: keep the last one (calls start at the dedup's first kernel, k_span;
+# a steady-state call replays the cached graphs)
+starts = [k for k, r in enumerate(rows) if "k_span(" in r[col["Kernel Name"]]] + [len(rows)]
+calls = [rows[a:b] for a, b in zip(starts[:-1], starts[1:])]
+complete = [c for c in calls if any("k_scatter" in r[col["Kernel Name"]] for r in c)]
+if complete:  # the last call that ran to its end (a capture can stop mid-call)
+    rows = complete[-1]
 peaks = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
 hbm_peak = 6545.6
 try:
@@ -41,7 +51,8 @@ def f(r, name):
 
 def short(name):
     name = re.sub(r"\(.*", "", name)
-    name = name.replace("void ", "").replace("dcat::<unnamed>::", "").replace("__nv_bfloat16", "bf16")
+    name = name.replace("void ", "").replace("__nv_bfloat16", "bf16")
+    name = re.sub(r"^.*?::(?=k_)", "", name)  # "dcat::<unnamed>::" / "unnamed>::" (ncu versions)
     return name.strip()
 
 
@@ -58,7 +69,7 @@ labels = iter(["ctx." + x for x in ctx] + ["cross." + x for x in cross])
 
 print("# Round 1 — every kernel of one PinFM-base call under `ncu --set full`\n")
 print("B200, 1000 users x 128 candidates, L = 256, 4 layers, d = 256, 8 heads; "
-      "`tools/profile_step.py --calls 1`, `--clock-control none`. ncu serialises launches and runs "
+      "`tools/profile_step.py --calls 3` (the last complete call, launched from the cached graph), `--clock-control none`. ncu serialises launches and runs "
       "each one cold, so the durations are per-launch and the step's real time is in `bench.py`; "
       f"DRAM % is against the measured HBM peak {hbm_peak:.1f} GB/s (MEASURED_PEAKS.json).\n")
 print("| # | stage | kernel | us | DRAM MB (r+w) | DRAM GB/s | % HBM peak | tensor pipe % | issue % |")

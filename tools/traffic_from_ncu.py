@@ -40,8 +40,16 @@ def f(r, name, scale=1.0):
         return None
 
 
+body = rows[2:]
+# several calls in the capture: keep the last complete one (it starts at the dedup's k_span and ends
+# with k_scatter; a capture can stop mid-call)
+starts = [k for k, r in enumerate(body) if len(r) == len(h) and "k_span(" in r[col["Kernel Name"]]] + [len(body)]
+calls = [body[a:b] for a, b in zip(starts[:-1], starts[1:])]
+complete = [c for c in calls if any(len(r) == len(h) and "k_scatter" in r[col["Kernel Name"]] for r in c)]
+if complete:
+    body = complete[-1]
 launches = []
-for k, r in enumerate(rows[2:]):
+for k, r in enumerate(body):
     if not r or len(r) != len(h) or not r[col["Kernel Name"]]:
         continue
     if not any(x in r[col["Kernel Name"]] for x in ("k_gemm_tc", "k_ffn_tc")):
