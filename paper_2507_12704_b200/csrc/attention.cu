@@ -102,7 +102,7 @@ struct FlashCfg {
 // or 8 (2 warps x 2 m-tiles, 128 registers)
 template <int DH, bool CAUSAL, int WARPS, int RT>
 constexpr int flash_min_blocks() {
-    return DH <= 32 ? (CAUSAL ? (RT == 2 ? 512 / (WARPS * 32) : 6) : 4) : (CAUSAL ? 4 : 2);
+    return DH <= 32 ? (RT == 2 ? 512 / (WARPS * 32) : (CAUSAL ? 6 : 4)) : (CAUSAL ? 4 : 2);
 }
 template <int DH, bool CAUSAL, int WARPS, int RT>
 __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS, RT>()) k_flash(AttnArgs p) {
@@ -466,7 +466,7 @@ void launch_flash(const AttnArgs& a, cudaStream_t s) {
     constexpr int RT = DH <= 32 ? DCAT_XRT : 1;
     constexpr int CRT = DH <= 32 ? DCAT_CRT : 1;
     if (a.causal) launch_flash_t<DH, true, kCtxTile / (16 * CRT), CRT>(a, s);
-    else launch_flash_t<DH, false, 8 / RT, RT>(a, s);
+    else launch_flash_t<DH, false, (DH <= 32 ? kCrossTile : 128) / (16 * RT), RT>(a, s);
 }
 
 }  // namespace

@@ -1132,7 +1132,7 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         if (B == 0) return DCAT_OK;
         m->vt = use_tc_attention(m, f32);
         m->tile_ctx = m->vt ? 128 : kCtxTile;
-        m->tile_cross = 128;
+        m->tile_cross = m->vt ? 128 : kCrossTile;
         int t0 = mark(m, s);
         Staged sb = stage_batch(m, batch, device,
                                 ft->variant == DCAT_VARIANT_AUX || ft->variant == DCAT_VARIANT_AUXLT, s, true);

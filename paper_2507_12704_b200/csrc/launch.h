@@ -41,6 +41,11 @@ __host__ __device__ __forceinline__ int seq_tokens(const DedupIn& in, int valid)
 #define DCAT_CTX_BQ 64
 #endif
 constexpr int kCtxTile = DCAT_CTX_BQ;
+// candidate rows per crossing-attention tile (mma.sync kernel: 2 m-tiles of 16 rows per warp)
+#ifndef DCAT_CROSS_BQ
+#define DCAT_CROSS_BQ 128
+#endif
+constexpr int kCrossTile = DCAT_CROSS_BQ;
 
 struct Tile {  // one attention work item: <= BM query rows of one unique
     int q0, nq;     // first query row, number of query rows
