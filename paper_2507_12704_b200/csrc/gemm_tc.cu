@@ -723,6 +723,9 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
 // then x_mid = acc2 + bo stays in acc2 as the FFN residual and LN2(x_mid) is written by the
 // epilogue warps straight into the A tile as the FFN1 operand. x_mid and LN2(x_mid) never
 // reach HBM: 384 KB less traffic per 128-row tile than the o-projection GEMM + FFN pair.
+#ifndef DCAT_FFN_PAIR_N
+#define DCAT_FFN_PAIR_N 1
+#endif
 template <int D, int CL, bool TAIL = false>
 struct FfnCfg {
     static_assert(!TAIL || (CL == 1 && D >= 128), "fused layer tail: single CTA, D = 128 or 256");
@@ -740,10 +743,16 @@ struct FfnCfg {
     static constexpr int W2_PER_SLOT = SLOT / W2_BLK;
     static constexpr int S1 = KB1 / W1_PER_SLOT;          // slots per FFN1 chunk
     static constexpr int S2 = 2 / W2_PER_SLOT;            // slots per FFN2 chunk (2 k-blocks of 64)
+    // single CTA, D = 256: the two 128-row N halves of a W2 / Wo k-block are consecutive ring slots
+    // and, with an even ring, always adjacent in smem (every phase pushes an even number of
+    // slots), so one N = 256 MMA reads both: the A operand (H / A_o) is read from smem once per
+    // 256 output columns instead of twice
+    static constexpr bool PAIR_N = CL == 1 && D == 256 && DCAT_FFN_PAIR_N;
 #ifndef DCAT_FFN_STAGES256
-#define DCAT_FFN_STAGES256 5
+#define DCAT_FFN_STAGES256 (DCAT_FFN_PAIR_N ? 4 : 5)
 #endif
     static constexpr int STAGES = D == 256 ? DCAT_FFN_STAGES256 : 7;  // weight blocks in flight (L2 latency)
+    static_assert(!PAIR_N || STAGES % 2 == 0, "paired N halves need an even ring");
     static constexpr int A_TILE = KB1 * 16384;
     static constexpr int H_BUF = 2 * 16384;  // [128 x CH] bf16 = 2 SW128 k-blocks
     // warp 0: TMA producer + TMEM allocator, warp 1: MMA issuer (leader CTA), warps 2..17:
@@ -987,6 +996,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
         if (lane == 0 && rank == 0) {
             constexpr uint32_t idesc1 = ptx::idesc_bf16(128 * CL, C::CH);
             constexpr uint32_t idesc2 = ptx::idesc_bf16(128 * CL, C::NW2);
+            constexpr uint32_t idesc_n2 = ptx::idesc_bf16(128, D);  // PAIR_N: N = 256 over two slots
             uint32_t it = 0, c1 = 0, c2 = 0, i = 0;
             const uint32_t a_base = ptx::smem_u32(sA), h_base = ptx::smem_u32(sH), r_base = ptx::smem_u32(ring);
             auto mma = [&](uint32_t d, uint32_t a, uint32_t b, uint32_t idesc, uint32_t acc) {
@@ -1032,15 +1042,28 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                     wait_lead(&acc1_empty[(c1 + 1) & 1], (((c1 + 1) >> 1) & 1) ^ 1);
                     resid_to(T_ACC1);
                     ptx::tc_fence_after();
-                    for (int kb = 0; kb < C::KB1; kb++)
-                        for (int nh = 0; nh < D / C::NW2; nh++, it++) {
-                            const uint32_t s = next_slot();
+                    for (int kb = 0; kb < C::KB1; kb++) {
+                        if constexpr (C::PAIR_N) {  // both N halves (adjacent slots) in one N = 256 MMA
+                            const uint32_t s0 = next_slot();
+                            it++;
+                            const uint32_t s1 = next_slot();
+                            it++;
 #pragma unroll
                             for (int k = 0; k < 4; k++)
-                                mma(T_ACC1 + nh * C::NW2, a_base + kb * 16384 + k * 32, r_base + s * C::SLOT + k * 32,
-                                    idesc2, 1u);
-                            commit(&empty[s]);
+                                mma(T_ACC1, a_base + kb * 16384 + k * 32, r_base + s0 * C::SLOT + k * 32, idesc_n2, 1u);
+                            commit(&empty[s0]);
+                            commit(&empty[s1]);
+                        } else {
+                            for (int nh = 0; nh < D / C::NW2; nh++, it++) {
+                                const uint32_t s = next_slot();
+#pragma unroll
+                                for (int k = 0; k < 4; k++)
+                                    mma(T_ACC1 + nh * C::NW2, a_base + kb * 16384 + k * 32,
+                                        r_base + s * C::SLOT + k * 32, idesc2, 1u);
+                                commit(&empty[s]);
+                            }
                         }
+                    }
                     commit(o_full);
                     ptx::mbar_wait(a2_full, i & 1);  // x_mid in acc2, LN2 rows in the A tile, acc1 free
                     ptx::tc_fence_after();
@@ -1073,7 +1096,20 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                         FFN_EV(2, jj);
                         if (!TAIL && jj == 0) resid_to_acc2();
                         ptx::tc_fence_after();
-                        if constexpr (CL == 1 && C::NW2 < D) {
+                        if constexpr (C::PAIR_N) {
+                            for (int kb2 = 0; kb2 < 2; kb2++) {
+                                const uint32_t s0 = next_slot();
+                                it++;
+                                const uint32_t s1 = next_slot();
+                                it++;
+#pragma unroll
+                                for (int k = 0; k < 4; k++)
+                                    mma(T_ACC2, h_base + hb * C::H_BUF + kb2 * 16384 + k * 32,
+                                        r_base + s0 * C::SLOT + k * 32, idesc_n2, 1u);
+                                commit(&empty[s0]);
+                                commit(&empty[s1]);
+                            }
+                        } else if constexpr (CL == 1 && C::NW2 < D) {
                             for (int kb2 = 0; kb2 < 2; kb2++)
                                 for (int nh = 0; nh < D / C::NW2; nh++, it++) {
                                     const uint32_t s = next_slot();
