@@ -753,6 +753,7 @@ struct FfnCfg {
 #endif
     static constexpr int STAGES = D == 256 ? DCAT_FFN_STAGES256 : 7;  // weight blocks in flight (L2 latency)
     static_assert(!PAIR_N || STAGES % 2 == 0, "paired N halves need an even ring");
+    static_assert(!PAIR_N || CH * 64 * 2 == SLOT, "paired FFN1: one [CH x 64] W1 block per slot");
     static constexpr int A_TILE = KB1 * 16384;
     static constexpr int H_BUF = 2 * 16384;  // [128 x CH] bf16 = 2 SW128 k-blocks
     // warp 0: TMA producer + TMEM allocator, warp 1: MMA issuer (leader CTA), warps 2..17:
@@ -971,7 +972,12 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                         for (int nh = 0; nh < D / C::NW2; nh++) push(&tmWo, kb * 64, nh * C::NW2, 1, C::SLOT);
                 }
                 for (int j = 0; j < nch + LA; j++) {  // same order as the MMA issuer
-                    if (j < nch)
+                    if (C::PAIR_N && j < nch && (j & 1) == 0) {  // W1 blocks of chunks j, j + 1 per k-block
+                        for (int kb = 0; kb < C::KB1; kb++) {
+                            push(&tmW1, kb * 64, chunk(j) * C::CH, 1, C::SLOT);
+                            push(&tmW1, kb * 64, chunk(j + 1) * C::CH, 1, C::SLOT);
+                        }
+                    } else if (!C::PAIR_N && j < nch)
                         for (int p = 0; p < C::S1; p++)
                             push(&tmW1, p * C::W1_PER_SLOT * 64, chunk(j) * C::CH + static_cast<int>(rank) * C::W1_ROWS,
                                  C::W1_PER_SLOT, C::W1_BLK);
@@ -997,6 +1003,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
             constexpr uint32_t idesc1 = ptx::idesc_bf16(128 * CL, C::CH);
             constexpr uint32_t idesc2 = ptx::idesc_bf16(128 * CL, C::NW2);
             constexpr uint32_t idesc_n2 = ptx::idesc_bf16(128, D);  // PAIR_N: N = 256 over two slots
+            constexpr uint32_t idesc_f1p = ptx::idesc_bf16(128, 2 * C::CH);  // PAIR_N: two FFN1 chunks
             uint32_t it = 0, c1 = 0, c2 = 0, i = 0;
             const uint32_t a_base = ptx::smem_u32(sA), h_base = ptx::smem_u32(sH), r_base = ptx::smem_u32(ring);
             auto mma = [&](uint32_t d, uint32_t a, uint32_t b, uint32_t idesc, uint32_t acc) {
@@ -1069,7 +1076,32 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                     ptx::tc_fence_after();
                 }
                 for (int j = 0; j < nch + LA; j++) {
-                    if (j < nch) {  // FFN1 chunk j -> acc1[b]
+                    if (C::PAIR_N && j < nch && (j & 1) == 0) {
+                        // FFN1 of chunks j, j + 1 as N = 256 MMAs into both acc1 buffers: per k-block
+                        // the two chunks' W1 blocks sit in adjacent slots (A read once per 256 columns)
+                        if (!TAIL || j >= 2) {
+                            wait_lead(&acc1_empty[c1 & 1], ((c1 >> 1) & 1) ^ 1);
+                            wait_lead(&acc1_empty[(c1 + 1) & 1], (((c1 + 1) >> 1) & 1) ^ 1);
+                        }
+                        FFN_EV(1, j);
+                        ptx::tc_fence_after();
+                        for (int kb = 0; kb < C::KB1; kb++) {
+                            const uint32_t s0 = next_slot();
+                            it++;
+                            const uint32_t s1 = next_slot();
+                            it++;
+#pragma unroll
+                            for (int k = 0; k < 4; k++)
+                                mma(T_ACC1, a_base + kb * 16384 + k * 32, r_base + s0 * C::SLOT + k * 32, idesc_f1p,
+                                    (kb | k) != 0);
+                            commit(&empty[s0]);
+                            commit(&empty[s1]);
+                        }
+                        commit(&acc1_full[c1 & 1]);
+                        commit(&acc1_full[(c1 + 1) & 1]);
+                        c1 += 2;
+                        if (j + 1 == nch - 1) commit(a_empty);  // the A tiles are free once these complete
+                    } else if (!C::PAIR_N && j < nch) {  // FFN1 chunk j -> acc1[b]
                         const int b = c1 & 1;
                         if (!TAIL || j >= 2) wait_lead(&acc1_empty[b], ((c1 >> 1) & 1) ^ 1);
                         FFN_EV(1, j);
