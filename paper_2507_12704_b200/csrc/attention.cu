@@ -102,7 +102,11 @@ struct FlashCfg {
 // or 8 (2 warps x 2 m-tiles, 128 registers)
 template <int DH, bool CAUSAL, int WARPS, int RT>
 constexpr int flash_min_blocks() {
+#ifdef DCAT_FLASH_THREADS_PER_SM  // experiments: resident threads per SM the register budget targets
+    return DH <= 32 ? (RT == 2 ? DCAT_FLASH_THREADS_PER_SM / (WARPS * 32) : (CAUSAL ? 6 : 4)) : (CAUSAL ? 4 : 2);
+#else
     return DH <= 32 ? (RT == 2 ? 512 / (WARPS * 32) : (CAUSAL ? 6 : 4)) : (CAUSAL ? 4 : 2);
+#endif
 }
 template <int DH, bool CAUSAL, int WARPS, int RT>
 __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS, RT>()) k_flash(AttnArgs p) {
