@@ -126,7 +126,7 @@ struct dcat_model {
     // workspace
     Buf b_in[8];
     Buf b_dd[24];
-    Buf b_act[20];
+    Buf b_act[28];
     Buf b_kv;
     Buf b_aux;
     Buf b_out[3];
@@ -150,6 +150,12 @@ struct dcat_model {
     // the candidate gather, which waits on cand_ready)
     cudaStream_t side = nullptr;
     cudaEvent_t side_start = nullptr, cand_ready = nullptr;
+    // two-stream scoring pass: the crossing pass runs on xs beside the context pass; crossing
+    // layer l waits only for kv_ev[l] (context layer l's K / V cache written), and xs joins back
+    // before the head (small batches; see run_dcat).
+    cudaStream_t xs = nullptr;
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+    std::vector<cudaEvent_t> kv_ev;
     // the dedup / plan launch sequence as a CUDA graph, re-captured when its arguments change
     struct DedupKey {
         DedupIn in;
@@ -174,6 +180,10 @@ struct dcat_model {
         if (side_start) cudaEventDestroy(side_start);
         if (cand_ready) cudaEventDestroy(cand_ready);
         if (side) cudaStreamDestroy(side);
+        if (xs) cudaStreamDestroy(xs);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        if (join_ev) cudaEventDestroy(join_ev);
+        for (auto e : kv_ev) cudaEventDestroy(e);
         if (dd_exec) cudaGraphExecDestroy(dd_exec);
         if (run_exec) cudaGraphExecDestroy(run_exec);
         if (cap) cudaStreamDestroy(cap);
@@ -588,6 +598,8 @@ void attn(dcat_model* m, const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cud
 //   AuxLt: the learnable token is appended to every unique's context (its K/V enter the cache,
 //     its final row through phi_out is the first selector) and candidates cross at position n + 1;
 //     the reference computes the same per example (:428-431), here once per unique.
+constexpr int64_t kDualStreamMaxRows = 65536;  // context / candidate rows (padded) below which run_dcat forks
+
 template <typename T>
 void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_finetune_config& ft, float* logits,
               float* mlogits, float* h_cand, cudaStream_t s) {
@@ -611,6 +623,32 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     int32_t* tok_unique = m->b_dd[22].get<int32_t>(std::max<int64_t>(T_ctx, 1));
     build_tiles(sb.in, o, b_u, m->tile_ctx, m->tile_cross, ctx_tiles, cross_tiles, tok_unique, s);
     m->stats.kernel_launches += 2;
+    // Two streams pay where the pass is launch-bound (small batches: tiny config 0.236 -> 0.204 ms).
+    // At full-machine tile counts the persistent kernels already hold all SMs and the streams only
+    // interleave (PinFM-base +0.4 %, high-fanout -2.3 %, low-dedup -1 %), so the default is by size;
+    // DCAT_DUAL_STREAM=0 / 1 forces it.
+    static const char* dual_env = getenv("DCAT_DUAL_STREAM");
+    const bool dual_fit = dual_env ? dual_env[0] == '1' : Rr <= kDualStreamMaxRows;
+    const bool dual = dual_fit && !(ft.variant == DCAT_VARIANT_LITE_MEAN || ft.variant == DCAT_VARIANT_LITE_LAST);
+    std::vector<char> kv_done(nl, 0);  // kv_ev[l] recorded in this call
+    if (dual) {
+        if (!m->xs) {
+            DCAT_CUDA_CHECK(cudaStreamCreateWithFlags(&m->xs, cudaStreamNonBlocking));
+            DCAT_CUDA_CHECK(cudaEventCreateWithFlags(&m->fork_ev, cudaEventDisableTiming));
+            DCAT_CUDA_CHECK(cudaEventCreateWithFlags(&m->join_ev, cudaEventDisableTiming));
+        }
+        while (static_cast<int>(m->kv_ev.size()) < nl) {
+            cudaEvent_t e;
+            DCAT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            m->kv_ev.push_back(e);
+        }
+        DCAT_CUDA_CHECK(cudaEventRecord(m->fork_ev, s));  // plan + tiles are ready
+    }
+    auto kv_written = [&](int l) {
+        if (!dual) return;
+        DCAT_CUDA_CHECK(cudaEventRecord(m->kv_ev[l], s));
+        kv_done[l] = 1;
+    };
     // V cache layout: V^T [d][Tp] (keys contiguous) for the tcgen05 attention, else rows [Tp][d]
     const bool vt = m->vt;
     const int ldvt = vt ? static_cast<int>(Tp) : 0;
@@ -678,6 +716,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
                 e.out_trans[1] = vt;
                 e.seg_cols = d;
                 gemm<T>(m, "gemm.ctx.kv", A.a, d, L.qkv, d, 2 * d, M, e, A.tmp, s);
+                kv_written(l);
                 break;
             }
             // layer_forward (model.cpp:336-398); K, V go straight to the cache
@@ -691,6 +730,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             e.out_trans[2] = vt;
             e.seg_cols = d;
             gemm<T>(m, "gemm.ctx.qkv", A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
+            kv_written(l);
             AttnArgs aa{A.q,     d,  K_l(l), V_l(l), d, ldvt, nullptr, nullptr, 0, A.ctx, d, ctx_tiles, st.ctx_tiles,
                         H,       dh, scale,  1,      c.max_len + 1};
             attn<T>(m, aa, Rr, Tp, s);
@@ -756,6 +796,19 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
 
     // ============ crossing pass (candidate_inputs + cross_forward) ============
     const int M = static_cast<int>(B);
+    const cudaStream_t s_main = s;
+    if (dual) {  // own activation buffers (Rr rows: the attention's TMA maps span Rr), own stream, forked at the plan
+        DCAT_CUDA_CHECK(cudaStreamWaitEvent(m->xs, m->fork_ev, 0));
+        s = m->xs;
+        A.E = m->b_act[20].get<T>(Rr * de);
+        A.h1 = m->b_act[21].get<T>(Rr * d);
+        A.a = m->b_act[22].get<T>(Rr * d);
+        A.q = m->b_act[23].get<T>(Rr * d);
+        A.ctx = m->b_act[24].get<T>(Rr * d);
+        A.f1 = m->b_act[25].get<T>(Rr * F);
+        A.x = m->b_act[26].get<float>(Rr * d);
+        A.tmp = f32 ? m->b_act[27].get<float>(Rr * std::max(3 * d, std::max(F, m->hidden))) : nullptr;
+    }
     CandParams cp{sb.candidate, sb.age, sb.aux, m->aux_proj, m->d_aux,
                   ft.variant == DCAT_VARIANT_AUX || ft.variant == DCAT_VARIANT_AUXLT,
                   ft.max_events, ft.fresh_days, ft.mid_days, m->d_module, kh, auxlt ? 1 : 0};
@@ -788,11 +841,17 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         e.out_ld[0] = e.out_ld[1] = e.out_ld[2] = d;
         e.seg_cols = d;
         gemm<T>(m, "gemm.cross.qkv", A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
+        if (dual && kv_done[l]) DCAT_CUDA_CHECK(cudaStreamWaitEvent(s, m->kv_ev[l], 0));
         AttnArgs aa{A.q, d,     K_l(l), V_l(l), d, ldvt, A.kself, A.vself, d, A.ctx, d, cross_tiles, st.cross_tiles,
                     H,   dh,    scale,  0,      c.max_len + 1};
         attn<T>(m, aa, Rr, std::max<int64_t>(Tp, 1), s);
         layer_tail<T>(m, "cross", A.ctx, L, l, M, A.x, A.a, l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr,
                       l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // last: copy for phi_out
+    }
+    if (dual) {  // join: the rest reads the context pass's selectors and goes out on the caller's stream
+        DCAT_CUDA_CHECK(cudaEventRecord(m->join_ev, s));
+        DCAT_CUDA_CHECK(cudaStreamWaitEvent(s_main, m->join_ev, 0));
+        s = s_main;
     }
     // phi_out (dcat.cpp:266) + module head (finetune.cpp:317-323)
     e = base_epi(m, EPI_BIAS);
