@@ -108,7 +108,11 @@ constexpr int flash_min_blocks() {
     return DH <= 32 ? (RT == 2 ? 512 / (WARPS * 32) : (CAUSAL ? 6 : 4)) : (CAUSAL ? 4 : 2);
 #endif
 }
-template <int DH, bool CAUSAL, int WARPS, int RT>
+// SKIP: warps whose rows all lie past the tile's queries only stage K/V. Instantiated for sparse
+// crossing tiles (a unique with few candidates fills a fraction of the 128 rows: low-dedup has 4
+// per tile, attention 10.0 -> 7.2 ms); full tiles run the variant without the branch, which
+// measured 1-2 % faster on them.
+template <int DH, bool CAUSAL, int WARPS, int RT, bool SKIP>
 __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS, RT>()) k_flash(AttnArgs p) {
     // keys per online-softmax step: the context kernel keeps whole 64-key blocks (6 CTAs/SM at
     // 80 registers), the crossing kernel halves them (register footprint)
@@ -242,6 +246,7 @@ __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS
             ldsm_x4(qf[t][kk], sQ + 2 * (row * LD + col));
         }
 
+    const bool warp_idle = rw[0] >= tile.nq;  // warp-uniform
     for (int blk = 0; blk < nblk; blk++) {
         const int buf = blk % NST;
         cp_async_wait<NST - 2>();  // block blk has landed (the NST - 2 newer groups may be in flight)
@@ -254,6 +259,7 @@ __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS
             constexpr int NJ = SUB / 8;                // n-tiles of S
             const int kbase = blk * BKV + sub * SUB;
             if (kbase >= tile.nkv) break;  // uniform across the CTA
+            if (SKIP && warp_idle) continue;  // idle warp: K/V staging only
             // causal: keys past this warp's last query row are masked for all its rows (warp-uniform)
             if (CAUSAL && kbase > tile.qloc + rw[RT - 1] + 15) continue;
             float s[RT][NJ][4];
@@ -451,16 +457,16 @@ void launch_simt(const AttnArgs& a, cudaStream_t s) {
     DCAT_LAUNCH_CHECK();
 }
 
-template <int DH, bool CAUSAL, int WARPS, int RT>
+template <int DH, bool CAUSAL, int WARPS, int RT, bool SKIP = false>
 void launch_flash_t(const AttnArgs& a, cudaStream_t s) {
     using C = FlashCfg<DH, CAUSAL, WARPS, RT>;
     static std::once_flag once;
     std::call_once(once, [] {
-        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_flash<DH, CAUSAL, WARPS, RT>,
+        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_flash<DH, CAUSAL, WARPS, RT, SKIP>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
     });
     const dim3 grid(static_cast<unsigned>(a.n_tiles) * static_cast<unsigned>(a.n_heads));
-    k_flash<DH, CAUSAL, WARPS, RT><<<grid, WARPS * 32, C::SMEM, s>>>(a);
+    k_flash<DH, CAUSAL, WARPS, RT, SKIP><<<grid, WARPS * 32, C::SMEM, s>>>(a);
     DCAT_LAUNCH_CHECK();
 }
 
@@ -470,7 +476,8 @@ void launch_flash(const AttnArgs& a, cudaStream_t s) {
     constexpr int RT = DH <= 32 ? DCAT_XRT : 1;
     constexpr int CRT = DH <= 32 ? DCAT_CRT : 1;
     if (a.causal) launch_flash_t<DH, true, kCtxTile / (16 * CRT), CRT>(a, s);
-    else launch_flash_t<DH, false, (DH <= 32 ? kCrossTile : 128) / (16 * RT), RT>(a, s);
+    else if (a.sparse_tiles) launch_flash_t<DH, false, (DH <= 32 ? kCrossTile : 128) / (16 * RT), RT, true>(a, s);
+    else launch_flash_t<DH, false, (DH <= 32 ? kCrossTile : 128) / (16 * RT), RT, false>(a, s);
 }
 
 }  // namespace

@@ -844,6 +844,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         if (dual && kv_done[l]) DCAT_CUDA_CHECK(cudaStreamWaitEvent(s, m->kv_ev[l], 0));
         AttnArgs aa{A.q, d,     K_l(l), V_l(l), d, ldvt, A.kself, A.vself, d, A.ctx, d, cross_tiles, st.cross_tiles,
                     H,   dh,    scale,  0,      c.max_len + 1};
+        aa.sparse_tiles = B < static_cast<int64_t>(st.cross_tiles) * (m->tile_cross / 2);
         attn<T>(m, aa, Rr, std::max<int64_t>(Tp, 1), s);
         layer_tail<T>(m, "cross", A.ctx, L, l, M, A.x, A.a, l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr,
                       l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // last: copy for phi_out

@@ -1,6 +1,7 @@
 """Runs every BASELINE.json config on one B200: throughput (device-resident, a few
 steps) and parity against the CPU oracle on a small user sample of the same dims.
-Usage: python tools/run_configs.py [config ...]"""
+Usage: python tools/run_configs.py [--stages] [config ...]
+--stages adds one profiled call per config (stage times in ms, top 12 by time)."""
 import json
 import os
 import sys
@@ -20,7 +21,7 @@ from paper_2507_12704_b200.synth import CONFIGS, make_batch  # noqa: E402
 PER_GPU_USERS = {"long-seq": 256}
 
 
-def main(names):
+def main(names, stages=False):
     orc = pyoracle.oracle()
     out = {}
     for name in names:
@@ -55,6 +56,11 @@ def main(names):
         ms = ev[0].elapsed_time(ev[1]) / K
         out[name] = {"users": U, "cands": C, "L": L, "rows": host.n_rows, "ms_per_step": round(ms, 3),
                      "cand_per_s": round(host.n_rows / ms * 1e3, 1), "parity": par}
+        if stages:
+            m.rank_forward_batch(dev, ft, profile=True)
+            torch.cuda.synchronize()
+            st = sorted(m.stage_times().items(), key=lambda kv: -kv[1])[:12]
+            out[name]["stages_ms"] = {k: round(v, 3) for k, v in st}
         print(name, json.dumps(out[name]), flush=True)
         del m, dev
         torch.cuda.empty_cache()
@@ -62,4 +68,5 @@ def main(names):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["tiny", "pinfm-base", "low-dedup", "high-fanout", "long-seq"])
+    args = [a for a in sys.argv[1:] if a != "--stages"]
+    main(args or ["tiny", "pinfm-base", "low-dedup", "high-fanout", "long-seq"], stages="--stages" in sys.argv)
