@@ -165,6 +165,23 @@ def test_bf16_pinfm_base_sample_vs_oracle(api, orc):
     assert rel_err(lf, rl) <= 1e-4
 
 
+@pytest.mark.parametrize("U,C", [(3, 128), (40, 3)])
+def test_bf16_crossing_tile_fill(api, orc, U, C):
+    """Full crossing tiles (128 candidates of one unique: the k_flash variant without the idle-warp
+    branch) and sparse ones (3 per 128-row tile: idle warps only stage K/V), both against the oracle."""
+    spec = ModelSpec(d_model=256, n_layers=2, n_heads=8, mlp_ratio=4, max_len=66, d_emb=256)
+    w = orc.init_weights(spec, 42, table=(8, 4096, 32, 7, 0.05), head_seed=11)
+    b = make_batch(U, C, 64, seed=21, ragged=True, layout="grouped")
+    ft = FinetuneSpec(max_events=64)
+    m = api.DcatModel(w)
+    logits, mlog, h = m.rank_forward_batch(b, ft, want_h=True)
+    rl, rm, _, rh = orc.rank_forward_batch(w, ft, b)
+    assert float(np.abs(h - rh).max()) <= 3e-2
+    assert cos_min(h, rh) >= 0.999
+    assert rel_err(logits, rl) <= 3e-2
+    assert rel_err(mlog, rm) <= 3e-2
+
+
 @pytest.mark.parametrize("d", [128, 256])
 def test_fused_layer_tail(api, orc, d, monkeypatch):
     """The fused layer tail (o-projection + residual + LN2 + FFN + residual + next LN1 in one
