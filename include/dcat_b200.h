@@ -201,6 +201,12 @@ typedef struct dcat_call_stats {
 } dcat_call_stats;
 int dcat_last_stats(dcat_model* m, dcat_call_stats* out);
 
+/* Test instrumentation: device counters of a model created with the environment variable
+ * DCAT_DEBUG_COUNTERS set (none otherwise). out[0] = online-softmax rescale events of the causal
+ * (context) attention kernel, out[1] = of the crossing kernel. Reads and resets them; returns the
+ * number of counters written (0 when the model has none). */
+int dcat_debug_counters(dcat_model* m, uint64_t* out, int32_t cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,12 +47,14 @@ def lib() -> C.CDLL:
         L.dcat_debug_kv.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, P(C.c_int32)]
         L.dcat_stage_times.argtypes = [C.c_void_p, P(C.c_char_p), P(C.c_float), C.c_int32]
         L.dcat_last_stats.argtypes = [C.c_void_p, P(CallStatsC)]
+        L.dcat_debug_counters.argtypes = [C.c_void_p, P(C.c_uint64), C.c_int32]
         _lib = L
     return _lib
 
 
 EXPORTS = ("dcat_last_error", "dcat_version", "dcat_model_create", "dcat_model_destroy", "dcat_dedup",
-           "dcat_rank_forward_batch", "dcat_debug_kv", "dcat_stage_times", "dcat_last_stats")
+           "dcat_rank_forward_batch", "dcat_debug_kv", "dcat_stage_times", "dcat_last_stats",
+           "dcat_debug_counters")
 
 
 def _check(rc: int):
@@ -145,6 +147,16 @@ class DcatModel:
             k = names[i].decode()
             out[k] = out.get(k, 0.0) + ms[i]
         return out
+
+    def debug_counters(self) -> dict:
+        """Attention rescale counters since the last read (model created with DCAT_DEBUG_COUNTERS)."""
+        buf = (C.c_uint64 * 8)()
+        n = lib().dcat_debug_counters(self._h, buf, 8)
+        if n < 0:
+            _check(n)
+        if n == 0:
+            raise RuntimeError("model was created without DCAT_DEBUG_COUNTERS")
+        return {"rescale_causal": int(buf[0]), "rescale_cross": int(buf[1])}
 
     def last_stats(self) -> dict:
         s = CallStatsC()

@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(WARPS * 32, flash_min_blocks<DH, CAUSAL, WARPS
                 float& m1 = mx[t][1];
                 const bool grow = (bm0 - m0) * sl2 > LAZY || (bm1 - m1) * sl2 > LAZY;  // -inf - -inf: NaN
                 if (__any_sync(0xffffffffu, grow)) {
+                    if (p.dbg != nullptr && lane == 0) atomicAdd(p.dbg + (CAUSAL ? 0 : 1), 1u);
                     const float nm0 = fmaxf(m0, bm0), nm1 = fmaxf(m1, bm1);
                     const float a0 = nm0 == -INFINITY ? 1.f : ex2((m0 - nm0) * sl2);  // m = -inf -> 0
                     const float a1 = nm1 == -INFINITY ? 1.f : ex2((m1 - nm1) * sl2);

@@ -48,6 +48,8 @@ uint64_t host_mix64(uint64_t x) {
 // replayed while every buffer it captured still exists
 std::atomic<uint64_t> g_alloc_epoch{0};
 
+constexpr int kDebugCounters = 8;
+
 struct Buf {
     void* p = nullptr;
     size_t cap = 0;
@@ -123,6 +125,7 @@ struct dcat_model {
     // status
     Status* st_dev = nullptr;
     Status* st_host = nullptr;
+    unsigned* dbg = nullptr;  // DCAT_DEBUG_COUNTERS at create: device counters (dcat_debug_counters)
     // workspace
     Buf b_in[8];
     Buf b_dd[24];
@@ -733,6 +736,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             kv_written(l);
             AttnArgs aa{A.q,     d,  K_l(l), V_l(l), d, ldvt, nullptr, nullptr, 0, A.ctx, d, ctx_tiles, st.ctx_tiles,
                         H,       dh, scale,  1,      c.max_len + 1};
+            aa.dbg = m->dbg;
             attn<T>(m, aa, Rr, Tp, s);
             layer_tail<T>(m, "ctx", A.ctx, L, l, M, A.x, A.a, l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr,
                           l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // emitted rows: copy
@@ -845,6 +849,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
         AttnArgs aa{A.q, d,     K_l(l), V_l(l), d, ldvt, A.kself, A.vself, d, A.ctx, d, cross_tiles, st.cross_tiles,
                     H,   dh,    scale,  0,      c.max_len + 1};
         aa.sparse_tiles = B < static_cast<int64_t>(st.cross_tiles) * (m->tile_cross / 2);
+        aa.dbg = m->dbg;
         attn<T>(m, aa, Rr, std::max<int64_t>(Tp, 1), s);
         layer_tail<T>(m, "cross", A.ctx, L, l, M, A.x, A.a, l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr,
                       l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // last: copy for phi_out
@@ -1094,6 +1099,11 @@ int dcat_model_create(const dcat_model_config* cfg, const dcat_params* params, c
         DCAT_CUDA_CHECK(cudaMalloc(&m->st_dev, sizeof(Status)));
         m->mem.ptrs.push_back(m->st_dev);
         DCAT_CUDA_CHECK(cudaMallocHost(&m->st_host, sizeof(Status)));
+        if (getenv("DCAT_DEBUG_COUNTERS") != nullptr) {
+            DCAT_CUDA_CHECK(cudaMalloc(&m->dbg, kDebugCounters * sizeof(unsigned)));
+            m->mem.ptrs.push_back(m->dbg);
+            DCAT_CUDA_CHECK(cudaMemset(m->dbg, 0, kDebugCounters * sizeof(unsigned)));
+        }
         *out = m.release();
         return DCAT_OK;
     });
@@ -1371,6 +1381,21 @@ int dcat_stage_times(dcat_model* m, const char** names, float* ms, int32_t cap) 
         n++;
     }
     return n;
+}
+
+int dcat_debug_counters(dcat_model* m, uint64_t* out, int32_t cap) {
+    if (!m || !out) return set_err(DCAT_EINVAL, "null argument");
+    return guarded(m, [&]() -> int {
+        unsigned h[kDebugCounters] = {};
+        if (m->dbg) {
+            DCAT_CUDA_CHECK(cudaDeviceSynchronize());
+            DCAT_CUDA_CHECK(cudaMemcpy(h, m->dbg, sizeof h, cudaMemcpyDeviceToHost));
+            DCAT_CUDA_CHECK(cudaMemset(m->dbg, 0, sizeof h));
+        }
+        const int n = std::min<int>(cap, kDebugCounters);
+        for (int i = 0; i < n; i++) out[i] = h[i];
+        return m->dbg ? n : 0;
+    });
 }
 
 int dcat_last_stats(dcat_model* m, dcat_call_stats* out) {

@@ -205,6 +205,8 @@ struct AttnArgs {
     int causal;                     // 1: context pass, 0: crossing (with self term)
     int max_keys;                   // fp32 path: upper bound on keys per query
     int sparse_tiles;               // crossing: tiles average under half full (k_flash skips idle warps)
+    unsigned* dbg;                  // debug counters (DCAT_DEBUG_COUNTERS) or null: [0] causal / [1] crossing
+                                    // online-softmax rescale events
 };
 void attention_bf16(const AttnArgs& a, cudaStream_t s);
 // tcgen05 attention (attn_tc.cu): bf16, V cache transposed (ldvt > 0); q_rows / kv_rows are the

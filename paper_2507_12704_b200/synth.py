@@ -19,13 +19,20 @@ DAY = 86400.0
 
 def make_batch(U: int, C: int, L: int, seed: int = 1, *, layout: str = "interleaved",
                shared_storage: bool = True, ragged: bool = False, d_aux: int = 0,
-               empty_users: int = 0) -> Batch:
+               empty_users: int = 0, valid=None) -> Batch:
     """U unique users x C candidates. layout: 'interleaved' rep[b] = b % U
     (dcat.cpp:515) or 'grouped' rep[b] = b // C. shared_storage: rows of one
     user point at one event span (CSR); otherwise every row carries its own
-    copy of the events, like a std::vector<RankingExample>."""
+    copy of the events, like a std::vector<RankingExample>. `valid`: explicit
+    per-user event counts (overrides L / ragged)."""
     rng = np.random.default_rng(seed)
-    valid = (rng.integers(1, L + 1, U) if ragged else np.full(U, L)).astype(np.int32)
+    drawn = (rng.integers(1, L + 1, U) if ragged else np.full(U, L)).astype(np.int32)
+    if valid is not None:
+        valid = np.asarray(valid, np.int32)
+        if valid.shape != (U,):
+            raise ValueError("valid must hold one count per user")
+    else:
+        valid = drawn
     if empty_users:
         valid[:empty_users] = 0
     uoff = np.zeros(U, np.int64)

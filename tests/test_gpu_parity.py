@@ -6,7 +6,8 @@ Tolerances (written next to each check):
     bound, max-abs 1e-4 on unit-norm H (test_dcat.cpp:227), rel 1e-4 on logits
     (test_finetune.cpp:359-361).
   * bf16 production mode (bf16 storage, fp32 accumulate): max-abs 3e-2 on H
-    (unit-norm rows), logits within 3e-2 of the logit scale, cosine(H) >= 0.999.
+    (unit-norm rows), logits within 3e-2 of the logit scale, cosine(H) >= 0.999 on
+    the small-d fixtures; 1e-2 at PinFM-base dims (observed ~4.5e-3).
 """
 import os
 
@@ -156,10 +157,11 @@ def test_bf16_pinfm_base_sample_vs_oracle(api, orc):
     m = api.DcatModel(w)
     logits, mlog, h = m.rank_forward_batch(b, ft, want_h=True)
     rl, rm, _, rh = orc.rank_forward_batch(w, ft, b)
-    assert float(np.abs(h - rh).max()) <= 3e-2
+    # PinFM-base, bf16 storage / fp32 accumulate: 1e-2 of the logit scale (observed ~4.5e-3)
+    assert float(np.abs(h - rh).max()) <= 1e-2
     assert cos_min(h, rh) >= 0.999
-    assert rel_err(logits, rl) <= 3e-2
-    assert rel_err(mlog, rm) <= 3e-2
+    assert rel_err(logits, rl) <= 1e-2
+    assert rel_err(mlog, rm) <= 1e-2
     lf, mf, hf = m.rank_forward_batch(b, ft, precision="fp32", want_h=True)
     assert float(np.abs(hf - rh).max()) <= 1e-4
     assert rel_err(lf, rl) <= 1e-4
@@ -270,8 +272,8 @@ def test_bf16_full_size_properties(api, orc):
     rows = np.nonzero(np.isin(np.arange(b.n_rows) % 1000, [0, 511, 999]))[0]
     sub = b.take(rows)
     rl, rm, _, _ = orc.rank_forward_batch(w, ft, sub)
-    assert rel_err(logits[rows], rl) <= 3e-2
-    assert rel_err(mlog[rows], rm) <= 3e-2
+    assert rel_err(logits[rows], rl) <= 1e-2
+    assert rel_err(mlog[rows], rm) <= 1e-2
 
 
 def test_device_resident_io_matches_host(api, orc):
