@@ -383,19 +383,15 @@ uint64_t debug_hash_mask() {
     return (1ull << bits) - 1;
 }
 
-// Attention kernels (bf16 path):
-//   default: attention.cu's mma.sync flash kernel (64-query context tiles, 128 crossing);
-//   DCAT_ATTN_PIPE=1 (head dim 32): attn_pipe.cu, persistent with two tcgen05 pipelines per SM
-//     (ties the flash kernel on the crossing pass, slower on the causal context pass; see
-//     profiles/r01_attention.md);
-//   DCAT_TC_ATTENTION=1 (head dim 32/64): attn_tc.cu, one CTA per tile x head.
-// The tcgen05 kernels take 128-query tiles and read the V cache transposed (keys
-// contiguous), so the K/V projection stores it that way when one of them is selected.
+// Attention kernels (bf16 path): attn_fa.cu (tcgen05 + TMA, S / P / O in TMEM) for head dims
+// 16 / 32 / 64; it reads the V cache transposed (keys contiguous), so the K/V projection stores it
+// that way and both passes use 128-query tiles. DCAT_ATTN_FLASH=1 selects the round-1 mma.sync
+// kernel (attention.cu, row-major V) for comparisons.
 bool use_tc_attention(const dcat_model* m, bool f32) {
     const int dh = m->cfg.d_model / m->cfg.n_heads;
     if (f32) return false;
-    if (getenv("DCAT_ATTN_PIPE") != nullptr && attention_pipe_supported(dh)) return true;
-    return getenv("DCAT_TC_ATTENTION") != nullptr && (dh == 32 || dh == 64);
+    if (getenv("DCAT_ATTN_FLASH") != nullptr) return false;
+    return attention_fa_supported(dh);
 }
 
 // dedup + validation; leaves the plan on the device and the counts in m->st_host
@@ -581,9 +577,7 @@ void attn(dcat_model* m, const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cud
     int t0 = mark(m, s);
     if constexpr (std::is_same<T, bf16>::value) {
         if (a.ldvt > 0) {
-            const bool pipe = getenv("DCAT_ATTN_PIPE") != nullptr;
-            if (pipe && attention_pipe_supported(a.dh)) attention_pipe(a, q_rows, kv_rows, s);
-            else attention_tc(a, q_rows, kv_rows, s);
+            attention_fa(a, q_rows, kv_rows, s);
         } else {
             attention_bf16(a, s);
         }
@@ -737,7 +731,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
             AttnArgs aa{A.q,     d,  K_l(l), V_l(l), d, ldvt, nullptr, nullptr, 0, A.ctx, d, ctx_tiles, st.ctx_tiles,
                         H,       dh, scale,  1,      c.max_len + 1};
             aa.dbg = m->dbg;
-            attn<T>(m, aa, Rr, Tp, s);
+            attn<T>(m, aa, Rr, T_ctx, s);
             layer_tail<T>(m, "ctx", A.ctx, L, l, M, A.x, A.a, l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr,
                           l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // emitted rows: copy
         }
@@ -850,7 +844,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
                     H,   dh,    scale,  0,      c.max_len + 1};
         aa.sparse_tiles = B < static_cast<int64_t>(st.cross_tiles) * (m->tile_cross / 2);
         aa.dbg = m->dbg;
-        attn<T>(m, aa, Rr, std::max<int64_t>(Tp, 1), s);
+        attn<T>(m, aa, Rr, T_ctx, s);
         layer_tail<T>(m, "cross", A.ctx, L, l, M, A.x, A.a, l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr,
                       l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // last: copy for phi_out
     }

@@ -209,13 +209,12 @@ struct AttnArgs {
                                     // online-softmax rescale events
 };
 void attention_bf16(const AttnArgs& a, cudaStream_t s);
-// tcgen05 attention (attn_tc.cu): bf16, V cache transposed (ldvt > 0); q_rows / kv_rows are the
-// row extents of the Q and K tensors.
-void attention_tc(const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t s);
-// persistent pipelined tcgen05 attention (attn_pipe.cu): bf16, head dim 32, V cache transposed
-bool attention_pipe_supported(int dh);
-void attention_pipe(const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t s);
 void attention_f32(const AttnArgs& a, cudaStream_t s);
+// FA4-style tcgen05 attention (attn_fa.cu): bf16, head dim 16 / 32 / 64, V cache transposed
+// (ldvt > 0); q_rows = rows of the Q (and k_self / v_self) tensors, kv_rows = context tokens
+// actually written (keys past it read as zeros).
+bool attention_fa_supported(int dh);
+void attention_fa(const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t s);
 
 // ---------------------------------------------------------------- head / scatter
 void scatter_outputs(const int32_t* perm, int64_t B, const float* logits_p, const float* mlog_p, const float* h_p,
