@@ -201,6 +201,37 @@ typedef struct dcat_call_stats {
 } dcat_call_stats;
 int dcat_last_stats(dcat_model* m, dcat_call_stats* out);
 
+/* ---- The DCAT sub-API (dcat.hpp:47-78) with a device-resident K/V cache ----------------------
+ * context_forward (dcat.hpp:47-49, dcat.cpp:137-178) / context_forward_fixed (dcat.hpp:95-98,
+ * dcat.cpp:281-336) -> dcat_kv (KVCache / FixedKVCache, dcat.hpp:30-41, 65-78, kept on the device),
+ * candidate_inputs (dcat.hpp:53-54, dcat.cpp:180-197), cross_forward / cross_forward_fixed
+ * (dcat.hpp:59-60, 100-101, dcat.cpp:199-271, 338-415). A cache computed once can be crossed with
+ * any number of candidate batches. Pointers are host memory unless DCAT_INPUT_DEVICE; a cache and
+ * the crosses over it use one precision (DCAT_PRECISION_FP32 or not). */
+typedef struct dcat_kv dcat_kv;
+
+/* One unique sequence per batch row (row_offset / row_valid / ev_*; candidate / age / aux
+ * unused). window = 0: the full valid prefix (context_forward); window >= 1: the newest window - 1
+ * events with positions from 0 (context_forward_fixed; the ring rotation does not change results).
+ * emit_hidden = 1 runs the last layer in full; h_user (NULL or sum_u n_u x d_model fp32, row u's
+ * tokens after rows 0..u-1) then receives phi_out of every token. *out owns the device cache. */
+int dcat_context_forward(dcat_model* m, const dcat_batch* uniques, int32_t window, int32_t emit_hidden,
+                         float* h_user, int32_t flags, void* stream, dcat_kv** out);
+int dcat_kv_destroy(dcat_kv* kv);
+/* n_uniques, n_layers, d_model and the per-unique token counts (SeqKV::n / FixedSeqKV::kept) of
+ * a cache; n may be NULL. */
+int dcat_kv_info(const dcat_kv* kv, int32_t* n_uniques, int32_t* n_layers, int32_t* d_model, int32_t* n);
+/* Layer `layer` K and V of unique u (SeqKV::k[layer], v[layer]) as fp32 host n_u x d_model. */
+int dcat_kv_read(const dcat_kv* kv, int32_t layer, int32_t unique, float* k, float* v);
+/* e_cand[n x d_emb] fp32 = id embedding of items[i] + pos_emb[pos[i]] (candidate_inputs). */
+int dcat_candidate_inputs(dcat_model* m, const uint64_t* items, const int32_t* pos, int64_t n, float* e_cand,
+                          int32_t flags, void* stream);
+/* cross_forward: h[n x d_model] (unit-norm rows) for candidate rows b whose unique is rep[b] (an
+ * index into the rows given to dcat_context_forward, DedupPlan::rep) with inputs e_cand[n x d_emb]
+ * (fp32, candidate_inputs). The fixed-window cache gives cross_forward_fixed. */
+int dcat_cross_forward(dcat_model* m, const dcat_kv* kv, const int32_t* rep, const float* e_cand, int64_t n,
+                       float* h, int32_t flags, void* stream);
+
 /* Test instrumentation: device counters of a model created with the environment variable
  * DCAT_DEBUG_COUNTERS set (none otherwise). out[0] = online-softmax rescale events of the causal
  * (context) attention kernel, out[1] = of the crossing kernel. Reads and resets them; returns the

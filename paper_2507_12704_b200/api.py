@@ -48,18 +48,66 @@ def lib() -> C.CDLL:
         L.dcat_stage_times.argtypes = [C.c_void_p, P(C.c_char_p), P(C.c_float), C.c_int32]
         L.dcat_last_stats.argtypes = [C.c_void_p, P(CallStatsC)]
         L.dcat_debug_counters.argtypes = [C.c_void_p, P(C.c_uint64), C.c_int32]
+        L.dcat_context_forward.argtypes = [C.c_void_p, P(BatchC), C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
+                                           C.c_void_p, P(C.c_void_p)]
+        L.dcat_kv_destroy.argtypes = [C.c_void_p]
+        L.dcat_kv_info.argtypes = [C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32), C.c_void_p]
+        L.dcat_kv_read.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
+        L.dcat_candidate_inputs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
+                                            C.c_void_p]
+        L.dcat_cross_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                         C.c_int32, C.c_void_p]
         _lib = L
     return _lib
 
 
 EXPORTS = ("dcat_last_error", "dcat_version", "dcat_model_create", "dcat_model_destroy", "dcat_dedup",
            "dcat_rank_forward_batch", "dcat_debug_kv", "dcat_stage_times", "dcat_last_stats",
-           "dcat_debug_counters")
+           "dcat_debug_counters", "dcat_context_forward", "dcat_kv_destroy", "dcat_kv_info", "dcat_kv_read",
+           "dcat_candidate_inputs", "dcat_cross_forward")
 
 
 def _check(rc: int):
     if rc != 0:
         raise RuntimeError(lib().dcat_last_error().decode())
+
+
+class KVCache:
+    """context_forward's KVCache / FixedKVCache (dcat.hpp:30-41, 65-78), resident on the device."""
+
+    def __init__(self, handle, model, precision: str, window: int):
+        self._h = handle
+        self._model = model  # keeps the model alive for the cache's lifetime
+        self.precision = precision
+        self.window = window
+        nu, nl, d = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(lib().dcat_kv_info(self._h, C.byref(nu), C.byref(nl), C.byref(d), None))
+        self.n_uniques, self.n_layers, self.d_model = nu.value, nl.value, d.value
+
+    def lengths(self) -> np.ndarray:
+        """SeqKV::n (FixedSeqKV::kept) of every unique."""
+        n = np.zeros(max(self.n_uniques, 1), np.int32)
+        _check(lib().dcat_kv_info(self._h, None, None, None, n.ctypes.data))
+        return n[:self.n_uniques]
+
+    def read(self, layer: int, unique: int):
+        """(K, V) of one unique at one layer, fp32 n_u x d_model."""
+        n = int(self.lengths()[unique])
+        k = np.zeros((max(n, 1), self.d_model), np.float32)
+        v = np.zeros_like(k)
+        _check(lib().dcat_kv_read(self._h, layer, unique, k.ctypes.data, v.ctypes.data))
+        return k[:n], v[:n]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dcat_kv_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class DcatModel:
@@ -129,6 +177,46 @@ class DcatModel:
         _check(lib().dcat_rank_forward_batch(self._h, C.byref(batch.c()), C.byref(ft.c()), p(logits), p(mlog),
                                              p(h) if h is not None else None, flags, C.c_void_p(stream)))
         return logits[:B], mlog[:B], (h[:B] if h is not None else None)
+
+    # ------------------------------------------------------------------ the DCAT sub-API
+    def context_forward(self, uniques: Batch, *, window: int = 0, emit_hidden: bool = False, want_h: bool = False,
+                        precision: str = "bf16"):
+        """context_forward (dcat.hpp:47-49) / context_forward_fixed (window >= 1) of one sequence per
+        row of `uniques` -> (KVCache on the device, h_user rows or None)."""
+        flags = FLAG_PRECISION_FP32 if precision == "fp32" else 0
+        h = C.c_void_p()
+        hu = None
+        if want_h:
+            total = int(np.minimum(uniques.row_valid, window - 1).sum()) if window > 0 else int(uniques.row_valid.sum())
+            hu = np.zeros((max(total, 1), self.d_model), np.float32)
+        _check(lib().dcat_context_forward(self._h, C.byref(uniques.c()), window, int(emit_hidden),
+                                          hu.ctypes.data if hu is not None else None, flags, None, C.byref(h)))
+        kv = KVCache(h, self, precision, window)
+        return kv, (hu[:int(kv.lengths().sum())] if hu is not None else None)
+
+    def candidate_inputs(self, items, pos) -> np.ndarray:
+        """candidate_inputs (dcat.hpp:53-54): id embedding + pos_emb[pos], fp32 n x d_emb."""
+        items = np.ascontiguousarray(items, np.uint64)
+        pos = np.ascontiguousarray(pos, np.int32)
+        if items.shape != pos.shape:
+            raise RuntimeError("candidate_inputs: size mismatch")
+        e = np.zeros((max(items.size, 1), self.spec.d_emb), np.float32)
+        _check(lib().dcat_candidate_inputs(self._h, items.ctypes.data, pos.ctypes.data, items.size, e.ctypes.data, 0,
+                                           None))
+        return e[:items.size]
+
+    def cross_forward(self, kv: KVCache, rep, e_cand) -> np.ndarray:
+        """cross_forward (dcat.hpp:59-60) / cross_forward_fixed over a device cache: rows b cross
+        unique rep[b] (DedupPlan::rep) with inputs e_cand -> unit-norm rows n x d_model."""
+        rep = np.ascontiguousarray(rep, np.int32)
+        e_cand = np.ascontiguousarray(e_cand, np.float32)
+        if e_cand.shape != (rep.size, self.spec.d_emb):
+            raise RuntimeError(f"cross_forward: {e_cand.shape[0]} candidate rows for {rep.size} batch rows")
+        h = np.zeros((max(rep.size, 1), self.d_model), np.float32)
+        flags = FLAG_PRECISION_FP32 if kv.precision == "fp32" else 0
+        _check(lib().dcat_cross_forward(self._h, kv._h, rep.ctypes.data, e_cand.ctypes.data, rep.size,
+                                        h.ctypes.data, flags, None))
+        return h[:rep.size]
 
     # ------------------------------------------------------------------
     def debug_kv(self, layer: int, unique: int, max_tokens: int):

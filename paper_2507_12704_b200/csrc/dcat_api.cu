@@ -133,6 +133,7 @@ struct dcat_model {
     Buf b_kv;
     Buf b_aux;
     Buf b_out[3];
+    Buf b_x[6];  // dcat_context_forward / dcat_candidate_inputs / dcat_cross_forward staging
     // last-call bookkeeping
     int64_t last_bu = 0, last_T = 0, last_Tp = 0;
     int last_precision_f32 = 0;
@@ -190,6 +191,21 @@ struct dcat_model {
         if (dd_exec) cudaGraphExecDestroy(dd_exec);
         if (run_exec) cudaGraphExecDestroy(run_exec);
         if (cap) cudaStreamDestroy(cap);
+    }
+};
+
+// context_forward's KVCache / FixedKVCache on the device (dcat_context_forward)
+struct dcat_kv {
+    dcat_model* m = nullptr;
+    int device = 0;
+    bool f32 = false, vt = false;
+    int n_layers = 0, d = 0, window = 0;
+    int64_t Tp = 0, T_ctx = 0;
+    void* buf = nullptr;           // [layer][K|V][Tp][d] (V^T [d][Tp] when vt), the model's layout
+    std::vector<int32_t> rep;      // caller row -> plan unique (equal sequences share one)
+    std::vector<int64_t> tok_off;  // plan unique -> first token, b_u + 1 entries
+    ~dcat_kv() {
+        if (buf) cudaFree(buf);
     }
 };
 
@@ -597,9 +613,51 @@ void attn(dcat_model* m, const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cud
 //     the reference computes the same per example (:428-431), here once per unique.
 constexpr int64_t kDualStreamMaxRows = 65536;  // context / candidate rows (padded) below which run_dcat forks
 
+// context_forward on its own (dcat_context_forward): the context pass only, its K/V left in the
+// model's cache buffer; emit_hidden runs the last layer in full and, with h_user, writes
+// phi_out of every context token (fp32, token order) to h_user (device)
+struct CtxOnly {
+    bool on = false;
+    bool emit_hidden = false;
+    float* h_user = nullptr;
+};
+
+// The crossing pass's transformer layers (cross_forward dcat.cpp:199-271 after phi_in): per layer
+// QKV of the candidate rows (q, own k / v), attention over the unique's cached K / V plus itself,
+// then the fused layer tail. kv = the cache base ([layer][K|V][Tp][d]), T_ctx = context tokens
+// written, ldvt = V^T leading dimension (0: row-major V). Leaves the final rows in A.a (copy).
+template <typename T>
+void cross_layers(dcat_model* m, Acts<T>& A, int M, const Tile* cross_tiles, int n_tiles, bool sparse_tiles,
+                  T* kv, int64_t Tp, int64_t T_ctx, int ldvt, const std::vector<char>* kv_done, cudaStream_t s) {
+    const dcat_model_config& c = m->cfg;
+    const int d = c.d_model, H = c.n_heads, dh = d / H, nl = c.n_layers;
+    const float scale = 1.0f / std::sqrt(static_cast<float>(dh));
+    for (int l = 0; l < nl; l++) {
+        const LayerW& L = m->layers[l];
+        Epi e = base_epi(m, EPI_BIAS);
+        e.bias = L.qkv.bias;
+        e.out[0] = A.q;
+        e.out[1] = A.kself;
+        e.out[2] = A.vself;
+        e.out_ld[0] = e.out_ld[1] = e.out_ld[2] = d;
+        e.seg_cols = d;
+        gemm<T>(m, "gemm.cross.qkv", A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
+        if (kv_done && (*kv_done)[l]) DCAT_CUDA_CHECK(cudaStreamWaitEvent(s, m->kv_ev[l], 0));
+        T* K = kv + static_cast<size_t>(2 * l) * Tp * d;
+        T* V = kv + static_cast<size_t>(2 * l + 1) * Tp * d;
+        AttnArgs aa{A.q, d,  K,     V, d, ldvt, A.kself, A.vself, d, A.ctx, d, cross_tiles, n_tiles,
+                    H,   dh, scale, 0, c.max_len + 1};
+        aa.sparse_tiles = sparse_tiles;
+        aa.dbg = m->dbg;
+        attn<T>(m, aa, std::max(A.Tp, A.Bp), T_ctx, s);
+        layer_tail<T>(m, "cross", A.ctx, L, l, M, A.x, A.a, l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr,
+                      l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // last: copy for phi_out
+    }
+}
+
 template <typename T>
 void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_finetune_config& ft, float* logits,
-              float* mlogits, float* h_cand, cudaStream_t s) {
+              float* mlogits, float* h_cand, cudaStream_t s, const CtxOnly& co = CtxOnly()) {
     const dcat_model_config& c = m->cfg;
     const int d = c.d_model, de = c.d_emb, F = c.d_model * c.mlp_ratio, H = c.n_heads, dh = d / H, nl = c.n_layers;
     const Status& st = *m->st_host;
@@ -610,7 +668,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     const int kh = f32 ? m->d_feat : m->kh;
     const bool lite = ft.variant == DCAT_VARIANT_LITE_MEAN || ft.variant == DCAT_VARIANT_LITE_LAST;
     const bool auxlt = ft.variant == DCAT_VARIANT_AUXLT;
-    const bool full_last = lite || auxlt;  // the context pass must emit the final hidden rows
+    const bool full_last = lite || auxlt || co.emit_hidden;  // the context pass must emit the final hidden rows
 
     int t_stage0 = mark(m, s);
     span(m, "host.after_sync", m->t_dedup_end, t_stage0);
@@ -626,7 +684,7 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     // DCAT_DUAL_STREAM=0 / 1 forces it.
     static const char* dual_env = getenv("DCAT_DUAL_STREAM");
     const bool dual_fit = dual_env ? dual_env[0] == '1' : Rr <= kDualStreamMaxRows;
-    const bool dual = dual_fit && !(ft.variant == DCAT_VARIANT_LITE_MEAN || ft.variant == DCAT_VARIANT_LITE_LAST);
+    const bool dual = dual_fit && !co.on && !(ft.variant == DCAT_VARIANT_LITE_MEAN || ft.variant == DCAT_VARIANT_LITE_LAST);
     std::vector<char> kv_done(nl, 0);  // kv_ev[l] recorded in this call
     if (dual) {
         if (!m->xs) {
@@ -736,6 +794,24 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
                           l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // emitted rows: copy
         }
     }
+    if (co.on) {  // context_forward alone: K/V stay in the cache; h_user = phi_out of every token
+        if (co.emit_hidden && co.h_user && T_ctx > 0) {
+            Epi e = base_epi(m, EPI_BIAS);
+            e.act = 1;
+            e.bias = m->phi_out1.bias;
+            e.out[0] = A.h1;
+            e.out_ld[0] = d;
+            e.seg_cols = d;
+            gemm<T>(m, "gemm.ctx.phi_out1", A.a, d, m->phi_out1, 0, d, static_cast<int>(T_ctx), e, A.tmp, s);
+            e = base_epi(m, EPI_L2NORM);
+            e.bias = m->phi_out2.bias;
+            e.x_out = co.h_user;
+            e.ld_x = d;
+            gemm<T>(m, "gemm.ctx.phi_out2", A.h1, d, m->phi_out2, 0, d, static_cast<int>(T_ctx), e, A.tmp, s);
+        }
+        span(m, "context", t_ctx0, mark(m, s));
+        return;
+    }
     // per-unique selector rows (fp32 b_u x d): Lite pools phi_out(H) over a unique's tokens,
     // AuxLt takes phi_out of its learnable token (the unique's last context row)
     float* sel = nullptr;
@@ -829,25 +905,8 @@ void run_dcat(dcat_model* m, const Staged& sb, const DedupOut& o, const dcat_fin
     e.ln_out = A.a;
     e.ln_ld = d;
     gemm<T>(m, "gemm.cross.phi_in2", A.h1, d, m->phi_in2, 0, d, M, e, A.tmp, s);
-    for (int l = 0; l < nl; l++) {
-        const LayerW& L = m->layers[l];
-        e = base_epi(m, EPI_BIAS);
-        e.bias = L.qkv.bias;
-        e.out[0] = A.q;
-        e.out[1] = A.kself;
-        e.out[2] = A.vself;
-        e.out_ld[0] = e.out_ld[1] = e.out_ld[2] = d;
-        e.seg_cols = d;
-        gemm<T>(m, "gemm.cross.qkv", A.a, d, L.qkv, 0, 3 * d, M, e, A.tmp, s);
-        if (dual && kv_done[l]) DCAT_CUDA_CHECK(cudaStreamWaitEvent(s, m->kv_ev[l], 0));
-        AttnArgs aa{A.q, d,     K_l(l), V_l(l), d, ldvt, A.kself, A.vself, d, A.ctx, d, cross_tiles, st.cross_tiles,
-                    H,   dh,    scale,  0,      c.max_len + 1};
-        aa.sparse_tiles = B < static_cast<int64_t>(st.cross_tiles) * (m->tile_cross / 2);
-        aa.dbg = m->dbg;
-        attn<T>(m, aa, Rr, T_ctx, s);
-        layer_tail<T>(m, "cross", A.ctx, L, l, M, A.x, A.a, l + 1 < nl ? m->layers[l + 1].ln1_g : nullptr,
-                      l + 1 < nl ? m->layers[l + 1].ln1_b : nullptr, A.f1, A.tmp, s);  // last: copy for phi_out
-    }
+    cross_layers<T>(m, A, M, cross_tiles, st.cross_tiles, B < static_cast<int64_t>(st.cross_tiles) * (m->tile_cross / 2),
+                    A.kv, Tp, T_ctx, ldvt, dual ? &kv_done : nullptr, s);
     if (dual) {  // join: the rest reads the context pass's selectors and goes out on the caller's stream
         DCAT_CUDA_CHECK(cudaEventRecord(m->join_ev, s));
         DCAT_CUDA_CHECK(cudaStreamWaitEvent(s_main, m->join_ev, 0));
@@ -975,6 +1034,124 @@ int guarded(dcat_model* m, F&& f) {
     } catch (const std::bad_alloc&) {
         return set_err(DCAT_ENOMEM, "host out of memory");
     }
+}
+
+// K and V rows [a, b) of one layer from a cache buffer (layout of run_dcat's A.kv) -> fp32 host
+void read_kv_rows(const void* buf, bool vt, bool f32, int64_t Tp, int d, int layer, int64_t a, int64_t b, float* k,
+                  float* v) {
+    const size_t cnt = static_cast<size_t>(b - a) * d;
+    for (int which = 0; which < 2; which++) {
+        float* dst = which ? v : k;
+        if (!dst) continue;
+        const size_t base = (static_cast<size_t>(2 * layer + which) * Tp + a) * d;
+        if (which == 1 && vt) {  // V^T [d][Tp]: gather the unique's key columns
+            const size_t vbase = static_cast<size_t>(2 * layer + 1) * Tp * d;
+            std::vector<bf16> tmp(static_cast<size_t>(d) * Tp);
+            DCAT_CUDA_CHECK(cudaMemcpy(tmp.data(), static_cast<const bf16*>(buf) + vbase, tmp.size() * 2,
+                                       cudaMemcpyDeviceToHost));
+            for (int64_t t = 0; t < b - a; t++)
+                for (int i = 0; i < d; i++) dst[t * d + i] = __bfloat162float(tmp[static_cast<size_t>(i) * Tp + a + t]);
+            continue;
+        }
+        if (f32) {
+            DCAT_CUDA_CHECK(cudaMemcpy(dst, static_cast<const float*>(buf) + base, cnt * 4, cudaMemcpyDeviceToHost));
+        } else {
+            std::vector<bf16> tmp(cnt);
+            DCAT_CUDA_CHECK(cudaMemcpy(tmp.data(), static_cast<const bf16*>(buf) + base, cnt * 2, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < cnt; i++) dst[i] = __bfloat162float(tmp[i]);
+        }
+    }
+}
+
+EmbParams emb_params(const dcat_model* m, bool f32) {
+    return EmbParams{m->table, m->qtable,     m->qbits,       m->qrow_bytes,  m->qcode_bytes, m->seed_mix, m->J,
+                     m->R,     m->d_sub,      m->action_emb,  m->surface_emb, m->pos_emb,     m->cfg.d_emb, m->lt,
+                     f32 ? nullptr : m->cmb, m->cfg.n_surfaces, m->cfg.max_len};
+}
+
+// cross_forward on a device cache (dcat_cross_forward): the candidate rows grouped by unique
+// (perm / tiles built on the host from rep), phi_in, the crossing layers, phi_out -> h (device,
+// caller row order)
+template <typename T>
+void run_cross_external(dcat_model* m, const dcat_kv* kv, const std::vector<int32_t>& du, const float* e_dev,
+                        float* h_dev, cudaStream_t s) {
+    const dcat_model_config& c = m->cfg;
+    const int d = c.d_model, de = c.d_emb, F = d * c.mlp_ratio;
+    const int64_t B = static_cast<int64_t>(du.size()), Bp = (B + 127) / 128 * 128;
+    const int64_t Rr = std::max(kv->Tp, Bp);
+    const int b_u = static_cast<int>(kv->tok_off.size()) - 1;
+    // counting sort of the rows by unique (stable), 128-row crossing tiles per unique
+    std::vector<int32_t> cnt(static_cast<size_t>(b_u) + 1, 0), perm(static_cast<size_t>(B));
+    for (int32_t u : du) cnt[static_cast<size_t>(u)]++;
+    std::vector<int64_t> goff(static_cast<size_t>(b_u) + 1, 0);
+    for (int u = 0; u < b_u; u++) goff[u + 1] = goff[u] + cnt[u];
+    std::vector<int64_t> cur(goff.begin(), goff.end() - 1);
+    for (int64_t b = 0; b < B; b++) perm[static_cast<size_t>(cur[du[b]]++)] = static_cast<int32_t>(b);
+    std::vector<Tile> tiles;
+    for (int u = 0; u < b_u; u++)
+        for (int64_t j = 0; j * 128 < cnt[u]; j++) {
+            Tile t{};
+            t.q0 = static_cast<int>(goff[u] + j * 128);
+            t.nq = static_cast<int>(std::min<int64_t>(128, cnt[u] - j * 128));
+            t.kv0 = static_cast<int>(kv->tok_off[u]);
+            t.nkv = static_cast<int>(kv->tok_off[u + 1] - kv->tok_off[u]);
+            t.u = u;
+            tiles.push_back(t);
+        }
+    int32_t* perm_d = m->b_x[1].get<int32_t>(B);
+    Tile* tiles_d = m->b_x[2].get<Tile>(std::max<size_t>(tiles.size(), 1));
+    DCAT_CUDA_CHECK(cudaMemcpyAsync(perm_d, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, s));
+    DCAT_CUDA_CHECK(cudaMemcpyAsync(tiles_d, tiles.data(), tiles.size() * sizeof(Tile), cudaMemcpyHostToDevice, s));
+    const bool f32 = std::is_same<T, float>::value;
+    Acts<T> A;
+    A.Tp = kv->Tp;
+    A.Bp = Bp;
+    A.E = m->b_act[0].get<T>(Rr * de);
+    A.h1 = m->b_act[1].get<T>(Rr * d);
+    A.a = m->b_act[2].get<T>(Rr * d);
+    A.q = m->b_act[3].get<T>(Rr * d);
+    A.ctx = m->b_act[4].get<T>(Rr * d);
+    A.f1 = m->b_act[5].get<T>(Rr * F);
+    A.kself = m->b_act[6].get<T>(Bp * d);
+    A.vself = m->b_act[7].get<T>(Bp * d);
+    A.x = m->b_act[9].get<float>(Rr * d);
+    A.hc = m->b_act[10].get<float>(Bp * d);
+    A.tmp = f32 ? m->b_act[13].get<float>(Rr * std::max(3 * d, std::max(F, m->hidden))) : nullptr;
+    gather_rows<T>(e_dev, perm_d, B, de, A.E, s);
+    m->stats.kernel_launches += 1;
+    const int M = static_cast<int>(B);
+    Epi e = base_epi(m, EPI_BIAS);
+    e.act = 1;
+    e.bias = m->phi_in1.bias;
+    e.out[0] = A.h1;
+    e.out_ld[0] = d;
+    e.seg_cols = d;
+    gemm<T>(m, "gemm.cross.phi_in1", A.E, de, m->phi_in1, 0, d, M, e, A.tmp, s);
+    e = base_epi(m, EPI_L2NORM);
+    e.bias = m->phi_in2.bias;
+    e.x_out = A.x;
+    e.ld_x = d;
+    e.ln_g = m->layers[0].ln1_g;
+    e.ln_b = m->layers[0].ln1_b;
+    e.ln_out = A.a;
+    e.ln_ld = d;
+    gemm<T>(m, "gemm.cross.phi_in2", A.h1, d, m->phi_in2, 0, d, M, e, A.tmp, s);
+    cross_layers<T>(m, A, M, tiles_d, static_cast<int>(tiles.size()), B < static_cast<int64_t>(tiles.size()) * 64,
+                    static_cast<T*>(kv->buf), kv->Tp, kv->T_ctx, kv->vt ? static_cast<int>(kv->Tp) : 0, nullptr, s);
+    e = base_epi(m, EPI_BIAS);
+    e.act = 1;
+    e.bias = m->phi_out1.bias;
+    e.out[0] = A.h1;
+    e.out_ld[0] = d;
+    e.seg_cols = d;
+    gemm<T>(m, "gemm.cross.phi_out1", A.a, d, m->phi_out1, 0, d, M, e, A.tmp, s);
+    e = base_epi(m, EPI_L2NORM);
+    e.bias = m->phi_out2.bias;
+    e.x_out = A.hc;
+    e.ld_x = d;
+    gemm<T>(m, "gemm.cross.phi_out2", A.h1, d, m->phi_out2, 0, d, M, e, A.tmp, s);
+    scatter_rows(A.hc, perm_d, B, d, h_dev, s);
+    m->stats.kernel_launches += 1;
 }
 
 }  // namespace
@@ -1336,31 +1513,213 @@ int dcat_debug_kv(dcat_model* m, int32_t layer, int32_t unique, float* k, float*
             return set_err(DCAT_EINVAL, "no such unique / layer in the last call");
         int64_t a = m->last_tok_off[unique], b = m->last_tok_off[unique + 1];
         *n = static_cast<int32_t>(b - a);
-        int d = m->cfg.d_model;
-        size_t cnt = static_cast<size_t>(b - a) * d;
-        for (int which = 0; which < 2; which++) {
-            float* dst = which ? v : k;
-            if (!dst) continue;
-            size_t base = (static_cast<size_t>(2 * layer + which) * m->last_Tp + a) * d;
-            if (which == 1 && m->last_vt) {  // V^T [d][Tp]: gather the unique's key columns
-                const size_t vbase = static_cast<size_t>(2 * layer + 1) * m->last_Tp * d;
-                std::vector<bf16> tmp(static_cast<size_t>(d) * m->last_Tp);
-                DCAT_CUDA_CHECK(cudaMemcpy(tmp.data(), static_cast<bf16*>(m->last_kv) + vbase, tmp.size() * 2,
-                                           cudaMemcpyDeviceToHost));
-                for (int64_t t = 0; t < b - a; t++)
-                    for (int i = 0; i < d; i++)
-                        dst[t * d + i] = __bfloat162float(tmp[static_cast<size_t>(i) * m->last_Tp + a + t]);
-                continue;
-            }
-            if (m->last_precision_f32) {
-                DCAT_CUDA_CHECK(cudaMemcpy(dst, static_cast<float*>(m->last_kv) + base, cnt * 4, cudaMemcpyDeviceToHost));
-            } else {
-                std::vector<bf16> tmp(cnt);
-                DCAT_CUDA_CHECK(cudaMemcpy(tmp.data(), static_cast<bf16*>(m->last_kv) + base, cnt * 2,
-                                           cudaMemcpyDeviceToHost));
-                for (size_t i = 0; i < cnt; i++) dst[i] = __bfloat162float(tmp[i]);
-            }
+        read_kv_rows(m->last_kv, m->last_vt, m->last_precision_f32, m->last_Tp, m->cfg.d_model, layer, a, b, k, v);
+        return DCAT_OK;
+    });
+}
+
+int dcat_context_forward(dcat_model* m, const dcat_batch* uniques, int32_t window, int32_t emit_hidden,
+                         float* h_user, int32_t flags, void* stream, dcat_kv** out) {
+    if (!m || !uniques || !out) return set_err(DCAT_EINVAL, "null argument");
+    *out = nullptr;
+    return guarded(m, [&]() -> int {
+        // context_forward / context_forward_fixed argument checks (dcat.cpp:141-142, 285-288)
+        const char* fn = window > 0 ? "context_forward_fixed" : "context_forward";
+        if (window < 0) return set_err(DCAT_EINVAL, "context_forward_fixed: window must be >= 1, got " +
+                                                        std::to_string(window));
+        if (m->cfg.n_layers < 1) return set_err(DCAT_EINVAL, std::string(fn) + ": needs at least one layer");
+        if (h_user && !emit_hidden) return set_err(DCAT_EINVAL, std::string(fn) + ": h_user requires emit_hidden");
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const bool device = flags & DCAT_INPUT_DEVICE, f32 = flags & DCAT_PRECISION_FP32;
+        m->profiling = false;
+        m->ev_next = 0;
+        m->ev_marks.clear();
+        std::memset(&m->stats, 0, sizeof m->stats);
+        std::unique_ptr<dcat_kv> kv(new dcat_kv());
+        kv->m = m;
+        kv->device = m->device;
+        kv->f32 = f32;
+        kv->n_layers = m->cfg.n_layers;
+        kv->d = m->cfg.d_model;
+        kv->window = window;
+        const int64_t B = uniques->n_rows;
+        if (B == 0) {
+            kv->tok_off.assign(1, 0);
+            *out = kv.release();
+            return DCAT_OK;
         }
+        m->vt = use_tc_attention(m, f32);
+        m->tile_ctx = m->vt ? 128 : kCtxTile;
+        m->tile_cross = m->vt ? 128 : kCrossTile;
+        Staged sb = stage_batch(m, uniques, device, false, s, false);
+        sb.in.window = window;
+        sb.in.lt_token = 0;
+        DedupOut o = dedup_buffers(m, B);
+        run_dedup(m, sb, o, s);
+        Status st = *m->st_host;
+        st.err_bits &= ~(ERR_POS_CAND | ERR_AGE);  // no candidate tokens here
+        if (st.err_bits) {
+            int code;
+            std::string msg = status_message(m, st, &code);
+            return set_err(code, msg);
+        }
+        dcat_finetune_config ft{};
+        ft.variant = DCAT_VARIANT_BASE;
+        ft.use_seq_module = 1;
+        ft.window = window;
+        ft.fresh_days = 1.0;
+        ft.mid_days = 2.0;
+        const int64_t T_ctx = st.ctx_tokens, d = m->cfg.d_model;
+        float* hdev = emit_hidden && h_user ? m->b_x[0].get<float>(std::max<int64_t>(T_ctx, 1) * d) : nullptr;
+        CtxOnly co;
+        co.on = true;
+        co.emit_hidden = emit_hidden != 0;
+        co.h_user = hdev;
+        if (f32) run_dcat<float>(m, sb, o, ft, nullptr, nullptr, nullptr, s, co);
+        else run_dcat<bf16>(m, sb, o, ft, nullptr, nullptr, nullptr, s, co);
+        kv->vt = m->vt;
+        kv->Tp = m->last_Tp;
+        kv->T_ctx = T_ctx;
+        const size_t bytes = static_cast<size_t>(2 * kv->n_layers) * kv->Tp * d * (f32 ? 4 : 2);
+        DCAT_CUDA_CHECK(cudaMalloc(&kv->buf, std::max<size_t>(bytes, 16)));
+        if (bytes) DCAT_CUDA_CHECK(cudaMemcpyAsync(kv->buf, m->last_kv, bytes, cudaMemcpyDeviceToDevice, s));
+        kv->rep.resize(static_cast<size_t>(B));
+        kv->tok_off.resize(static_cast<size_t>(st.b_u) + 1);
+        DCAT_CUDA_CHECK(cudaMemcpyAsync(kv->rep.data(), o.rep, sizeof(int32_t) * B, cudaMemcpyDeviceToHost, s));
+        DCAT_CUDA_CHECK(cudaMemcpyAsync(kv->tok_off.data(), o.tok_off, sizeof(int64_t) * (st.b_u + 1),
+                                        cudaMemcpyDeviceToHost, s));
+        DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
+        DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (m->st_host->nonfinite_layer > 0)
+            return set_err(DCAT_ENONFINITE,
+                           "non-finite activation in layer " + std::to_string(m->st_host->nonfinite_layer - 1));
+        if (hdev) {  // per caller row, its unique's tokens (duplicates repeat them)
+            int64_t at = 0;
+            const cudaMemcpyKind kind = device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+            for (int64_t r = 0; r < B; r++) {
+                const int32_t u = kv->rep[static_cast<size_t>(r)];
+                const int64_t a = kv->tok_off[u], n = kv->tok_off[u + 1] - a;
+                if (n) DCAT_CUDA_CHECK(cudaMemcpyAsync(h_user + at * d, hdev + a * d, sizeof(float) * n * d, kind, s));
+                at += n;
+            }
+            DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+        }
+        *out = kv.release();
+        return DCAT_OK;
+    });
+}
+
+int dcat_kv_destroy(dcat_kv* kv) {
+    if (!kv) return DCAT_OK;
+    cudaSetDevice(kv->device);
+    cudaDeviceSynchronize();
+    delete kv;
+    return DCAT_OK;
+}
+
+int dcat_kv_info(const dcat_kv* kv, int32_t* n_uniques, int32_t* n_layers, int32_t* d_model, int32_t* n) {
+    if (!kv) return set_err(DCAT_EINVAL, "null argument");
+    if (n_uniques) *n_uniques = static_cast<int32_t>(kv->rep.size());
+    if (n_layers) *n_layers = kv->n_layers;
+    if (d_model) *d_model = kv->d;
+    if (n)
+        for (size_t r = 0; r < kv->rep.size(); r++) {
+            const int32_t u = kv->rep[r];
+            n[r] = static_cast<int32_t>(kv->tok_off[u + 1] - kv->tok_off[u]);
+        }
+    return DCAT_OK;
+}
+
+int dcat_kv_read(const dcat_kv* kv, int32_t layer, int32_t unique, float* k, float* v) {
+    if (!kv) return set_err(DCAT_EINVAL, "null argument");
+    return guarded(kv->m, [&]() -> int {
+        if (unique < 0 || unique >= static_cast<int32_t>(kv->rep.size()) || layer < 0 || layer >= kv->n_layers)
+            return set_err(DCAT_EINVAL, "dcat_kv_read: no such unique / layer");
+        const int32_t u = kv->rep[static_cast<size_t>(unique)];
+        read_kv_rows(kv->buf, kv->vt, kv->f32, kv->Tp, kv->d, layer, kv->tok_off[u], kv->tok_off[u + 1], k, v);
+        return DCAT_OK;
+    });
+}
+
+int dcat_candidate_inputs(dcat_model* m, const uint64_t* items, const int32_t* pos, int64_t n, float* e_cand,
+                          int32_t flags, void* stream) {
+    if (!m || (n > 0 && (!items || !pos || !e_cand))) return set_err(DCAT_EINVAL, "null argument");
+    return guarded(m, [&]() -> int {
+        if (n <= 0) return DCAT_OK;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const bool device = flags & DCAT_INPUT_DEVICE;
+        const int de = m->cfg.d_emb;
+        const uint64_t* it = items;
+        const int32_t* ps = pos;
+        float* e = e_cand;
+        if (!device) {
+            uint64_t* it_d = m->b_x[3].get<uint64_t>(n);
+            int32_t* ps_d = m->b_x[4].get<int32_t>(n);
+            DCAT_CUDA_CHECK(cudaMemcpyAsync(it_d, items, sizeof(uint64_t) * n, cudaMemcpyHostToDevice, s));
+            DCAT_CUDA_CHECK(cudaMemcpyAsync(ps_d, pos, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+            it = it_d;
+            ps = ps_d;
+            e = m->b_x[5].get<float>(n * de);
+        }
+        DCAT_CUDA_CHECK(cudaMemsetAsync(m->st_dev, 0, sizeof(Status), s));
+        candidate_inputs(emb_params(m, true), it, ps, n, e, m->st_dev, s);
+        if (!device) DCAT_CUDA_CHECK(cudaMemcpyAsync(e_cand, e, sizeof(float) * n * de, cudaMemcpyDeviceToHost, s));
+        DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
+        DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (m->st_host->err_bits & ERR_POS_CAND)
+            return set_err(DCAT_EINVAL, "candidate_inputs: position " + std::to_string(m->st_host->err_val) +
+                                            " out of range (max_len " + std::to_string(m->cfg.max_len) + ")");
+        return DCAT_OK;
+    });
+}
+
+int dcat_cross_forward(dcat_model* m, const dcat_kv* kv, const int32_t* rep, const float* e_cand, int64_t n,
+                       float* h, int32_t flags, void* stream) {
+    if (!m || !kv || (n > 0 && (!rep || !e_cand || !h))) return set_err(DCAT_EINVAL, "null argument");
+    return guarded(m, [&]() -> int {
+        const char* fn = kv->window > 0 ? "cross_forward_fixed" : "cross_forward";
+        if (kv->m != m) return set_err(DCAT_EINVAL, std::string(fn) + ": cache/model config mismatch");
+        const bool device = flags & DCAT_INPUT_DEVICE, f32 = flags & DCAT_PRECISION_FP32;
+        if (f32 != kv->f32)
+            return set_err(DCAT_EINVAL, std::string(fn) + ": precision differs from the cache's (DCAT_PRECISION_FP32)");
+        if (n <= 0) return DCAT_OK;
+        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        const int d = m->cfg.d_model, de = m->cfg.d_emb;
+        std::vector<int32_t> hrep(static_cast<size_t>(n));
+        if (device) DCAT_CUDA_CHECK(cudaMemcpy(hrep.data(), rep, sizeof(int32_t) * n, cudaMemcpyDeviceToHost));
+        else std::memcpy(hrep.data(), rep, sizeof(int32_t) * n);
+        std::vector<int32_t> du(static_cast<size_t>(n));
+        const int32_t n_uniques = static_cast<int32_t>(kv->rep.size());
+        for (int64_t b = 0; b < n; b++) {
+            const int32_t r = hrep[static_cast<size_t>(b)];
+            if (r < 0 || r >= n_uniques)
+                return set_err(DCAT_EINVAL, std::string(fn) + ": plan rep " + std::to_string(r) + " of row " +
+                                                std::to_string(b) + " outside the cache's " +
+                                                std::to_string(n_uniques) + " uniques");
+            du[static_cast<size_t>(b)] = kv->rep[static_cast<size_t>(r)];
+        }
+        const float* e_dev = e_cand;
+        if (!device) {
+            float* tmp = m->b_x[5].get<float>(n * de);
+            DCAT_CUDA_CHECK(cudaMemcpyAsync(tmp, e_cand, sizeof(float) * n * de, cudaMemcpyHostToDevice, s));
+            e_dev = tmp;
+        }
+        float* h_dev = device ? h : m->b_x[0].get<float>(n * d);
+        m->profiling = false;
+        m->ev_next = 0;
+        m->ev_marks.clear();
+        std::memset(&m->stats, 0, sizeof m->stats);
+        m->vt = kv->vt;
+        m->tile_cross = 128;
+        DCAT_CUDA_CHECK(cudaMemsetAsync(m->st_dev, 0, sizeof(Status), s));
+        if (f32) run_cross_external<float>(m, kv, du, e_dev, h_dev, s);
+        else run_cross_external<bf16>(m, kv, du, e_dev, h_dev, s);
+        if (!device) DCAT_CUDA_CHECK(cudaMemcpyAsync(h, h_dev, sizeof(float) * n * d, cudaMemcpyDeviceToHost, s));
+        DCAT_CUDA_CHECK(cudaMemcpyAsync(m->st_host, m->st_dev, sizeof(Status), cudaMemcpyDeviceToHost, s));
+        DCAT_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (m->st_host->nonfinite_layer > 0)
+            return set_err(DCAT_ENONFINITE,
+                           "non-finite activation in layer " + std::to_string(m->st_host->nonfinite_layer - 1));
         return DCAT_OK;
     });
 }

@@ -449,6 +449,43 @@ void build_combined_emb(const float* action_emb, const float* surface_emb, const
     DCAT_LAUNCH_CHECK();
 }
 
+// candidate_inputs (dcat.cpp:180-197) as its own entry point: e[i] = lookup(items[i]) +
+// pos_emb[pos[i]] (learned positions), fp32, one warp per row; a position outside [0, max_len)
+// is reported like the reference's check (dcat.cpp:190-192)
+__global__ void __launch_bounds__(256) k_cand_inputs(EmbParams ep, const uint64_t* __restrict__ items,
+                                                     const int32_t* __restrict__ pos, int64_t n, float* __restrict__ e,
+                                                     Status* st) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (row >= n) return;
+    const uint64_t item = items[row];
+    const uint32_t rows = warp_rows(ep, item, lane);
+    const int ps = pos[row];
+    const bool pos_ok = ps >= 0 && ps < ep.max_len;
+    if (ep.pos_emb && !pos_ok) {
+        if (lane == 0) {
+            atomicOr(&st->err_bits, ERR_POS_CAND);
+            atomicMin(&st->err_row, static_cast<int>(row));
+            st->err_val = ps;
+        }
+        return;
+    }
+    const float* pe = ep.pos_emb ? ep.pos_emb + static_cast<size_t>(ps) * ep.d_emb : nullptr;
+    float* out = e + row * ep.d_emb;
+    for (int c0 = 0; c0 < ep.d_emb; c0 += 32) {
+        const int c = c0 + lane;
+        const float v = lookup1(ep, item, rows, c);  // every lane takes part in the shuffle
+        if (c < ep.d_emb) out[c] = pe ? v + pe[c] : v;
+    }
+}
+
+void candidate_inputs(const EmbParams& ep, const uint64_t* items, const int32_t* pos, int64_t n, float* e, Status* st,
+                      cudaStream_t s) {
+    if (n <= 0) return;
+    k_cand_inputs<<<static_cast<unsigned>((n * 32 + 255) / 256), 256, 0, s>>>(ep, items, pos, n, e, st);
+    DCAT_LAUNCH_CHECK();
+}
+
 template <typename T>
 void gather_context(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const int32_t* tok_unique,
                     int64_t T_ctx, T* E, int ldE, cudaStream_t s) {

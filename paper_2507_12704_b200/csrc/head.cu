@@ -87,6 +87,38 @@ __global__ void k_mlogits(const int32_t* __restrict__ perm, const int32_t* __res
 
 }  // namespace
 
+// dst[p] = src[perm[p]] (fp32 source rows -> activation type), and the inverse scatter of fp32 rows
+template <typename T>
+__global__ void k_gather_rows(const float* __restrict__ src, const int32_t* __restrict__ perm, int64_t B, int d,
+                              T* __restrict__ dst) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= B * d) return;
+    const int64_t p = i / d;
+    const int c = static_cast<int>(i - p * d);
+    ActIO<T>::store(dst + i, src[static_cast<int64_t>(perm[p]) * d + c]);
+}
+__global__ void k_scatter_rows(const float* __restrict__ src, const int32_t* __restrict__ perm, int64_t B, int d,
+                               float* __restrict__ dst) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= B * d) return;
+    const int64_t p = i / d;
+    const int c = static_cast<int>(i - p * d);
+    dst[static_cast<int64_t>(perm[p]) * d + c] = src[i];
+}
+template <typename T>
+void gather_rows(const float* src, const int32_t* perm, int64_t B, int d, T* dst, cudaStream_t s) {
+    if (B <= 0) return;
+    k_gather_rows<T><<<static_cast<unsigned>((B * d + 255) / 256), 256, 0, s>>>(src, perm, B, d, dst);
+    DCAT_LAUNCH_CHECK();
+}
+void scatter_rows(const float* src, const int32_t* perm, int64_t B, int d, float* dst, cudaStream_t s) {
+    if (B <= 0) return;
+    k_scatter_rows<<<static_cast<unsigned>((B * d + 255) / 256), 256, 0, s>>>(src, perm, B, d, dst);
+    DCAT_LAUNCH_CHECK();
+}
+template void gather_rows<float>(const float*, const int32_t*, int64_t, int, float*, cudaStream_t);
+template void gather_rows<bf16>(const float*, const int32_t*, int64_t, int, bf16*, cudaStream_t);
+
 void pool_selectors(const int64_t* tok_off, int b_u, const float* H, int d, int last, float* sel, cudaStream_t s) {
     if (b_u <= 0) return;
     k_pool<<<b_u, 128, 0, s>>>(tok_off, b_u, H, d, last, sel);

@@ -130,6 +130,9 @@ struct CandParams {
     int aux_first;          // 1: (lookup + aux) + pos as build_input (finetune.cpp:193-203, AuxLt);
                             // 0: (lookup + pos) + aux as the batched Aux path (finetune.cpp:468-479)
 };
+// candidate_inputs (dcat.cpp:180-197): e[n x d_emb] fp32 = lookup(items) + pos_emb[pos]
+void candidate_inputs(const EmbParams& ep, const uint64_t* items, const int32_t* pos, int64_t n, float* e, Status* st,
+                      cudaStream_t s);
 template <typename T>
 void gather_candidates(const DedupIn& in, const DedupOut& o, const EmbParams& ep, const CandParams& cp, int64_t B,
                        T* E, int ldE, T* feat, cudaStream_t s);
@@ -219,6 +222,10 @@ void attention_fa(const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream
 // ---------------------------------------------------------------- head / scatter
 void scatter_outputs(const int32_t* perm, int64_t B, const float* logits_p, const float* mlog_p, const float* h_p,
                      int d, float* logits, float* mlogits, float* h_cand, cudaStream_t s);
+// dst[p] = src[perm[p]] (fp32 rows -> activation type); scatter_rows: dst[perm[p]] = src[p]
+template <typename T>
+void gather_rows(const float* src, const int32_t* perm, int64_t B, int d, T* dst, cudaStream_t s);
+void scatter_rows(const float* src, const int32_t* perm, int64_t B, int d, float* dst, cudaStream_t s);
 // Lite selectors (gather_selectors, finetune.cpp:258-274): per unique, the mean (row-order sum,
 // then one division) or the last of its token rows of H (fp32, ld d); zeros when it has none.
 void pool_selectors(const int64_t* tok_off, int b_u, const float* H, int d, int last, float* sel, cudaStream_t s);
