@@ -201,6 +201,11 @@ typedef struct dcat_call_stats {
 } dcat_call_stats;
 int dcat_last_stats(dcat_model* m, dcat_call_stats* out);
 
+/* Page-locked host memory for staging batches (cudaHostAlloc): copies from it to the device are
+ * asynchronous DMA. Used by the C++ shim to pack std::vector<RankingExample> batches. */
+int dcat_host_alloc(uint64_t bytes, void** out);
+int dcat_host_free(void* p);
+
 /* ---- The DCAT sub-API (dcat.hpp:47-78) with a device-resident K/V cache ----------------------
  * context_forward (dcat.hpp:47-49, dcat.cpp:137-178) / context_forward_fixed (dcat.hpp:95-98,
  * dcat.cpp:281-336) -> dcat_kv (KVCache / FixedKVCache, dcat.hpp:30-41, 65-78, kept on the device),

@@ -51,6 +51,8 @@ def lib() -> C.CDLL:
         L.dcat_context_forward.argtypes = [C.c_void_p, P(BatchC), C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                            C.c_void_p, P(C.c_void_p)]
         L.dcat_kv_destroy.argtypes = [C.c_void_p]
+        L.dcat_host_alloc.argtypes = [C.c_uint64, P(C.c_void_p)]
+        L.dcat_host_free.argtypes = [C.c_void_p]
         L.dcat_kv_info.argtypes = [C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32), C.c_void_p]
         L.dcat_kv_read.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
         L.dcat_candidate_inputs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
@@ -64,7 +66,7 @@ def lib() -> C.CDLL:
 EXPORTS = ("dcat_last_error", "dcat_version", "dcat_model_create", "dcat_model_destroy", "dcat_dedup",
            "dcat_rank_forward_batch", "dcat_debug_kv", "dcat_stage_times", "dcat_last_stats",
            "dcat_debug_counters", "dcat_context_forward", "dcat_kv_destroy", "dcat_kv_info", "dcat_kv_read",
-           "dcat_candidate_inputs", "dcat_cross_forward")
+           "dcat_candidate_inputs", "dcat_cross_forward", "dcat_host_alloc", "dcat_host_free")
 
 
 def _check(rc: int):

@@ -1609,6 +1609,20 @@ int dcat_context_forward(dcat_model* m, const dcat_batch* uniques, int32_t windo
     });
 }
 
+int dcat_host_alloc(uint64_t bytes, void** out) {
+    if (!out) return set_err(DCAT_EINVAL, "null argument");
+    *out = nullptr;
+    return guarded(nullptr, [&]() -> int {
+        DCAT_CUDA_CHECK(cudaHostAlloc(out, std::max<uint64_t>(bytes, 16), cudaHostAllocPortable));
+        return DCAT_OK;
+    });
+}
+
+int dcat_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+    return DCAT_OK;
+}
+
 int dcat_kv_destroy(dcat_kv* kv) {
     if (!kv) return DCAT_OK;
     cudaSetDevice(kv->device);

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <stdexcept>
+#include <thread>
 #include <vector>
 
 #include "seqfm/dcat.hpp"
@@ -83,7 +84,7 @@ static void check_rank(const char* name, const ModelConfig& mc, int L, int users
     Rng ar(5);
     for (auto& x : rp.aux_proj.v.a) x = 0.3f * static_cast<float>(ar.normal());
     Rng rng(77);
-    auto batch = make_batch(users, cands, L, v == FusionVariant::Aux ? 4 : 0, rng, with_empty);
+    auto batch = make_batch(users, cands, L, v == FusionVariant::Aux || v == FusionVariant::AuxLt ? 4 : 0, rng, with_empty);
     auto ref = seqfm::rank_forward_batch(p, table, rp, batch, cfg);
     b200::Scorer sc(p, table, rp);
     for (int fp32 = 1; fp32 >= 0; fp32--) {
@@ -119,6 +120,7 @@ int main() {
     tiny.d_emb = 8;
     check_rank("tiny base", tiny, 4, 5, 3, FusionVariant::Base, false);
     check_rank("tiny aux", tiny, 4, 5, 3, FusionVariant::Aux, false);
+    check_rank("tiny aux-lt", tiny, 4, 5, 3, FusionVariant::AuxLt, false);
     check_rank("tiny base + empty seq", tiny, 4, 5, 3, FusionVariant::Base, true);
     ModelConfig base;
     base.d_model = 256;
@@ -248,6 +250,142 @@ int main() {
         for (size_t i = 0; i < ref.size(); i++)
             for (int k = 0; k < kRankHeadCount; k++) mb = std::max(mb, std::fabs(free_fn[i].logit[k] - ref[i].logit[k]));
         EXPECT(mb <= 3e-2, "quantized table via the free function");
+    }
+
+    // 3d. the DCAT sub-API with a device cache: context_forward -> candidate_inputs ->
+    // cross_forward (+ the fixed pair) against the reference's own functions (dcat.hpp:47-101)
+    {
+        ModelConfig c;
+        c.d_model = 64;
+        c.n_layers = 2;
+        c.n_heads = 4;
+        c.d_emb = 64;
+        c.max_len = 40;
+        TransformerParams p;
+        p.init(c, 303, 0.3f);
+        HashedEmbeddingTable table(8, 256, 8, 31);
+        RankingHeadParams rp;
+        rp.init(64, 64, 16, 8, 64, 1, 11);
+        Rng r5(41);
+        auto batch = make_batch(5, 4, 30, 0, r5, true);
+        std::vector<Segment> segs, uniques;
+        std::vector<u64> items;
+        for (auto& ex : batch) {
+            segs.push_back(ex.seq);
+            items.push_back(ex.candidate);
+        }
+        DedupPlan plan = dedup_segments(segs, &uniques);
+        std::vector<Mat> h_ref;
+        KVCache ref_cache = context_forward(p, table, uniques, true, &h_ref);
+        std::vector<int> pos;
+        for (int i = 0; i < plan.b; i++) pos.push_back(uniques[static_cast<size_t>(plan.rep[static_cast<size_t>(i)])].valid);
+        Mat e_ref = candidate_inputs(p, table, items, pos);
+        Mat x_ref = cross_forward(p, ref_cache, plan, e_ref);
+        b200::Scorer sc(p, table, rp);
+        sc.set_fp32(true);
+        std::vector<Mat> h_dev;
+        b200::DeviceKVCache dc = sc.context_forward(uniques, true, &h_dev);
+        KVCache got = dc.to_host();
+        double mk = 0, mh = 0;
+        for (size_t u = 0; u < uniques.size(); u++) {
+            EXPECT(got.seqs[u].n == ref_cache.seqs[u].n, "SeqKV::n");
+            for (int l = 0; l < c.n_layers; l++)
+                for (size_t i = 0; i < got.seqs[u].k[static_cast<size_t>(l)].a.size(); i++) {
+                    mk = std::max(mk, static_cast<double>(std::fabs(got.seqs[u].k[static_cast<size_t>(l)].a[i] -
+                                                                    ref_cache.seqs[u].k[static_cast<size_t>(l)].a[i])));
+                    mk = std::max(mk, static_cast<double>(std::fabs(got.seqs[u].v[static_cast<size_t>(l)].a[i] -
+                                                                    ref_cache.seqs[u].v[static_cast<size_t>(l)].a[i])));
+                }
+            for (size_t i = 0; i < h_dev[u].a.size(); i++)
+                mh = std::max(mh, static_cast<double>(std::fabs(h_dev[u].a[i] - h_ref[u].a[i])));
+        }
+        Mat e_dev = sc.candidate_inputs(items, pos);
+        double me = 0, mx = 0;
+        for (size_t i = 0; i < e_dev.a.size(); i++) me = std::max(me, static_cast<double>(std::fabs(e_dev.a[i] - e_ref.a[i])));
+        Mat x_dev = sc.cross_forward(dc, plan, e_ref);
+        for (size_t i = 0; i < x_dev.a.size(); i++) mx = std::max(mx, static_cast<double>(std::fabs(x_dev.a[i] - x_ref.a[i])));
+        std::printf("sub-API fp32: K/V max abs %.3e, h_user %.3e, candidate_inputs %.3e, cross rows %.3e\n", mk, mh, me, mx);
+        EXPECT(mk <= 1e-5 && mh <= 1e-4 && me <= 1e-6 && mx <= 1e-4, "sub-API vs context_forward / cross_forward");
+        // the free functions with the reference signatures (bf16, cached model)
+        b200::DeviceKVCache fc = b200::context_forward(p, table, uniques, false);
+        Mat xb = b200::cross_forward(p, fc, plan, b200::candidate_inputs(p, table, items, pos));
+        double mb = 0;
+        for (size_t i = 0; i < xb.a.size(); i++) mb = std::max(mb, static_cast<double>(std::fabs(xb.a[i] - x_ref.a[i])));
+        std::printf("sub-API free functions bf16: cross rows max abs %.3e\n", mb);
+        EXPECT(mb <= 2e-2, "free-function sub-API");
+        for (int window : {1, 5, 16}) {
+            FixedKVCache rf = context_forward_fixed(p, table, uniques, window, 2);
+            std::vector<int> kpos;
+            for (int i = 0; i < plan.b; i++) kpos.push_back(rf.seqs[static_cast<size_t>(plan.rep[static_cast<size_t>(i)])].kept);
+            Mat ef = candidate_inputs(p, table, items, kpos);
+            Mat xr = cross_forward_fixed(p, rf, plan, ef);
+            b200::DeviceKVCache df = sc.context_forward_fixed(uniques, window, 2);
+            Mat xd = sc.cross_forward_fixed(df, plan, ef);
+            double m = 0;
+            for (size_t i = 0; i < xd.a.size(); i++) m = std::max(m, static_cast<double>(std::fabs(xd.a[i] - xr.a[i])));
+            std::printf("sub-API fixed window %d: cross rows max abs %.3e\n", window, m);
+            EXPECT(m <= 1e-4, "cross_forward_fixed via the device cache");
+        }
+        bool threw = false;
+        try {
+            DedupPlan bad = plan;
+            bad.b_u += 1;
+            sc.cross_forward(dc, bad, e_ref);
+        } catch (const std::runtime_error& e) {
+            threw = std::string(e.what()).find("uniques, plan") != std::string::npos;
+        }
+        EXPECT(threw, "cross_forward plan / cache mismatch must throw");
+    }
+
+    // 3e. one Scorer shared by several threads (calls are serialised per handle) and the free
+    // function's weight fingerprint (in-place weight edits are picked up without invalidate())
+    {
+        ModelConfig c;
+        c.d_model = 32;
+        c.n_layers = 1;
+        c.n_heads = 2;
+        c.d_emb = 32;
+        c.max_len = 20;
+        TransformerParams p;
+        p.init(c, 71, 0.3f);
+        HashedEmbeddingTable table(4, 64, 8, 9);
+        RankingHeadParams rp;
+        FinetuneConfig cfg;
+        cfg.max_events = 16;
+        rp.init(32, 32, cfg.d_aux, cfg.n_ctx(), cfg.crossing_hidden, 1, 13);
+        Rng r6(23);
+        auto batch = make_batch(6, 5, 16, 0, r6, false);
+        b200::Scorer sc(p, table, rp);
+        auto one = sc.rank_forward_batch(batch, cfg);
+        std::vector<std::thread> th;
+        std::vector<int> ok(8, 0);
+        for (int t = 0; t < 8; t++)
+            th.emplace_back([&, t] {
+                bool same = true;
+                for (int it = 0; it < 5; it++) {
+                    auto got = sc.rank_forward_batch(batch, cfg);
+                    for (size_t i = 0; i < got.size(); i++)
+                        for (int k = 0; k < kRankHeadCount; k++) same = same && got[i].logit[k] == one[i].logit[k];
+                }
+                ok[static_cast<size_t>(t)] = same;
+            });
+        for (auto& x : th) x.join();
+        int all = 0;
+        for (int v : ok) all += v;
+        std::printf("8 threads x 5 calls on one Scorer: %d / 8 bit-identical\n", all);
+        EXPECT(all == 8, "shared Scorer under concurrency");
+        auto before = b200::rank_forward_batch(p, table, rp, batch, cfg);
+        for (auto& x : p.layers[0].wq.v.a) x *= 3.0f;  // in place: same object addresses
+        auto after = b200::rank_forward_batch(p, table, rp, batch, cfg);
+        auto ref = rank_forward_batch(p, table, rp, batch, cfg);
+        double m = 0, moved = 0;
+        for (size_t i = 0; i < ref.size(); i++)
+            for (int k = 0; k < kRankHeadCount; k++) {
+                m = std::max(m, std::fabs(after[i].logit[k] - ref[i].logit[k]));
+                moved = std::max(moved, std::fabs(after[i].logit[k] - before[i].logit[k]));
+            }
+        std::printf("weights edited in place: new scores follow the reference (max abs %.3e, moved %.3e)\n", m, moved);
+        EXPECT(m <= 3e-2 && moved > 1e-6, "fingerprinted weight cache");
     }
 
     // 4. errors surface as std::runtime_error (SEQFM_CHECK)
