@@ -182,7 +182,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2507_12704_b200.sharding import ScoreGather
     from paper_2507_12704_b200.sharding import local_batch, shard_rows
     glob = make_batch(U * world, C, L, seed=1, layout="interleaved", shared_storage=not args.private_rows)
-    shards = shard_rows(glob, world)
+    shards = shard_rows(glob, world, spec.n_layers, spec.d_model, spec.n_heads, spec.d_emb)
     host = local_batch(glob, shards[rank]) if world > 1 else glob
     B = host.n_rows
     B_total = glob.n_rows

@@ -62,13 +62,30 @@ class CallStatsC(C.Structure):
                 ("gemm_launches", C.c_int64), ("gemm_flops", C.c_double), ("attn_flops", C.c_double)]
 
 
-def ptr(a) -> Optional[int]:
-    """Raw address of a numpy array or torch tensor (None for None)."""
+def ptr(a, dtype=None, name: str = "array") -> Optional[int]:
+    """Raw address of a numpy array or torch tensor (None for None), after checking what the C
+    side will read: C-contiguous layout and, when given, the element type (the ABI reads raw
+    bytes, so an int64 row_valid or a float32 age would be silently misread)."""
     if a is None:
         return None
     if isinstance(a, np.ndarray):
-        assert a.flags["C_CONTIGUOUS"], "arrays handed to the ABI must be C-contiguous"
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name}: arrays handed to the ABI must be C-contiguous")
+        if dtype is not None and a.dtype != np.dtype(dtype):
+            raise TypeError(f"{name}: expected {np.dtype(dtype)}, got {a.dtype}")
         return a.ctypes.data
+    if not hasattr(a, "data_ptr"):
+        raise TypeError(f"{name}: expected a numpy array or a torch tensor, got {type(a).__name__}")
+    if not a.is_contiguous():
+        raise ValueError(f"{name}: tensors handed to the ABI must be contiguous")
+    if dtype is not None:
+        import torch
+        # uint64 arrays travel as int64 tensors (same bytes; torch has no general uint64)
+        want = {np.dtype(np.int64): (torch.int64,), np.dtype(np.uint64): (torch.int64, torch.uint64),
+                np.dtype(np.int32): (torch.int32,), np.dtype(np.uint8): (torch.uint8,),
+                np.dtype(np.float64): (torch.float64,), np.dtype(np.float32): (torch.float32,)}[np.dtype(dtype)]
+        if a.dtype not in want:
+            raise TypeError(f"{name}: expected {np.dtype(dtype)}, got {a.dtype}")
     return a.data_ptr()  # torch.Tensor
 
 
@@ -186,9 +203,20 @@ class Batch:
 
     def c(self) -> BatchC:
         d_aux = 0 if self.aux is None else int(self.aux.shape[1])
-        return BatchC(self.n_rows, ptr(self.row_offset), ptr(self.row_valid), self.n_events,
-                      ptr(self.ev_ts), ptr(self.ev_action), ptr(self.ev_surface), ptr(self.ev_item),
-                      ptr(self.candidate), ptr(self.age_seconds), ptr(self.aux), d_aux)
+        dev = [hasattr(getattr(self, f), "device") for f in ("row_offset", "row_valid", "ev_ts", "candidate")]
+        if any(dev) and not all(dev):
+            raise ValueError("batch arrays must all be host (numpy) or all device (torch) arrays")
+        if self.row_valid.shape[0] != self.n_rows or self.candidate.shape[0] != self.n_rows or \
+                self.age_seconds.shape[0] != self.n_rows:
+            raise ValueError("batch: per-row arrays differ in length")
+        if not (self.ev_action.shape[0] == self.ev_surface.shape[0] == self.ev_item.shape[0] == self.n_events):
+            raise ValueError("batch: event arrays differ in length")
+        return BatchC(self.n_rows, ptr(self.row_offset, np.int64, "row_offset"),
+                      ptr(self.row_valid, np.int32, "row_valid"), self.n_events,
+                      ptr(self.ev_ts, np.uint64, "ev_ts"), ptr(self.ev_action, np.uint8, "ev_action"),
+                      ptr(self.ev_surface, np.uint8, "ev_surface"), ptr(self.ev_item, np.uint64, "ev_item"),
+                      ptr(self.candidate, np.uint64, "candidate"), ptr(self.age_seconds, np.float64, "age_seconds"),
+                      ptr(self.aux, np.float32, "aux"), d_aux)
 
     def to(self, fn) -> "Batch":
         """Apply fn to every array (e.g. move to device)."""

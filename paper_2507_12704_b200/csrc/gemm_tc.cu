@@ -1618,7 +1618,11 @@ int ffn_trace_read(unsigned long long* out, int cap) {
 }
 #endif
 
-bool ffn_tc_supported(int D, int F) { return (D == 64 || D == 128 || D == 256) && F % 128 == 0 && F <= 1024; }
+// D = 256 runs FFN1 of two hidden chunks as one N = 256 MMA (PAIR_N): the chunk count F / 128 must
+// be even there, or the kernel would read the W1 blocks of a chunk that does not exist
+bool ffn_tc_supported(int D, int F) {
+    return (D == 64 || D == 128 || D == 256) && F % 128 == 0 && F <= 1024 && (D != 256 || (F / 128) % 2 == 0);
+}
 
 void ffn_tc(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M, int D, int F, const Epi& e,
             cudaStream_t s) {
@@ -1643,7 +1647,9 @@ void ffn_tc(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M, int
     }
 }
 
-bool layer_tail_tc_supported(int D, int F) { return (D == 128 || D == 256) && F % 128 == 0 && F <= 1024; }
+bool layer_tail_tc_supported(int D, int F) {
+    return (D == 128 || D == 256) && F % 128 == 0 && F <= 1024 && (D != 256 || (F / 128) % 2 == 0);
+}
 
 void layer_tail_tc(const bf16* A_o, int lda, const bf16* Wot, const bf16* W1t, const bf16* W2t, int M, int D, int F,
                    const Epi& e, cudaStream_t s) {

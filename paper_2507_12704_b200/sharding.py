@@ -54,14 +54,37 @@ def row_content_hash(b: Batch) -> np.ndarray:
     return h[inv]
 
 
-def shard_rows(b: Batch, world: int, token_cost: float = 13.0, cand_cost: float = 20.0) -> List[np.ndarray]:
+# Throughputs of the cost model (B200, measured at PinFM-base): tensor-core GEMM flops
+# and softmax exponentials per second of one GPU.
+GEMM_FLOPS_PER_S = 6.0e14
+EXP_PER_S = 2.5e12
+
+
+def unique_cost(n_u: np.ndarray, c_u: np.ndarray, n_layers: int, d_model: int, n_heads: int,
+                d_emb: int = 0) -> np.ndarray:
+    """Seconds of device work of a unique with n_u context tokens and c_u candidates (SURVEY
+    §8(e): alpha l n^2 d + beta l n d^2 + gamma C l (d^2 + n d)): the context pass (phi_in, l - 1
+    full layers + the last layer's K/V, 24 d^2 flops per token-layer, and the causal softmax
+    H n (n + 1) / 2 exponentials per layer) and the crossing pass (phi_in / phi_out, l layers and
+    H (n + 1) exponentials per candidate-layer)."""
+    d, de = float(d_model), float(d_emb or d_model)
+    n = n_u.astype(np.float64)
+    c = c_u.astype(np.float64)
+    tok_flops = 2 * (de * d + d * d) + (n_layers - 1) * 24 * d * d + 4 * d * d
+    ctx = n * tok_flops / GEMM_FLOPS_PER_S + (n_layers - 1) * n_heads * n * (n + 1) / 2 / EXP_PER_S
+    cand_flops = 2 * (de * d + d * d) + n_layers * 24 * d * d + 4 * d * d
+    cross = c * (cand_flops / GEMM_FLOPS_PER_S + n_layers * n_heads * (n + 1) / EXP_PER_S)
+    return ctx + cross
+
+
+def shard_rows(b: Batch, world: int, n_layers: int = 4, d_model: int = 256, n_heads: int = 8,
+               d_emb: int = 0) -> List[np.ndarray]:
     """Row indices of each rank: user-disjoint, in original row order.
 
-    Uniques (rows of equal content) are assigned whole, longest-processing-time
-    first, on the cost model t_u = token_cost * n_u + cand_cost * C_u (ns per
-    context token / per candidate measured on B200 at PinFM-base), so ranks
-    finish together; ties break on the content hash, so the split depends only
-    on the batch content."""
+    Uniques (rows of equal content) are assigned whole, longest-processing-time first, on the
+    model's cost (unique_cost: quadratic context attention, linear GEMMs, per-candidate crossing),
+    so ranks finish together on ragged real traffic at any model size; ties break on the content
+    hash, so the split depends only on the batch content."""
     if world == 1:
         return [np.arange(b.n_rows)]
     h = row_content_hash(b)
@@ -69,14 +92,16 @@ def shard_rows(b: Batch, world: int, token_cost: float = 13.0, cand_cost: float 
     inv = inv.reshape(-1)
     n_u = np.zeros(len(keys), np.int64)
     n_u[inv] = b.row_valid
-    cost = token_cost * n_u + cand_cost * counts
+    cost = unique_cost(n_u, counts, n_layers, d_model, n_heads, d_emb)
     order = np.lexsort((keys, -cost))
-    load = np.zeros(world)
+    # greedy LPT with a heap of (load, rank): O(U log world)
+    import heapq
+    heap = [(0.0, r) for r in range(world)]
     owner_u = np.empty(len(keys), np.int64)
     for u in order:
-        r = int(np.argmin(load))
+        load, r = heapq.heappop(heap)
         owner_u[u] = r
-        load[r] += cost[u]
+        heapq.heappush(heap, (load + float(cost[u]), r))
     owner = owner_u[inv]
     return [np.nonzero(owner == r)[0] for r in range(world)]
 
@@ -106,7 +131,9 @@ class ScoreGather:
     def __init__(self, rows: List[np.ndarray], n_rows: int, widths, device, dtype=None, group=None, dst: int = 0):
         import torch
         import torch.distributed as dist
+        # dst is a rank of `group`; dist.gather takes the global rank
         self.group, self.dst = group, dst
+        self.dst_global = dist.get_global_rank(group, dst) if group is not None else dst
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.widths = list(widths)
@@ -131,7 +158,7 @@ class ScoreGather:
             self.send[: self.n_local, c:c + w].copy_(t[: self.n_local])
             c += w
         chunks = list(self.recv.chunk(self.world)) if self.recv is not None else None
-        dist.gather(self.send, chunks, dst=self.dst, group=self.group)
+        dist.gather(self.send, chunks, dst=self.dst_global, group=self.group)
         if self.recv is None:
             return None
         return torch.index_select(self.recv, 0, self.src)
@@ -150,7 +177,7 @@ def gather_scores(local: "torch.Tensor", rows: List[np.ndarray], n_rows: int, gr
     pad = torch.zeros((cap, width), dtype=local.dtype, device=local.device)
     pad[: local.shape[0]] = local
     bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
-    dist.gather(pad, bufs, dst=dst, group=group)
+    dist.gather(pad, bufs, dst=dist.get_global_rank(group, dst) if group is not None else dst, group=group)
     if rank != dst:
         return None
     out = torch.empty((n_rows, width), dtype=local.dtype, device=local.device)

@@ -61,6 +61,13 @@ def test_sharding_is_user_disjoint_and_covers_every_row():
         owner[s] = r
     for v in np.unique(h):
         assert len(set(owner[h == v])) == 1  # one content -> one rank
+    # the cost model is config-aware: long sequences weigh quadratically, so at long-seq dims a
+    # 1024-token user outweighs many short ones and the split balances the modelled cost
+    from paper_2507_12704_b200.sharding import unique_cost
+    c_small = unique_cost(np.array([100]), np.array([8]), 4, 256, 8)
+    c_long = unique_cost(np.array([1024]), np.array([8]), 8, 512, 8)
+    assert c_long[0] > 20 * c_small[0]
+    assert unique_cost(np.array([256]), np.array([1]), 4, 256, 8)[0] < unique_cost(np.array([256]), np.array([512]), 4, 256, 8)[0]
     # equal content hashes equal whatever the storage layout
     bs = make_batch(40, 5, 10, seed=3, ragged=True, shared_storage=True, layout="interleaved")
     np.testing.assert_array_equal(row_content_hash(bs), h)
