@@ -150,6 +150,7 @@ typedef struct dcat_batch {
 #define DCAT_INPUT_DEVICE 0x1   /* batch and output pointers are device pointers    */
 #define DCAT_PRECISION_FP32 0x2 /* fp32 storage + SIMT math (parity/debug mode)     */
 #define DCAT_PROFILE 0x4        /* record per-stage CUDA events (dcat_stage_times)  */
+#define DCAT_OUTPUT_DEVICE 0x8  /* output pointers are device pointers (inputs per DCAT_INPUT_DEVICE) */
 
 typedef struct dcat_model dcat_model;
 
@@ -236,6 +237,22 @@ int dcat_candidate_inputs(dcat_model* m, const uint64_t* items, const int32_t* p
  * (fp32, candidate_inputs). The fixed-window cache gives cross_forward_fixed. */
 int dcat_cross_forward(dcat_model* m, const dcat_kv* kv, const int32_t* rep, const float* e_cand, int64_t n,
                        float* h, int32_t flags, void* stream);
+
+/* ---- rank_forward_batch over several GPUs of one box from one process -----------------------
+ * Rows are split user-disjoint by a content hash of their event span (equal sequences always on one
+ * device, so each device's dedup equals the global one), uniques assigned longest-processing-time
+ * first on a config-aware cost; every device scores its rows in its own host thread; the scores
+ * are gathered to devices[0] with one NCCL group (send / recv over NVLink) and returned in the
+ * caller's row order. Host buffers; errors via dcat_multi_last_error(). */
+typedef struct dcat_multi dcat_multi;
+const char* dcat_multi_last_error(void);
+int dcat_multi_create(const dcat_model_config* cfg, const dcat_params* params, const dcat_table* table,
+                      const dcat_head* head, const int32_t* devices, int32_t n_devices, dcat_multi** out);
+int dcat_multi_destroy(dcat_multi* mh);
+int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const dcat_finetune_config* cfg,
+                                  float* logits, float* module_logits, int32_t flags);
+/* the device index (into devices[]) each row of `batch` is scored on */
+int dcat_multi_shard(dcat_multi* mh, const dcat_batch* batch, int32_t* owner);
 
 /* Test instrumentation: device counters of a model created with the environment variable
  * DCAT_DEBUG_COUNTERS set (none otherwise). out[0] = online-softmax rescale events of the causal

@@ -53,6 +53,13 @@ def lib() -> C.CDLL:
         L.dcat_kv_destroy.argtypes = [C.c_void_p]
         L.dcat_host_alloc.argtypes = [C.c_uint64, P(C.c_void_p)]
         L.dcat_host_free.argtypes = [C.c_void_p]
+        L.dcat_multi_last_error.restype = C.c_char_p
+        L.dcat_multi_create.argtypes = [P(ModelConfigC), P(ParamsC), P(TableC), P(HeadC), C.c_void_p, C.c_int32,
+                                        P(C.c_void_p)]
+        L.dcat_multi_destroy.argtypes = [C.c_void_p]
+        L.dcat_multi_rank_forward_batch.argtypes = [C.c_void_p, P(BatchC), P(FinetuneConfigC), C.c_void_p,
+                                                    C.c_void_p, C.c_int32]
+        L.dcat_multi_shard.argtypes = [C.c_void_p, P(BatchC), C.c_void_p]
         L.dcat_kv_info.argtypes = [C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32), C.c_void_p]
         L.dcat_kv_read.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]
         L.dcat_candidate_inputs.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
@@ -66,7 +73,9 @@ def lib() -> C.CDLL:
 EXPORTS = ("dcat_last_error", "dcat_version", "dcat_model_create", "dcat_model_destroy", "dcat_dedup",
            "dcat_rank_forward_batch", "dcat_debug_kv", "dcat_stage_times", "dcat_last_stats",
            "dcat_debug_counters", "dcat_context_forward", "dcat_kv_destroy", "dcat_kv_info", "dcat_kv_read",
-           "dcat_candidate_inputs", "dcat_cross_forward", "dcat_host_alloc", "dcat_host_free")
+           "dcat_candidate_inputs", "dcat_cross_forward", "dcat_host_alloc", "dcat_host_free",
+           "dcat_multi_last_error", "dcat_multi_create", "dcat_multi_destroy", "dcat_multi_rank_forward_batch",
+           "dcat_multi_shard")
 
 
 def _check(rc: int):
@@ -252,6 +261,51 @@ class DcatModel:
         s = CallStatsC()
         _check(lib().dcat_last_stats(self._h, C.byref(s)))
         return {f: getattr(s, f) for f, _ in CallStatsC._fields_}
+
+
+def _check_multi(rc: int):
+    if rc != 0:
+        raise RuntimeError(lib().dcat_multi_last_error().decode())
+
+
+class MultiDcatModel:
+    """rank_forward_batch over several GPUs of one box from this process (the C++ multi-device
+    path, csrc/multi.cu): user-disjoint content-hash shards, one host thread per device, the scores
+    gathered to devices[0] with NCCL and returned in row order."""
+
+    def __init__(self, w: Weights, devices):
+        self.devices = [int(x) for x in devices]
+        devs = np.ascontiguousarray(self.devices, np.int32)
+        h = C.c_void_p()
+        _check_multi(lib().dcat_multi_create(C.byref(w.spec.c()), C.byref(w.params_c()), C.byref(w.table_c()),
+                                             C.byref(w.head_c()), devs.ctypes.data, len(self.devices), C.byref(h)))
+        self._h = h
+
+    def shard(self, batch: Batch) -> np.ndarray:
+        owner = np.zeros(max(batch.n_rows, 1), np.int32)
+        _check_multi(lib().dcat_multi_shard(self._h, C.byref(batch.c()), owner.ctypes.data))
+        return owner[:batch.n_rows]
+
+    def rank_forward_batch(self, batch: Batch, ft: FinetuneSpec, *, precision: str = "bf16", out=None):
+        B = batch.n_rows
+        if out is None:
+            out = (np.zeros((max(B, 1), 3), np.float32), np.zeros((max(B, 1), 3), np.float32))
+        logits, mlog = out
+        flags = FLAG_PRECISION_FP32 if precision == "fp32" else 0
+        _check_multi(lib().dcat_multi_rank_forward_batch(self._h, C.byref(batch.c()), C.byref(ft.c()),
+                                                         logits.ctypes.data, mlog.ctypes.data, flags))
+        return logits[:B], mlog[:B]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dcat_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def probs_from_logits(logits) -> np.ndarray:

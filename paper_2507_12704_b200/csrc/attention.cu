@@ -461,11 +461,7 @@ void launch_simt(const AttnArgs& a, cudaStream_t s) {
 template <int DH, bool CAUSAL, int WARPS, int RT, bool SKIP = false>
 void launch_flash_t(const AttnArgs& a, cudaStream_t s) {
     using C = FlashCfg<DH, CAUSAL, WARPS, RT>;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_flash<DH, CAUSAL, WARPS, RT, SKIP>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    });
+    set_smem_attr(reinterpret_cast<const void*>(k_flash<DH, CAUSAL, WARPS, RT, SKIP>), C::SMEM);
     const dim3 grid(static_cast<unsigned>(a.n_tiles) * static_cast<unsigned>(a.n_heads));
     k_flash<DH, CAUSAL, WARPS, RT, SKIP><<<grid, WARPS * 32, C::SMEM, s>>>(a);
     DCAT_LAUNCH_CHECK();

@@ -659,10 +659,7 @@ void launch_fa(const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t 
     using Sm = FaSmem<DH, CAUSAL>;
     static_assert(Sm::TOTAL <= 227 * 1024, "shared memory budget");
     auto kern = k_attn_fa<DH, CAUSAL, DCAT_FA_POLY>;
-    static std::once_flag once;
-    std::call_once(once, [&] {
-        DCAT_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Sm::TOTAL));
-    });
+    set_smem_attr(reinterpret_cast<const void*>(kern), Sm::TOTAL);
     const int d = a.n_heads * DH;
     const CUtensorMapSwizzle swq =
         DH == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : (DH == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B);

@@ -5,7 +5,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <set>
 #include <string>
+#include <utility>
 
 namespace dcat {
 
@@ -108,4 +111,17 @@ struct InvalidArg {
     int code;
     explicit InvalidArg(std::string m, int c = -1) : msg(std::move(m)), code(c) {}
 };
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute
+// belongs to the device context, so a process driving several GPUs (csrc/multi.cu) sets it on every
+// device it launches on
+inline void set_smem_attr(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    DCAT_CUDA_CHECK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert({func, dev}).second)
+        DCAT_CUDA_CHECK(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
 }  // namespace dcat

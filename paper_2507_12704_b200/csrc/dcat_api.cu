@@ -1406,7 +1406,8 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
         m->last_precision_f32 = f32;
         m->last_vt = m->vt;
         float *dl = logits, *dm = module_logits, *dh = h_cand;
-        if (!device) {
+        const bool out_device = device || (flags & DCAT_OUTPUT_DEVICE);
+        if (!out_device) {
             dl = m->b_out[0].get<float>(B * 3);
             dm = m->b_out[1].get<float>(B * 3);
             dh = h_cand ? m->b_out[2].get<float>(B * m->cfg.d_model) : nullptr;
@@ -1462,7 +1463,7 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
             else run_head_only<bf16>(m, sb, o, *ft, dl, dm, s);
         }
         int t3 = mark(m, s);
-        if (!device) {
+        if (!out_device) {
             DCAT_CUDA_CHECK(cudaMemcpyAsync(logits, dl, sizeof(float) * B * 3, cudaMemcpyDeviceToHost, s));
             DCAT_CUDA_CHECK(cudaMemcpyAsync(module_logits, dm, sizeof(float) * B * 3, cudaMemcpyDeviceToHost, s));
             if (h_cand)

@@ -1499,11 +1499,7 @@ template <int BN, int MODE, bool RB = false>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e, cudaStream_t s) {
     using C = Cfg<BN, MODE, RB>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
-    static std::once_flag once;
-    std::call_once(once, [] {
-        DCAT_CUDA_CHECK(cudaFuncSetAttribute(k_gemm_tc<BN, MODE, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             C::SMEM));
-    });
+    set_smem_attr(reinterpret_cast<const void*>(k_gemm_tc<BN, MODE, RB>), C::SMEM);
     {
         const int npad = (N + 31) & ~31;
         const int need = RB ? BN : MODE == EPI_BIAS ? npad : MODE == EPI_HEAD ? 4 * npad + 3 : 6 * npad + 3;
@@ -1558,11 +1554,7 @@ void launch_ffn(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M,
                 const EpiMaps& mp, cudaStream_t s, const bf16* Wot = nullptr) {
     using C = FfnCfg<D, CL, TAIL>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
-    static std::once_flag once;
-    std::call_once(once, [] {
-        DCAT_CUDA_CHECK(
-            cudaFuncSetAttribute(k_ffn_tc<D, CL, TAIL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-    });
+    set_smem_attr(reinterpret_cast<const void*>(k_ffn_tc<D, CL, TAIL>), C::SMEM);
     const CUtensorMap ta = tmap_bf16(A, static_cast<uint64_t>(D), static_cast<uint64_t>(M),
                                      static_cast<uint64_t>(lda) * 2, 128);
     const CUtensorMap t1 = tmap_bf16(W1t, static_cast<uint64_t>(D), static_cast<uint64_t>(F),

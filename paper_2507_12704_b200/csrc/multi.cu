@@ -1,0 +1,426 @@
+// multi.cu — rank_forward_batch over several GPUs of one box from one host process (C++):
+// the multi-device host path of the reference's batch scorer (finetune.cpp:414-493, called by
+// score_groups finetune.cpp:766-786).
+//
+// The scoring path shards by unique user: a user's context pass, K/V cache and
+// its candidates' crossing pass touch no other user. So
+//   1. rows are keyed by a 64-bit content hash of their event span (equal sequences, equal key),
+//      hashed once per distinct (offset, valid) span by host threads;
+//   2. uniques are assigned whole to devices, longest-processing-time first on a config-aware
+//      cost (context GEMMs linear in n_u, causal softmax quadratic, crossing per candidate), so
+//      each device's own dedup equals the global one and the devices finish together;
+//   3. every device scores its rows in its own host thread (its own dcat_model, streams, CUDA
+//      graphs; no collective inside the scoring pass);
+//   4. the per-row scores are gathered to the first device with one NCCL group of sends / receives
+//      over NVLink, copied to the host once and put back in the caller's row order.
+// NCCL is loaded at run time (libnccl.so.2: the system's or the one a host framework already
+// loaded); a multi-device call fails loudly when it is missing.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <queue>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/dcat_b200.h"
+#include "launch.h"
+
+namespace {
+
+thread_local std::string g_merr;
+int merr(int code, const std::string& m) {
+    g_merr = m;
+    return code;
+}
+
+// ---- NCCL through dlopen (the subset this file uses; nccl.h 2.x ABI)
+typedef struct ncclComm* ncclComm_t;
+typedef int ncclResult_t;
+constexpr int kNcclFloat32 = 7;  // ncclFloat32 / ncclFloat
+struct Nccl {
+    void* h = nullptr;
+    ncclResult_t (*commInitAll)(ncclComm_t*, int, const int*) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+    bool load() {
+        if (h) return true;
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (h) break;
+        }
+        if (!h) return false;
+        commInitAll = reinterpret_cast<decltype(commInitAll)>(dlsym(h, "ncclCommInitAll"));
+        commDestroy = reinterpret_cast<decltype(commDestroy)>(dlsym(h, "ncclCommDestroy"));
+        send = reinterpret_cast<decltype(send)>(dlsym(h, "ncclSend"));
+        recv = reinterpret_cast<decltype(recv)>(dlsym(h, "ncclRecv"));
+        groupStart = reinterpret_cast<decltype(groupStart)>(dlsym(h, "ncclGroupStart"));
+        groupEnd = reinterpret_cast<decltype(groupEnd)>(dlsym(h, "ncclGroupEnd"));
+        errorString = reinterpret_cast<decltype(errorString)>(dlsym(h, "ncclGetErrorString"));
+        return commInitAll && commDestroy && send && recv && groupStart && groupEnd && errorString;
+    }
+};
+Nccl& nccl() {
+    static Nccl n;
+    return n;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != 0) throw dcat::CudaError(std::string(what) + ": " + nccl().errorString(r));
+}
+
+uint64_t mix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+// content key of one event span (the dedup key's fields, dcat.cpp:45-56): equal spans, equal key
+uint64_t span_hash(const dcat_batch& b, int64_t off, int32_t n) {
+    uint64_t acc = 0;
+    for (int32_t i = 0; i < n; i++) {
+        const uint64_t pos = static_cast<uint64_t>(i);
+        uint64_t t = mix64(b.ev_ts[off + i] ^ mix64(pos));
+        t = mix64(t ^ b.ev_item[off + i]);
+        t = mix64(t ^ (static_cast<uint64_t>(b.ev_action[off + i]) | static_cast<uint64_t>(b.ev_surface[off + i]) << 8));
+        acc ^= mix64(t + pos);
+    }
+    return mix64(static_cast<uint64_t>(n) ^ acc);
+}
+
+struct SpanKey {
+    int64_t off;
+    int32_t valid;
+    bool operator==(const SpanKey& o) const { return off == o.off && valid == o.valid; }
+};
+struct SpanKeyHash {
+    size_t operator()(const SpanKey& k) const {
+        return static_cast<size_t>(mix64(static_cast<uint64_t>(k.off) ^ (static_cast<uint64_t>(k.valid) << 40)));
+    }
+};
+
+struct DevState {
+    dcat_model* m = nullptr;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    float* out = nullptr;  // [rows x 6]: logits | module logits (device)
+    size_t out_cap = 0;
+    float* gather = nullptr;  // root only: [B x 6] in shard order
+    size_t gather_cap = 0;
+};
+
+}  // namespace
+
+struct dcat_multi {
+    dcat_model_config cfg{};
+    std::vector<DevState> dev;
+    std::vector<int32_t> last_owner;
+    std::vector<float> host_scores;
+    ~dcat_multi() {
+        for (auto& d : dev) {
+            cudaSetDevice(d.device);
+            cudaDeviceSynchronize();
+            if (d.comm) nccl().commDestroy(d.comm);
+            if (d.out) cudaFree(d.out);
+            if (d.gather) cudaFree(d.gather);
+            if (d.stream) cudaStreamDestroy(d.stream);
+            if (d.m) dcat_model_destroy(d.m);
+        }
+    }
+};
+
+namespace {
+
+// Seconds of device work of a unique (SURVEY §8(e) cost model; throughputs of one B200 at
+// PinFM-base): context GEMMs 24 d^2 flops per token-layer + the causal softmax's
+// H n (n + 1) / 2 exponentials per layer; per candidate its GEMMs and H (n + 1) exponentials per layer.
+double unique_cost(const dcat_model_config& c, double n, double cands) {
+    const double G = 6.0e14, X = 2.5e12, d = c.d_model, de = c.d_emb, l = c.n_layers, H = c.n_heads;
+    const double tok = 2 * (de * d + d * d) + (l - 1) * 24 * d * d + 4 * d * d;
+    const double ctx = n * tok / G + (l - 1) * H * n * (n + 1) / 2 / X;
+    const double cand = 2 * (de * d + d * d) + l * 24 * d * d + 4 * d * d;
+    return ctx + cands * (cand / G + l * H * (n + 1) / X);
+}
+
+// owner device of every row: content-keyed uniques, LPT on unique_cost
+void shard(const dcat_multi* mh, const dcat_batch& b, std::vector<int32_t>& owner) {
+    const int64_t B = b.n_rows;
+    const int nd = static_cast<int>(mh->dev.size());
+    owner.assign(static_cast<size_t>(B), 0);
+    if (nd == 1 || B == 0) return;
+    // distinct spans (rows of one user often share one): hash each once, on host threads
+    std::unordered_map<SpanKey, int64_t, SpanKeyHash> span_id;
+    std::vector<int64_t> row_span(static_cast<size_t>(B));
+    std::vector<std::pair<int64_t, int32_t>> spans;
+    span_id.reserve(static_cast<size_t>(B));
+    for (int64_t r = 0; r < B; r++) {
+        const SpanKey key{b.row_offset[r], b.row_valid[r]};
+        auto it = span_id.find(key);
+        if (it == span_id.end()) {
+            spans.push_back({key.off, key.valid});
+            it = span_id.emplace(key, static_cast<int64_t>(spans.size()) - 1).first;
+        }
+        row_span[static_cast<size_t>(r)] = it->second;
+    }
+    std::vector<uint64_t> sh(spans.size());
+    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; t++)
+        th.emplace_back([&, t] {
+            for (size_t i = t; i < spans.size(); i += T) sh[i] = span_hash(b, spans[i].first, spans[i].second);
+        });
+    for (auto& x : th) x.join();
+    // uniques by content key
+    std::unordered_map<uint64_t, int32_t> uid;
+    std::vector<double> n_u, c_u;
+    std::vector<int32_t> row_u(static_cast<size_t>(B));
+    std::vector<uint64_t> ukey;
+    for (int64_t r = 0; r < B; r++) {
+        const uint64_t k = sh[static_cast<size_t>(row_span[static_cast<size_t>(r)])];
+        auto it = uid.find(k);
+        int32_t u;
+        if (it == uid.end()) {
+            u = static_cast<int32_t>(n_u.size());
+            uid.emplace(k, u);
+            n_u.push_back(b.row_valid[r]);
+            c_u.push_back(0);
+            ukey.push_back(k);
+        } else {
+            u = it->second;
+        }
+        c_u[static_cast<size_t>(u)] += 1;
+        row_u[static_cast<size_t>(r)] = u;
+    }
+    std::vector<int32_t> order(n_u.size());
+    std::vector<double> cost(n_u.size());
+    for (size_t u = 0; u < n_u.size(); u++) {
+        order[u] = static_cast<int32_t>(u);
+        cost[u] = unique_cost(mh->cfg, n_u[u], c_u[u]);
+    }
+    std::sort(order.begin(), order.end(), [&](int32_t a, int32_t c) {
+        return cost[a] != cost[c] ? cost[a] > cost[c] : ukey[a] < ukey[c];
+    });
+    using Load = std::pair<double, int>;
+    std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+    for (int d = 0; d < nd; d++) heap.push({0.0, d});
+    std::vector<int32_t> u_owner(n_u.size());
+    for (int32_t u : order) {
+        Load top = heap.top();
+        heap.pop();
+        u_owner[static_cast<size_t>(u)] = top.second;
+        heap.push({top.first + cost[static_cast<size_t>(u)], top.second});
+    }
+    for (int64_t r = 0; r < B; r++) owner[static_cast<size_t>(r)] = u_owner[static_cast<size_t>(row_u[static_cast<size_t>(r)])];
+}
+
+// one device's rows as a compact host batch (each used span copied once)
+struct LocalBatch {
+    std::vector<int64_t> rows, off;
+    std::vector<int32_t> valid;
+    std::vector<uint64_t> ts, item, cand;
+    std::vector<uint8_t> act, surf;
+    std::vector<double> age;
+    std::vector<float> aux;
+    dcat_batch c{};
+    void build(const dcat_batch& b, const std::vector<int32_t>& owner, int d) {
+        rows.clear();
+        for (int64_t r = 0; r < b.n_rows; r++)
+            if (owner[static_cast<size_t>(r)] == d) rows.push_back(r);
+        const size_t n = rows.size();
+        off.resize(n);
+        valid.resize(n);
+        cand.resize(n);
+        age.resize(n);
+        aux.resize(b.aux ? n * static_cast<size_t>(b.d_aux) : 0);
+        ts.clear();
+        item.clear();
+        act.clear();
+        surf.clear();
+        std::unordered_map<SpanKey, int64_t, SpanKeyHash> copied;  // global span -> local offset
+        for (size_t i = 0; i < n; i++) {
+            const int64_t r = rows[i];
+            const int64_t o = b.row_offset[r];
+            const int32_t v = b.row_valid[r];
+            const SpanKey key{o, v};  // spans of equal start and length are one copy
+            auto it = copied.find(key);
+            if (it == copied.end()) {
+                it = copied.emplace(key, static_cast<int64_t>(ts.size())).first;
+                ts.insert(ts.end(), b.ev_ts + o, b.ev_ts + o + v);
+                item.insert(item.end(), b.ev_item + o, b.ev_item + o + v);
+                act.insert(act.end(), b.ev_action + o, b.ev_action + o + v);
+                surf.insert(surf.end(), b.ev_surface + o, b.ev_surface + o + v);
+            }
+            off[i] = it->second;
+            valid[i] = v;
+            cand[i] = b.candidate[r];
+            age[i] = b.age_seconds[r];
+            if (b.aux) std::memcpy(aux.data() + i * b.d_aux, b.aux + r * b.d_aux, sizeof(float) * b.d_aux);
+        }
+        c = dcat_batch{};
+        c.n_rows = static_cast<int64_t>(n);
+        c.row_offset = off.data();
+        c.row_valid = valid.data();
+        c.n_events = static_cast<int64_t>(ts.size());
+        c.ev_ts = ts.data();
+        c.ev_action = act.data();
+        c.ev_surface = surf.data();
+        c.ev_item = item.data();
+        c.candidate = cand.data();
+        c.age_seconds = age.data();
+        c.aux = b.aux ? aux.data() : nullptr;
+        c.d_aux = b.aux ? b.d_aux : 0;
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* dcat_multi_last_error(void) { return g_merr.c_str(); }
+
+int dcat_multi_create(const dcat_model_config* cfg, const dcat_params* params, const dcat_table* table,
+                      const dcat_head* head, const int32_t* devices, int32_t n_devices, dcat_multi** out) {
+    if (!cfg || !params || !table || !head || !devices || !out || n_devices < 1)
+        return merr(DCAT_EINVAL, "null argument");
+    *out = nullptr;
+    std::unique_ptr<dcat_multi> mh(new dcat_multi());
+    mh->cfg = *cfg;
+    for (int i = 0; i < n_devices; i++)
+        for (int j = 0; j < i; j++)
+            if (devices[i] == devices[j]) return merr(DCAT_EINVAL, "dcat_multi_create: devices must be distinct");
+    try {
+        mh->dev.resize(static_cast<size_t>(n_devices));
+        for (int i = 0; i < n_devices; i++) {
+            DevState& d = mh->dev[static_cast<size_t>(i)];
+            d.device = devices[i];
+            int rc = dcat_model_create(cfg, params, table, head, devices[i], &d.m);
+            if (rc) return merr(rc, dcat_last_error());
+            DCAT_CUDA_CHECK(cudaSetDevice(devices[i]));
+            DCAT_CUDA_CHECK(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+        }
+        if (n_devices > 1) {
+            if (!nccl().load()) return merr(DCAT_EUNSUPPORTED, "dcat_multi_create: libnccl.so.2 not loadable");
+            std::vector<ncclComm_t> comms(static_cast<size_t>(n_devices));
+            nccl_check(nccl().commInitAll(comms.data(), n_devices, devices), "ncclCommInitAll");
+            for (int i = 0; i < n_devices; i++) mh->dev[static_cast<size_t>(i)].comm = comms[static_cast<size_t>(i)];
+        }
+    } catch (const dcat::CudaError& e) {
+        return merr(DCAT_ECUDA, e.msg);
+    }
+    *out = mh.release();
+    return DCAT_OK;
+}
+
+int dcat_multi_destroy(dcat_multi* mh) {
+    delete mh;
+    return DCAT_OK;
+}
+
+int dcat_multi_shard(dcat_multi* mh, const dcat_batch* batch, int32_t* owner) {
+    if (!mh || !batch || !owner) return merr(DCAT_EINVAL, "null argument");
+    std::vector<int32_t> o;
+    shard(mh, *batch, o);
+    std::memcpy(owner, o.data(), sizeof(int32_t) * o.size());
+    return DCAT_OK;
+}
+
+int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const dcat_finetune_config* ft,
+                                  float* logits, float* module_logits, int32_t flags) {
+    if (!mh || !batch || !ft || !logits || !module_logits) return merr(DCAT_EINVAL, "null argument");
+    if (flags & (DCAT_INPUT_DEVICE | DCAT_OUTPUT_DEVICE))
+        return merr(DCAT_EINVAL, "dcat_multi_rank_forward_batch takes host buffers");
+    try {
+        const int nd = static_cast<int>(mh->dev.size());
+        const int64_t B = batch->n_rows;
+        if (B == 0) return DCAT_OK;
+        shard(mh, *batch, mh->last_owner);
+        std::vector<LocalBatch> lb(static_cast<size_t>(nd));
+        for (int d = 0; d < nd; d++) lb[static_cast<size_t>(d)].build(*batch, mh->last_owner, d);
+        // 3. every device scores its rows (device outputs, no host round trip), one host thread each
+        std::vector<int> rc(static_cast<size_t>(nd), 0);
+        std::vector<std::string> msg(static_cast<size_t>(nd));
+        auto work = [&](int d) {
+            DevState& s = mh->dev[static_cast<size_t>(d)];
+            const size_t n = lb[static_cast<size_t>(d)].rows.size();
+            try {
+                DCAT_CUDA_CHECK(cudaSetDevice(s.device));
+                if (n * 6 > s.out_cap) {
+                    if (s.out) DCAT_CUDA_CHECK(cudaFree(s.out));
+                    s.out_cap = n * 6 + n * 6 / 4 + 64;
+                    DCAT_CUDA_CHECK(cudaMalloc(&s.out, s.out_cap * sizeof(float)));
+                }
+                if (n == 0) return;
+                rc[static_cast<size_t>(d)] =
+                    dcat_rank_forward_batch(s.m, &lb[static_cast<size_t>(d)].c, ft, s.out, s.out + n * 3, nullptr,
+                                            (flags & DCAT_PRECISION_FP32) | DCAT_OUTPUT_DEVICE, s.stream);
+                if (rc[static_cast<size_t>(d)]) msg[static_cast<size_t>(d)] = dcat_last_error();
+            } catch (const dcat::CudaError& e) {
+                rc[static_cast<size_t>(d)] = DCAT_ECUDA;
+                msg[static_cast<size_t>(d)] = e.msg;
+            }
+        };
+        std::vector<std::thread> th;
+        for (int d = 1; d < nd; d++) th.emplace_back(work, d);
+        work(0);
+        for (auto& x : th) x.join();
+        for (int d = 0; d < nd; d++)
+            if (rc[static_cast<size_t>(d)]) return merr(rc[static_cast<size_t>(d)], msg[static_cast<size_t>(d)]);
+        // 4. gather to the first device: one NCCL group of sends / receives over NVLink
+        DevState& root = mh->dev[0];
+        DCAT_CUDA_CHECK(cudaSetDevice(root.device));
+        if (static_cast<size_t>(B) * 6 > root.gather_cap) {
+            if (root.gather) DCAT_CUDA_CHECK(cudaFree(root.gather));
+            root.gather_cap = static_cast<size_t>(B) * 6;
+            DCAT_CUDA_CHECK(cudaMalloc(&root.gather, root.gather_cap * sizeof(float)));
+        }
+        std::vector<size_t> at(static_cast<size_t>(nd) + 1, 0);
+        for (int d = 0; d < nd; d++) at[d + 1] = at[d] + lb[static_cast<size_t>(d)].rows.size() * 6;
+        const size_t n0 = lb[0].rows.size();
+        if (n0) DCAT_CUDA_CHECK(cudaMemcpyAsync(root.gather, root.out, n0 * 6 * sizeof(float), cudaMemcpyDeviceToDevice,
+                                                root.stream));
+        if (nd > 1) {
+            nccl_check(nccl().groupStart(), "ncclGroupStart");
+            for (int d = 1; d < nd; d++) {
+                const size_t cnt = at[d + 1] - at[d];
+                if (!cnt) continue;
+                DevState& s = mh->dev[static_cast<size_t>(d)];
+                nccl_check(nccl().send(s.out, cnt, kNcclFloat32, 0, s.comm, s.stream), "ncclSend");
+                nccl_check(nccl().recv(root.gather + at[d], cnt, kNcclFloat32, d, root.comm, root.stream), "ncclRecv");
+            }
+            nccl_check(nccl().groupEnd(), "ncclGroupEnd");
+        }
+        mh->host_scores.resize(static_cast<size_t>(B) * 6);
+        DCAT_CUDA_CHECK(cudaMemcpyAsync(mh->host_scores.data(), root.gather, sizeof(float) * B * 6,
+                                        cudaMemcpyDeviceToHost, root.stream));
+        DCAT_CUDA_CHECK(cudaStreamSynchronize(root.stream));
+        for (int d = 1; d < nd; d++) {
+            DCAT_CUDA_CHECK(cudaSetDevice(mh->dev[static_cast<size_t>(d)].device));
+            DCAT_CUDA_CHECK(cudaStreamSynchronize(mh->dev[static_cast<size_t>(d)].stream));
+        }
+        // back to the caller's row order: device d's block holds its n_d rows as [logits | module logits]
+        for (int d = 0; d < nd; d++) {
+            const auto& rows = lb[static_cast<size_t>(d)].rows;
+            const float* blk = mh->host_scores.data() + at[d];
+            const size_t n = rows.size();
+            for (size_t i = 0; i < n; i++) {
+                std::memcpy(logits + rows[i] * 3, blk + i * 3, 3 * sizeof(float));
+                std::memcpy(module_logits + rows[i] * 3, blk + n * 3 + i * 3, 3 * sizeof(float));
+            }
+        }
+        return DCAT_OK;
+    } catch (const dcat::CudaError& e) {
+        return merr(DCAT_ECUDA, e.msg);
+    } catch (const std::bad_alloc&) {
+        return merr(DCAT_ENOMEM, "host out of memory");
+    }
+}
+
+}  // extern "C"

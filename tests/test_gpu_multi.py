@@ -1,0 +1,64 @@
+"""The C++ multi-device host path (csrc/multi.cu, dcat_multi_*): content-hash user-disjoint
+shards, one host thread per GPU, NCCL gather of the scores to the first GPU. Every row's scores
+must match the single-device call (up to the regrouping of sums a different cache offset brings)."""
+import numpy as np
+import pytest
+
+from oracle import pyoracle
+from paper_2507_12704_b200.abi import FinetuneSpec, ModelSpec
+from paper_2507_12704_b200.synth import make_batch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_mod():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return torch
+
+
+def _setup():
+    orc = pyoracle.oracle()
+    spec = ModelSpec(d_model=256, n_layers=2, n_heads=8, mlp_ratio=4, max_len=130, d_emb=256)
+    w = orc.init_weights(spec, 42, table=(8, 4096, 32, 7, 0.05), head_seed=11)
+    b = make_batch(40, 9, 128, seed=4, ragged=True, shared_storage=False)
+    return orc, spec, w, b
+
+
+@pytest.mark.parametrize("n", [1, 2, 4])
+def test_multi_device_equals_single(torch_mod, n):
+    if torch_mod.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    from paper_2507_12704_b200 import api
+    orc, spec, w, b = _setup()
+    ft = FinetuneSpec(max_events=128)
+    single = api.DcatModel(w, device=0)
+    for precision in ("bf16", "fp32"):
+        l1, m1, _ = single.rank_forward_batch(b, ft, precision=precision)
+        mm = api.MultiDcatModel(w, list(range(n)))
+        ln, mn = mm.rank_forward_batch(b, ft, precision=precision)
+        # a shard places a unique at another cache offset: its key chunks start on another 8-token
+        # boundary, so sums regroup and an attention output can round to the neighbouring bf16
+        # value; the scores agree to well inside the parity tolerance
+        scale = max(1e-3, float(np.abs(l1).max()))
+        tol = 5e-3 if precision == "bf16" else 1e-5
+        assert float(np.abs(ln - l1).max()) <= tol * scale, precision
+        assert float(np.abs(mn - m1).max()) <= tol * max(1e-3, float(np.abs(m1).max())), precision
+        owner = mm.shard(b)
+        # user-disjoint: equal sequences share a device; every device gets work when n <= uniques
+        rep, first, b_u = orc.dedup(b)
+        for u in range(b_u):
+            assert len(set(owner[rep == u].tolist())) == 1
+        if n > 1:
+            assert len(set(owner.tolist())) == n
+        mm.close()
+    rl, rm, _, _ = orc.rank_forward_batch(w, ft, b)
+    assert float(np.abs(l1 - rl).max()) <= 1e-2 * max(1e-3, float(np.abs(rl).max()))
+
+
+def test_multi_devices_must_be_distinct(torch_mod):
+    from paper_2507_12704_b200 import api
+    orc, spec, w, b = _setup()
+    with pytest.raises(RuntimeError, match="distinct"):
+        api.MultiDcatModel(w, [0, 0])
