@@ -23,7 +23,6 @@
 #include <queue>
 #include <string>
 #include <thread>
-#include <unordered_map>
 #include <vector>
 
 #include "../../include/dcat_b200.h"
@@ -95,17 +94,31 @@ uint64_t span_hash(const dcat_batch& b, int64_t off, int32_t n) {
     return mix64(static_cast<uint64_t>(n) ^ acc);
 }
 
-struct SpanKey {
-    int64_t off;
-    int32_t valid;
-    bool operator==(const SpanKey& o) const { return off == o.off && valid == o.valid; }
-};
-struct SpanKeyHash {
-    size_t operator()(const SpanKey& k) const {
-        return static_cast<size_t>(mix64(static_cast<uint64_t>(k.off) ^ (static_cast<uint64_t>(k.valid) << 40)));
+// open-addressing map from a non-zero 64-bit key to an int32 (per-thread scratch: no locking)
+struct FlatMap {
+    std::vector<uint64_t> key;
+    std::vector<int32_t> val;
+    size_t mask = 0;
+    explicit FlatMap(size_t n) {
+        size_t cap = 16;
+        while (cap < 2 * n) cap <<= 1;
+        key.assign(cap, 0);
+        val.assign(cap, -1);
+        mask = cap - 1;
+    }
+    int32_t& slot(uint64_t k, bool* fresh) {
+        size_t i = mix64(k) & mask;
+        while (key[i] != 0 && key[i] != k) i = (i + 1) & mask;
+        *fresh = key[i] == 0;
+        key[i] = k;
+        return val[i];
     }
 };
-
+// a row's event span as one non-zero key (offsets < 2^43, valid < 2^20)
+inline uint64_t span_key(int64_t off, int32_t valid) {
+    return (static_cast<uint64_t>(off) << 20 | static_cast<uint64_t>(valid)) + 1;
+}
+unsigned host_threads() { return std::max(1u, std::min(16u, std::thread::hardware_concurrency())); }
 struct DevState {
     dcat_model* m = nullptr;
     int device = 0;
@@ -115,6 +128,8 @@ struct DevState {
     size_t out_cap = 0;
     float* gather = nullptr;  // root only: [B x 6] in shard order
     size_t gather_cap = 0;
+    void* arena = nullptr;  // page-locked staging of this device's rows
+    size_t arena_bytes = 0;
 };
 
 }  // namespace
@@ -133,6 +148,7 @@ struct dcat_multi {
             if (d.gather) cudaFree(d.gather);
             if (d.stream) cudaStreamDestroy(d.stream);
             if (d.m) dcat_model_destroy(d.m);
+            if (d.arena) dcat_host_free(d.arena);
         }
     }
 };
@@ -150,133 +166,189 @@ double unique_cost(const dcat_model_config& c, double n, double cands) {
     return ctx + cands * (cand / G + l * H * (n + 1) / X);
 }
 
-// owner device of every row: content-keyed uniques, LPT on unique_cost
+// owner device of every row: content-keyed uniques, LPT on unique_cost. Host threads take
+// contiguous row ranges: each content-hashes the distinct spans of its range once (rows of one user
+// usually share a span) and groups its rows by content; the per-thread groups are merged, assigned
+// longest-processing-time first, and mapped back to rows in parallel.
 void shard(const dcat_multi* mh, const dcat_batch& b, std::vector<int32_t>& owner) {
     const int64_t B = b.n_rows;
     const int nd = static_cast<int>(mh->dev.size());
     owner.assign(static_cast<size_t>(B), 0);
     if (nd == 1 || B == 0) return;
-    // distinct spans (rows of one user often share one): hash each once, on host threads
-    std::unordered_map<SpanKey, int64_t, SpanKeyHash> span_id;
-    std::vector<int64_t> row_span(static_cast<size_t>(B));
-    std::vector<std::pair<int64_t, int32_t>> spans;
-    span_id.reserve(static_cast<size_t>(B));
-    for (int64_t r = 0; r < B; r++) {
-        const SpanKey key{b.row_offset[r], b.row_valid[r]};
-        auto it = span_id.find(key);
-        if (it == span_id.end()) {
-            spans.push_back({key.off, key.valid});
-            it = span_id.emplace(key, static_cast<int64_t>(spans.size()) - 1).first;
+    struct Local {
+        std::vector<uint64_t> ukey;  // content hash of each local unique
+        std::vector<int32_t> n, c;   // its tokens and rows
+        std::vector<int32_t> row_u;  // local unique of each row of the range
+        std::vector<int32_t> to_global;
+    };
+    const unsigned T = static_cast<unsigned>(std::min<int64_t>(host_threads(), std::max<int64_t>(1, B / 4096)));
+    std::vector<Local> loc(T);
+    std::vector<int64_t> r0s(T + 1);
+    for (unsigned t = 0; t <= T; t++) r0s[t] = B * t / T;
+    auto group = [&](unsigned t) {
+        Local& L = loc[t];
+        const int64_t r0 = r0s[t], r1 = r0s[t + 1];
+        FlatMap spans(static_cast<size_t>(r1 - r0)), uniq(static_cast<size_t>(r1 - r0));
+        std::vector<uint64_t> span_hashes;
+        L.row_u.resize(static_cast<size_t>(r1 - r0));
+        for (int64_t r = r0; r < r1; r++) {
+            bool fresh;
+            int32_t& si = spans.slot(span_key(b.row_offset[r], b.row_valid[r]), &fresh);
+            if (fresh) {
+                si = static_cast<int32_t>(span_hashes.size());
+                span_hashes.push_back(span_hash(b, b.row_offset[r], b.row_valid[r]));
+            }
+            const uint64_t h = span_hashes[static_cast<size_t>(si)] | 1;  // non-zero map key
+            int32_t& ui = uniq.slot(h, &fresh);
+            if (fresh) {
+                ui = static_cast<int32_t>(L.ukey.size());
+                L.ukey.push_back(h);
+                L.n.push_back(b.row_valid[r]);
+                L.c.push_back(0);
+            }
+            L.c[static_cast<size_t>(ui)]++;
+            L.row_u[static_cast<size_t>(r - r0)] = ui;
         }
-        row_span[static_cast<size_t>(r)] = it->second;
+    };
+    {
+        std::vector<std::thread> th;
+        for (unsigned t = 1; t < T; t++) th.emplace_back(group, t);
+        group(0);
+        for (auto& x : th) x.join();
     }
-    std::vector<uint64_t> sh(spans.size());
-    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    std::vector<std::thread> th;
-    for (unsigned t = 0; t < T; t++)
-        th.emplace_back([&, t] {
-            for (size_t i = t; i < spans.size(); i += T) sh[i] = span_hash(b, spans[i].first, spans[i].second);
-        });
-    for (auto& x : th) x.join();
-    // uniques by content key
-    std::unordered_map<uint64_t, int32_t> uid;
-    std::vector<double> n_u, c_u;
-    std::vector<int32_t> row_u(static_cast<size_t>(B));
-    std::vector<uint64_t> ukey;
-    for (int64_t r = 0; r < B; r++) {
-        const uint64_t k = sh[static_cast<size_t>(row_span[static_cast<size_t>(r)])];
-        auto it = uid.find(k);
-        int32_t u;
-        if (it == uid.end()) {
-            u = static_cast<int32_t>(n_u.size());
-            uid.emplace(k, u);
-            n_u.push_back(b.row_valid[r]);
-            c_u.push_back(0);
-            ukey.push_back(k);
-        } else {
-            u = it->second;
+    // merge the per-thread uniques
+    size_t total = 0;
+    for (auto& L : loc) total += L.ukey.size();
+    FlatMap gmap(total);
+    std::vector<uint64_t> gkey;
+    std::vector<double> gn, gc;
+    for (auto& L : loc) {
+        L.to_global.resize(L.ukey.size());
+        for (size_t i = 0; i < L.ukey.size(); i++) {
+            bool fresh;
+            int32_t& g = gmap.slot(L.ukey[i], &fresh);
+            if (fresh) {
+                g = static_cast<int32_t>(gkey.size());
+                gkey.push_back(L.ukey[i]);
+                gn.push_back(L.n[i]);
+                gc.push_back(0);
+            }
+            gc[static_cast<size_t>(g)] += L.c[i];
+            L.to_global[i] = g;
         }
-        c_u[static_cast<size_t>(u)] += 1;
-        row_u[static_cast<size_t>(r)] = u;
     }
-    std::vector<int32_t> order(n_u.size());
-    std::vector<double> cost(n_u.size());
-    for (size_t u = 0; u < n_u.size(); u++) {
+    const size_t U = gkey.size();
+    std::vector<int32_t> order(U);
+    std::vector<double> cost(U);
+    for (size_t u = 0; u < U; u++) {
         order[u] = static_cast<int32_t>(u);
-        cost[u] = unique_cost(mh->cfg, n_u[u], c_u[u]);
+        cost[u] = unique_cost(mh->cfg, gn[u], gc[u]);
     }
-    std::sort(order.begin(), order.end(), [&](int32_t a, int32_t c) {
-        return cost[a] != cost[c] ? cost[a] > cost[c] : ukey[a] < ukey[c];
+    std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+        return cost[x] != cost[y] ? cost[x] > cost[y] : gkey[x] < gkey[y];
     });
     using Load = std::pair<double, int>;
     std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
     for (int d = 0; d < nd; d++) heap.push({0.0, d});
-    std::vector<int32_t> u_owner(n_u.size());
+    std::vector<int32_t> u_owner(U);
     for (int32_t u : order) {
         Load top = heap.top();
         heap.pop();
         u_owner[static_cast<size_t>(u)] = top.second;
         heap.push({top.first + cost[static_cast<size_t>(u)], top.second});
     }
-    for (int64_t r = 0; r < B; r++) owner[static_cast<size_t>(r)] = u_owner[static_cast<size_t>(row_u[static_cast<size_t>(r)])];
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; t++)
+        th.emplace_back([&, t] {
+            const Local& L = loc[t];
+            for (int64_t r = r0s[t]; r < r0s[t + 1]; r++)
+                owner[static_cast<size_t>(r)] =
+                    u_owner[static_cast<size_t>(L.to_global[static_cast<size_t>(L.row_u[static_cast<size_t>(r - r0s[t])])])];
+        });
+    for (auto& x : th) x.join();
 }
 
 // one device's rows as a compact host batch (each used span copied once)
+// one device's rows as a compact batch (each used span copied once) in the device's page-locked
+// staging arena, so its H2D copies are asynchronous DMA
 struct LocalBatch {
-    std::vector<int64_t> rows, off;
-    std::vector<int32_t> valid;
-    std::vector<uint64_t> ts, item, cand;
-    std::vector<uint8_t> act, surf;
-    std::vector<double> age;
-    std::vector<float> aux;
+    std::vector<int64_t> rows;
     dcat_batch c{};
-    void build(const dcat_batch& b, const std::vector<int32_t>& owner, int d) {
+    void build(const dcat_batch& b, const std::vector<int32_t>& owner, int d, void*& arena, size_t& arena_bytes) {
         rows.clear();
         for (int64_t r = 0; r < b.n_rows; r++)
             if (owner[static_cast<size_t>(r)] == d) rows.push_back(r);
         const size_t n = rows.size();
-        off.resize(n);
-        valid.resize(n);
-        cand.resize(n);
-        age.resize(n);
-        aux.resize(b.aux ? n * static_cast<size_t>(b.d_aux) : 0);
-        ts.clear();
-        item.clear();
-        act.clear();
-        surf.clear();
-        std::unordered_map<SpanKey, int64_t, SpanKeyHash> copied;  // global span -> local offset
+        // pass 1: distinct spans and their local offsets
+        FlatMap copied(n);
+        std::vector<int32_t> row_span(n);
+        std::vector<std::pair<int64_t, int32_t>> spans;
+        std::vector<int64_t> span_off;
+        size_t E = 0;
         for (size_t i = 0; i < n; i++) {
             const int64_t r = rows[i];
-            const int64_t o = b.row_offset[r];
-            const int32_t v = b.row_valid[r];
-            const SpanKey key{o, v};  // spans of equal start and length are one copy
-            auto it = copied.find(key);
-            if (it == copied.end()) {
-                it = copied.emplace(key, static_cast<int64_t>(ts.size())).first;
-                ts.insert(ts.end(), b.ev_ts + o, b.ev_ts + o + v);
-                item.insert(item.end(), b.ev_item + o, b.ev_item + o + v);
-                act.insert(act.end(), b.ev_action + o, b.ev_action + o + v);
-                surf.insert(surf.end(), b.ev_surface + o, b.ev_surface + o + v);
+            bool fresh;  // spans of equal start and length are one copy
+            int32_t& si = copied.slot(span_key(b.row_offset[r], b.row_valid[r]), &fresh);
+            if (fresh) {
+                si = static_cast<int32_t>(spans.size());
+                spans.push_back({b.row_offset[r], b.row_valid[r]});
+                span_off.push_back(static_cast<int64_t>(E));
+                E += static_cast<size_t>(b.row_valid[r]);
             }
-            off[i] = it->second;
-            valid[i] = v;
+            row_span[i] = si;
+        }
+        const int da = b.aux ? b.d_aux : 0;
+        auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+        const size_t o_off = 0, o_valid = al(8 * n), o_cand = al(o_valid + 4 * n), o_age = al(o_cand + 8 * n),
+                     o_aux = al(o_age + 8 * n), o_ts = al(o_aux + 4 * n * static_cast<size_t>(da)), o_item = al(o_ts + 8 * E),
+                     o_act = al(o_item + 8 * E), o_surf = al(o_act + E), total = al(o_surf + E) + 16;
+        if (total > arena_bytes) {
+            if (arena) dcat_host_free(arena);
+            arena = nullptr;
+            arena_bytes = 0;
+            const size_t want = total + total / 4;
+            if (dcat_host_alloc(want, &arena) != DCAT_OK) throw dcat::CudaError("pinned staging allocation failed");
+            arena_bytes = want;
+        }
+        uint8_t* base = static_cast<uint8_t*>(arena);
+        int64_t* off = reinterpret_cast<int64_t*>(base + o_off);
+        int32_t* valid = reinterpret_cast<int32_t*>(base + o_valid);
+        uint64_t* cand = reinterpret_cast<uint64_t*>(base + o_cand);
+        double* age = reinterpret_cast<double*>(base + o_age);
+        float* aux = reinterpret_cast<float*>(base + o_aux);
+        uint64_t* ts = reinterpret_cast<uint64_t*>(base + o_ts);
+        uint64_t* item = reinterpret_cast<uint64_t*>(base + o_item);
+        uint8_t* act = base + o_act;
+        uint8_t* surf = base + o_surf;
+        for (size_t k = 0; k < spans.size(); k++) {  // pass 2: the events of every distinct span
+            const int64_t o = spans[k].first, e0 = span_off[k];
+            const size_t v = static_cast<size_t>(spans[k].second);
+            std::memcpy(ts + e0, b.ev_ts + o, 8 * v);
+            std::memcpy(item + e0, b.ev_item + o, 8 * v);
+            std::memcpy(act + e0, b.ev_action + o, v);
+            std::memcpy(surf + e0, b.ev_surface + o, v);
+        }
+        for (size_t i = 0; i < n; i++) {
+            const int64_t r = rows[i];
+            off[i] = span_off[static_cast<size_t>(row_span[i])];
+            valid[i] = b.row_valid[r];
             cand[i] = b.candidate[r];
             age[i] = b.age_seconds[r];
-            if (b.aux) std::memcpy(aux.data() + i * b.d_aux, b.aux + r * b.d_aux, sizeof(float) * b.d_aux);
+            if (da) std::memcpy(aux + i * da, b.aux + r * da, sizeof(float) * static_cast<size_t>(da));
         }
         c = dcat_batch{};
         c.n_rows = static_cast<int64_t>(n);
-        c.row_offset = off.data();
-        c.row_valid = valid.data();
-        c.n_events = static_cast<int64_t>(ts.size());
-        c.ev_ts = ts.data();
-        c.ev_action = act.data();
-        c.ev_surface = surf.data();
-        c.ev_item = item.data();
-        c.candidate = cand.data();
-        c.age_seconds = age.data();
-        c.aux = b.aux ? aux.data() : nullptr;
-        c.d_aux = b.aux ? b.d_aux : 0;
+        c.row_offset = off;
+        c.row_valid = valid;
+        c.n_events = static_cast<int64_t>(E);
+        c.ev_ts = ts;
+        c.ev_action = act;
+        c.ev_surface = surf;
+        c.ev_item = item;
+        c.candidate = cand;
+        c.age_seconds = age;
+        c.aux = da ? aux : nullptr;
+        c.d_aux = da;
     }
 };
 
@@ -341,14 +413,20 @@ int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const
         const int nd = static_cast<int>(mh->dev.size());
         const int64_t B = batch->n_rows;
         if (B == 0) return DCAT_OK;
+        if (nd == 1) {  // one device: the single-device call on the caller's buffers
+            mh->last_owner.assign(static_cast<size_t>(B), 0);
+            int rc = dcat_rank_forward_batch(mh->dev[0].m, batch, ft, logits, module_logits, nullptr,
+                                             flags & DCAT_PRECISION_FP32, mh->dev[0].stream);
+            return rc ? merr(rc, dcat_last_error()) : DCAT_OK;
+        }
         shard(mh, *batch, mh->last_owner);
-        std::vector<LocalBatch> lb(static_cast<size_t>(nd));
-        for (int d = 0; d < nd; d++) lb[static_cast<size_t>(d)].build(*batch, mh->last_owner, d);
+        std::vector<LocalBatch> lb(static_cast<size_t>(nd));  // built by each device's own thread
         // 3. every device scores its rows (device outputs, no host round trip), one host thread each
         std::vector<int> rc(static_cast<size_t>(nd), 0);
         std::vector<std::string> msg(static_cast<size_t>(nd));
         auto work = [&](int d) {
             DevState& s = mh->dev[static_cast<size_t>(d)];
+            lb[static_cast<size_t>(d)].build(*batch, mh->last_owner, d, s.arena, s.arena_bytes);
             const size_t n = lb[static_cast<size_t>(d)].rows.size();
             try {
                 DCAT_CUDA_CHECK(cudaSetDevice(s.device));
@@ -406,15 +484,18 @@ int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const
             DCAT_CUDA_CHECK(cudaStreamSynchronize(mh->dev[static_cast<size_t>(d)].stream));
         }
         // back to the caller's row order: device d's block holds its n_d rows as [logits | module logits]
-        for (int d = 0; d < nd; d++) {
-            const auto& rows = lb[static_cast<size_t>(d)].rows;
-            const float* blk = mh->host_scores.data() + at[d];
-            const size_t n = rows.size();
-            for (size_t i = 0; i < n; i++) {
-                std::memcpy(logits + rows[i] * 3, blk + i * 3, 3 * sizeof(float));
-                std::memcpy(module_logits + rows[i] * 3, blk + n * 3 + i * 3, 3 * sizeof(float));
-            }
-        }
+        std::vector<std::thread> sc;
+        for (int d = 0; d < nd; d++)
+            sc.emplace_back([&, d] {
+                const auto& rows = lb[static_cast<size_t>(d)].rows;
+                const float* blk = mh->host_scores.data() + at[d];
+                const size_t n = rows.size();
+                for (size_t i = 0; i < n; i++) {
+                    std::memcpy(logits + rows[i] * 3, blk + i * 3, 3 * sizeof(float));
+                    std::memcpy(module_logits + rows[i] * 3, blk + n * 3 + i * 3, 3 * sizeof(float));
+                }
+            });
+        for (auto& x : sc) x.join();
         return DCAT_OK;
     } catch (const dcat::CudaError& e) {
         return merr(DCAT_ECUDA, e.msg);
