@@ -520,10 +520,15 @@ __global__ void __launch_bounds__(384, 1)
                 const int lim_min = __reduce_min_sync(0xffffffffu, lim), lim_max = __reduce_max_sync(0xffffffffu, lim);
                 FA_WAIT(&b.s_full, sc & 1, 7);  // S(sc) ready, and every earlier PV of this pipeline done
                 ptx::tc_fence_after();
+                // a warp whose 32 rows all lie past the tile's queries (sparse crossing tiles: a unique
+                // with few candidates; the last tile of a unique's causal pass) keeps the pipeline's
+                // barrier protocol but does no softmax: its P / O lanes feed rows nobody reads
+                const bool idle = 32 * q >= it.t.nq;  // warp-uniform
                 if (c == 0) {  // O: flush the previous item's, then this item's initial state
                     if (pend_out) flush();
 #pragma unroll
                     for (int jc = 0; jc < DH / 8; jc++) {
+                        if (idle) break;
                         float o[8];
                         if constexpr (CAUSAL) {
 #pragma unroll
@@ -537,9 +542,14 @@ __global__ void __launch_bounds__(384, 1)
                         __syncwarp();
                         if (lane == 0) arrive1(&b.q_empty[qs]);  // slot read (q, k_self, v_self)
                     }
-                    pend_out = true;
+                    pend_out = !idle;
                     pend_row = live ? it.t.q0 + r : -1;
                     pend_hc = hc;
+                }
+                if (idle) {
+                    __syncwarp();
+                    if (lane == 0) arrive1(&b.p_full);
+                    continue;
                 }
                 // Running max by exception: P is computed against the current m (the self logit for the
                 // crossing pass; 0 for a causal item's first chunk, which has no prior). Every p <= the
