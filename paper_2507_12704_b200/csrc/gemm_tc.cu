@@ -73,9 +73,13 @@ struct EpiMaps {
 // every tile of a CTA has the same n0) and streams only A: per 128 x 256 tile the TMA moves
 // 64 KB instead of 192 KB (a per-SM TMA ingress of ~27 B/clk is the bound of these small-K
 // GEMMs; profiles/r01_ffn.md).
-template <int BN, int MODE, bool RB = false>
+// SPL = 2: a full-row epilogue over d = 2 BN columns split across a CTA pair (thread-block cluster
+// of 2): each CTA owns BN columns with double-buffered accumulators, and the per-row statistics
+// (LayerNorm mean / variance, l2 norm) are summed over the pair through distributed shared memory.
+template <int BN, int MODE, bool RB = false, int SPL = 1>
 struct Cfg {
     static_assert(!RB || (MODE == EPI_BIAS && BN == 256), "resident B: EPI_BIAS, BN = 256");
+    static_assert(SPL == 1 || ((MODE == EPI_RESID_LN || MODE == EPI_L2NORM) && BN == 256), "split: full-row, BN 256");
     static constexpr bool FULL = MODE == EPI_RESID_LN || MODE == EPI_L2NORM;
     static constexpr int CG = BN == 64 ? 2 : (FULL ? (BN == 512 ? 1 : 2) : 4);  // epilogue warps per lane quadrant
     static constexpr int EPI_WARPS = 4 * CG;
@@ -98,8 +102,10 @@ struct Cfg {
     static constexpr int RED = MODE == EPI_BIAS ? 0 : 4 * 3 * CG * 32 * 4;  // [quadrant][value][cg][lane]
     // smem params: EPI_BIAS keeps the whole bias (N <= 4096, every N tile of a persistent CTA);
     // full-row / head modes: bias | ln_g | ln_b | mod_w/w2 | mod_b/b2 of one row (d <= 512)
-    static constexpr int PARAM_FLOATS = RB ? BN : MODE == EPI_BIAS ? 4096 : BN == 512 ? 3088 : 1600;
-    static constexpr int SMEM = RING + EPI_SMEM + RED + PARAM_FLOATS * 4 + 1024 + 512;
+    static constexpr int PARAM_FLOATS = RB ? BN : MODE == EPI_BIAS ? 4096 : (BN == 512 || SPL == 2) ? 3088 : 1600;
+    static constexpr int XCH = SPL == 2 ? 2 * 4 * 3 * 32 * 4 + 8 * 8 : 0;  // pair exchange: [set][quadrant][value][lane] + 8 mbarriers
+    static constexpr int SMEM = RING + EPI_SMEM + RED + PARAM_FLOATS * 4 + 512 + XCH + 1024;
+    static_assert((2 * STAGES + 4 + 2 * EPI_WARPS + 1) * 8 + 4 <= 512, "barrier block");
 };
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -266,6 +272,44 @@ __device__ __forceinline__ void quad_reduce(uint32_t red, float* vals, int cg, i
     named_bar(1 + q, CG * 32);
 }
 
+// Split full-row epilogue (SPL = 2): the per-row partials of this CTA's columns plus the
+// partner CTA's, summed in rank order (both CTAs get bit-identical totals). The cg == 0 warp of
+// each quadrant writes its NV partials into the partner's exchange slot over DSMEM and arrives
+// (release.cluster) on the partner's mbarrier; every warp of the quadrant then waits for the
+// partner's partials in its own slot. Slots and barriers alternate by round (set r & 1, phase
+// r >> 1). The quad_reduce barrier that precedes every exchange keeps the partner from reaching
+// round r + 2 before every warp here has read round r: its round r + 1 write follows its own
+// quadrant's barrier, which follows its reads of round r.
+struct PairX {
+    uint32_t slots;   // smem: float [2][4][3][32]
+    uint32_t bars;    // smem: uint64 [2][4]
+    uint32_t round;   // exchanges so far (same count in every epilogue warp of both CTAs)
+    uint32_t rank;    // cluster rank of this CTA (0 / 1)
+};
+template <int NV>
+__device__ __forceinline__ void pair_sum(PairX& X, float* vals, int cg, int lane, int q) {
+    static_assert(NV <= 3, "exchange slot");
+    const uint32_t set = X.round & 1;
+    const uint32_t slot = X.slots + 4u * (((set * 4 + q) * 3) * 32 + lane);
+    const uint32_t bar = X.bars + 8u * (set * 4 + q);
+    if (cg == 0) {
+        const uint32_t rs = ptx::mapa(slot, X.rank ^ 1u);
+#pragma unroll
+        for (int k = 0; k < NV; k++)
+            asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(rs + 128u * k), "f"(vals[k]) : "memory");
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cl(ptx::mapa(bar, X.rank ^ 1u));
+    }
+    while (!ptx::mbar_try_wait_cl(bar, (X.round >> 1) & 1)) {
+    }
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        const float other = lds1(slot + 128u * k);
+        vals[k] = X.rank == 0 ? vals[k] + other : other + vals[k];
+    }
+    X.round++;
+}
+
 // smem parameter layout (floats): [0, N) bias; then per mode
 //   RESID_LN / L2NORM: [P_G, +N) ln_g, [P_B, +N) ln_b; L2NORM: [P_W, +3N) mod_w, [P_W + 3N, +3) mod_b
 //   HEAD: [P_W, +3N) w2, [P_W + 3N, +3) b2
@@ -312,11 +356,11 @@ struct EpiWarp {
     uint32_t hb;       // next bf16 staging buffer (alternates on every bf16 store)
 };
 
-template <int BN, int MODE, bool RB>
+template <int BN, int MODE, bool RB, int SPL = 1>
 __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, uint32_t tacc, EpiWarp& W,
                                               uint32_t red, uint32_t sp, int q, int cg, int lane, int m0, int n0,
-                                              int M, int N, int nvalid, int t, int tiles) {
-    using C = Cfg<BN, MODE, RB>;
+                                              int M, int N, int nvalid, int t, int tiles, int step, PairX& X) {
+    using C = Cfg<BN, MODE, RB, SPL>;
     const ParamLayout PL = param_layout(N);
     const int row_base = m0 + q * 32;
     const int row = row_base + lane;
@@ -389,11 +433,12 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
             o[2] = lg[2] + lds1(b + 8);
         }
     } else {
-        // full-row modes: n0 == 0, nvalid == N == d. Columns past d carry zeros
-        // (TMA zero fill of W and of the residual, zero params) and are masked
-        // out of the centred variance.
+        // full-row modes: n0 == 0, nvalid == N == d (SPL = 2: this CTA's columns [n0, n0 + nvalid) of
+        // d = N, row statistics summed over the pair). Columns past d carry zeros (TMA zero fill of
+        // W and of the residual, zero params) and are masked out of the centred variance.
         const uint32_t F0 = W.ew, H0 = W.ew + 2 * F_BYTES;
-        const float dn = static_cast<float>(nvalid);
+        const float dn = static_cast<float>(SPL == 2 ? N : nvalid);
+        const int pc = SPL == 2 ? n0 : 0;  // global column of local column 0 (params, stores)
         int nchunks = 0;
 #pragma unroll 1
         for (int ch = 0; ch < C::CHUNKS; ch++)
@@ -412,7 +457,7 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
                 tmem_load32(tacc + c, v);
 #pragma unroll
                 for (int i = 0; i < 32; i++) p[i] += v[i];
-                lds32(sp, c, v);
+                lds32(sp, pc + c, v);
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
                     v[i] = p[i] + v[i];  // (acc + resid) + bias
@@ -421,23 +466,23 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
                 }
                 __syncwarp();
                 write_f32_row(F, lane, v);  // the residual slot becomes the x_out slot
-                store_block(&mp.xout, F, c, row_base, lane);
+                store_block(&mp.xout, F, pc + c, row_base, lane);
                 if (e.ln_g == nullptr && e.ln_out) {
                     const uint32_t H = H0 + W.hb * H_BYTES;
                     W.hb ^= 1;
                     staging_free<1>(lane);
                     write_bf16_row(H, lane, v);
-                    store_block(&mp.ln, H, c, row_base, lane);
+                    store_block(&mp.ln, H, pc + c, row_base, lane);
                 }
                 tmem_store32(tacc + c, v);
                 // refill this slot with the residual block two chunks ahead (maybe in a later tile;
                 // full-row GEMMs have one N tile, so tile index -> m0 = tile * BM)
                 const int ahead = (ch + 2) / nchunks;
-                const int ta = t + ahead * static_cast<int>(gridDim.x);
+                const int ta = t + ahead * step;
                 if (lane == 0 && ta < tiles) {
                     bulk_wait_read<0>();  // the x_out store must have read the slot
                     mbar_expect_tx_s(W.rbar + 8 * b, F_BYTES);
-                    tma_load_s(F, &mp.resid, W.rbar + 8 * b, col_lo + ((ch + 2) % nchunks) * 32, ta * BM + q * 32);
+                    tma_load_s(F, &mp.resid, W.rbar + 8 * b, pc + col_lo + ((ch + 2) % nchunks) * 32, ta * BM + q * 32);
                 }
                 W.gc++;
                 __syncwarp();
@@ -449,7 +494,7 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
             for (int ch = 0; ch < nchunks; ch++) {
                 const int c = col_lo + ch * 32;
                 tmem_load32(tacc + c, v);
-                lds32(sp, c, p);
+                lds32(sp, pc + c, p);
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
                     v[i] += p[i];
@@ -458,6 +503,7 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
                 tmem_store32(tacc + c, v);
             }
             quad_reduce<C::CG, 1>(red, ss, cg, lane, q);
+            if constexpr (SPL == 2) pair_sum<1>(X, ss, cg, lane, q);
             const float nrm = sqrtf(ss[0]);
             const float inv = 1.0f / (nrm < 1e-12f ? 1e-12f : nrm);
             float ml[3] = {0.f, 0.f, 0.f};
@@ -473,7 +519,7 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
                 if (e.mod_w) {
 #pragma unroll
                     for (int i = 0; i < 32; i++) {
-                        const uint32_t w = sp + 4u * (PL.P_W + (c + i) * 3);
+                        const uint32_t w = sp + 4u * (PL.P_W + (pc + c + i) * 3);
                         ml[0] += v[i] * lds1(w);
                         ml[1] += v[i] * lds1(w + 4);
                         ml[2] += v[i] * lds1(w + 8);
@@ -483,25 +529,26 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
                     const uint32_t F = F0;
                     staging_free<0>(lane);
                     write_f32_row(F, lane, v);
-                    store_block(&mp.xout, F, c, row_base, lane);
+                    store_block(&mp.xout, F, pc + c, row_base, lane);
                 }
                 if (e.out2) {
                     const uint32_t H = H0;
                     staging_free<0>(lane);
                     write_bf16_row(H, lane, v);
-                    store_block(&mp.out2, H, c, row_base, lane);
+                    store_block(&mp.out2, H, pc + c, row_base, lane);
                 }
                 if (e.ln_g == nullptr && e.ln_out) {
                     const uint32_t H = H0 + H_BYTES;
                     staging_free<0>(lane);
                     write_bf16_row(H, lane, v);
-                    store_block(&mp.ln, H, c, row_base, lane);
+                    store_block(&mp.ln, H, pc + c, row_base, lane);
                 }
                 tmem_store32(tacc + c, v);
             }
             if (e.mod_w) {
                 quad_reduce<C::CG, 3>(red, ml, cg, lane, q);
-                if (live && cg == 0) {
+                if constexpr (SPL == 2) pair_sum<3>(X, ml, cg, lane, q);
+                if (live && cg == 0 && (SPL == 1 || X.rank == 0)) {
                     const uint32_t b = sp + 4u * (PL.P_W + 3 * PL.npad);
                     float* o = e.mlogits + static_cast<size_t>(row) * 3;
                     o[0] = ml[0] + lds1(b);
@@ -512,6 +559,7 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
         }
         if (e.ln_out == nullptr || e.ln_g == nullptr) return;
         quad_reduce<C::CG, 1>(red, s1, cg, lane, q);
+        if constexpr (SPL == 2) pair_sum<1>(X, s1, cg, lane, q);
         const float mu = s1[0] / dn;
         float var[1] = {0.f};
 #pragma unroll 1
@@ -526,31 +574,32 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
             }
         }
         quad_reduce<C::CG, 1>(red, var, cg, lane, q);
+        if constexpr (SPL == 2) pair_sum<1>(X, var, cg, lane, q);
         const float rs = 1.0f / sqrtf(var[0] / dn + 1e-5f);
 #pragma unroll 1
         for (int ch = 0; ch < nchunks; ch++) {
             const int c = col_lo + ch * 32;
             tmem_load32(tacc + c, v);
-            lds32(sp, PL.P_G + c, p);
+            lds32(sp, PL.P_G + pc + c, p);
 #pragma unroll
             for (int i = 0; i < 32; i++) v[i] = p[i] * ((v[i] - mu) * rs);
-            lds32(sp, PL.P_B + c, p);
+            lds32(sp, PL.P_B + pc + c, p);
 #pragma unroll
             for (int i = 0; i < 32; i++) v[i] += p[i];
             const uint32_t H = H0 + W.hb * H_BYTES;
             W.hb ^= 1;
             staging_free<1>(lane);
             write_bf16_row(H, lane, v);
-            store_block(&mp.ln, H, c, row_base, lane);
+            store_block(&mp.ln, H, pc + c, row_base, lane);
         }
     }
 }
 
-template <int BN, int MODE, bool RB>
-__global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
+template <int BN, int MODE, bool RB, int SPL = 1>
+__global__ void __launch_bounds__(Cfg<BN, MODE, RB, SPL>::THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
               const __grid_constant__ Epi e, const __grid_constant__ EpiMaps mp) {
-    using C = Cfg<BN, MODE, RB>;
+    using C = Cfg<BN, MODE, RB, SPL>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -565,10 +614,16 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
     uint64_t* rbars = tempty + 2;  // 2 per epilogue warp
     uint64_t* b_full = rbars + 2 * C::EPI_WARPS;  // resident B loaded
     uint32_t* tslot = reinterpret_cast<uint32_t*>(b_full + 1);
+    // pair exchange (SPL = 2): slots and mbarriers after the 512-byte barrier block
+    const uint32_t s_xch = ptx::smem_u32(full) + 512;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nk = (K + BK - 1) / BK;
-    const int num_n = (N + BN - 1) / BN;
+    // SPL = 2: a cluster of 2 walks the row tiles, CTA rank r owns columns [r BN, (r + 1) BN)
+    const int rank = SPL == 2 ? static_cast<int>(ptx::cluster_rank()) : 0;
+    const int cta0 = SPL == 2 ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+    const int step = SPL == 2 ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
+    const int num_n = SPL == 2 ? 1 : (N + BN - 1) / BN;
     const int tiles = ((M + BM - 1) / BM) * num_n;
 
     if (warp == 0 && lane == 0) {
@@ -584,6 +639,9 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
         }
         for (int b = 0; b < 2 * C::EPI_WARPS; b++) ptx::mbar_init(&rbars[b], 1);
         ptx::mbar_init(b_full, 1);
+        if constexpr (SPL == 2)
+            for (int b = 0; b < 8; b++)
+                ptx::mbar_init(reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(full) + 512 + 3072 + 8 * b), 1);
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc(tslot, C::TMEM_COLS);
@@ -599,6 +657,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if constexpr (SPL == 2) ptx::cluster_sync();  // the partner's exchange barriers are initialised
     ptx::tc_fence_after();
     const uint32_t tmem = *tslot;
 
@@ -613,8 +672,8 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
                         ptx::tma_load_2d(sB + kb * C::B_BYTES + h * C::MMA_N * 128, &tmB, b_full, kb * BK,
                                          n_res + h * C::MMA_N);
             }
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-                const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+            for (int t = cta0; t < tiles; t += step) {
+                const int m0 = (t / num_n) * BM, n0 = SPL == 2 ? rank * BN : (t % num_n) * BN;
                 for (int kb = 0; kb < nk; kb++, it++) {
                     const int s = it % C::STAGES;
                     ptx::mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
@@ -633,7 +692,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
             constexpr uint32_t idesc = ptx::idesc_bf16(BM, C::MMA_N);
             uint32_t it = 0, i = 0;
             if constexpr (RB) ptx::mbar_wait(b_full, 0);
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
+            for (int t = cta0; t < tiles; t += step, i++) {
                 const int buf = i % C::ACC_BUFS;
                 ptx::mbar_wait(&tempty[buf], ((i / C::ACC_BUFS) & 1) ^ 1);
                 ptx::tc_fence_after();
@@ -662,6 +721,11 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
         const int ew = warp - 4;
         const int q = warp & 3, cg = ew >> 2;
         EpiWarp W;
+        PairX X;
+        X.slots = s_xch;
+        X.bars = s_xch + 3072;
+        X.round = 0;
+        X.rank = static_cast<uint32_t>(rank);
         W.ew = s_epi + ew * C::EW;
         W.rbar = ptx::smem_u32(&rbars[2 * ew]);
         W.rph = 0;
@@ -671,28 +735,28 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
             // prime the residual pipeline: global blocks 0 and 1 of this warp
             int nck = 0;
             for (int ch = 0; ch < C::CHUNKS; ch++)
-                if (cg * C::CPW + ch * 32 < N) nck++;
+                if (cg * C::CPW + ch * 32 < (SPL == 2 ? min(BN, N - rank * BN) : N)) nck++;
             if (lane == 0 && nck > 0) {
                 for (int g = 0; g < 2; g++) {
-                    const int ta = blockIdx.x + (g / nck) * gridDim.x;
+                    const int ta = cta0 + (g / nck) * step;
                     if (ta < tiles) {
                         mbar_expect_tx_s(W.rbar + 8 * g, F_BYTES);
-                        tma_load_s(W.ew + g * F_BYTES, &mp.resid, W.rbar + 8 * g, cg * C::CPW + (g % nck) * 32,
-                                   ta * BM + q * 32);
+                        tma_load_s(W.ew + g * F_BYTES, &mp.resid, W.rbar + 8 * g,
+                                   (SPL == 2 ? rank * BN : 0) + cg * C::CPW + (g % nck) * 32, ta * BM + q * 32);
                     }
                 }
             }
             __syncwarp();
         }
         uint32_t i = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, i++) {
+        for (int t = cta0; t < tiles; t += step, i++) {
             const int buf = i % C::ACC_BUFS;
-            const int m0 = (t / num_n) * BM, n0 = (t % num_n) * BN;
+            const int m0 = (t / num_n) * BM, n0 = SPL == 2 ? rank * BN : (t % num_n) * BN;
             ptx::mbar_wait(&tfull[buf], (i / C::ACC_BUFS) & 1);
             ptx::tc_fence_after();
             const uint32_t tacc = tmem + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
-            epilogue_tile<BN, MODE, RB>(e, mp, tacc, W, s_red, s_par, q, cg, lane, m0, n0, M, N, min(BN, N - n0), t,
-                                    tiles);
+            epilogue_tile<BN, MODE, RB, SPL>(e, mp, tacc, W, s_red, s_par, q, cg, lane, m0, n0, M, N,
+                                             min(BN, N - n0), t, tiles, step, X);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[buf]);
@@ -702,6 +766,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB>::THREADS, 1)
     }
     ptx::tc_fence_before();
     __syncthreads();
+    if constexpr (SPL == 2) ptx::cluster_sync();  // no CTA leaves while its partner may still write to it
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, C::TMEM_COLS);
@@ -1496,6 +1561,39 @@ int num_sms() {
 }
 
 template <int BN, int MODE, bool RB = false>
+void launch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e, cudaStream_t s);
+
+// full-row epilogue over d = 512 on a CTA pair (SPL = 2): BN = 256 columns per CTA
+template <int MODE>
+void launch_split(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e, cudaStream_t s) {
+    using C = Cfg<256, MODE, false, 2>;
+    static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
+    auto kern = k_gemm_tc<256, MODE, false, 2>;
+    set_smem_attr(reinterpret_cast<const void*>(kern), C::SMEM);
+    {
+        const int npad = (N + 31) & ~31;
+        if (6 * npad + 3 > C::PARAM_FLOATS)
+            throw InvalidArg("gemm_tc: epilogue parameters of N=" + std::to_string(N) + " exceed the smem staging");
+    }
+    const EpiMaps mp = make_maps(e, M, N);
+    const int m_tiles = (M + BM - 1) / BM;
+    const int pairs = m_tiles < num_sms() / 2 ? m_tiles : num_sms() / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+    cfg.blockDim = dim3(C::THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DCAT_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, M, N, K, e, mp));
+}
+
+template <int BN, int MODE, bool RB>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e, cudaStream_t s) {
     using C = Cfg<BN, MODE, RB>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
@@ -1538,7 +1636,11 @@ void launch_mode(int BN, const CUtensorMap& ta, const CUtensorMap& tb, int M, in
             break;
         case 512:
             if constexpr (MODE == EPI_RESID_LN || MODE == EPI_L2NORM) {
-                launch<512, MODE>(ta, tb, M, N, K, e, s);
+                // d = 512: the row split over a CTA pair (double-buffered accumulators, 8 epilogue
+                // warps per CTA) unless DCAT_NO_PAIR_EPILOGUE selects the one-CTA BN = 512 tile
+                static const bool one_cta = getenv("DCAT_NO_PAIR_EPILOGUE") != nullptr;
+                if (one_cta) launch<512, MODE>(ta, tb, M, N, K, e, s);
+                else launch_split<MODE>(ta, tb, M, N, K, e, s);
                 break;
             }
             [[fallthrough]];
