@@ -129,6 +129,8 @@ __device__ __forceinline__ float4 lds4(uint32_t a) {
 __device__ __forceinline__ void sts1(uint32_t a, float x) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory");
 }
+// read-only parameter vector through L1 (16-byte aligned device arrays)
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ float lds1(uint32_t a) {
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
@@ -255,10 +257,11 @@ __device__ __forceinline__ void staging_free(int lane) {
 }
 
 // sum of NV per-row partials over the CG warps of one lane quadrant (fixed order)
-template <int CG, int NV>
+template <int CG, int NV, int NVS = 3>  // NVS: values per quadrant the buffer is laid out for
 __device__ __forceinline__ void quad_reduce(uint32_t red, float* vals, int cg, int lane, int q) {
+    static_assert(NV <= NVS, "reduction buffer layout");
     if constexpr (CG == 1) return;
-    const uint32_t r = red + 4u * (q * 3 * CG * 32);
+    const uint32_t r = red + 4u * (q * NVS * CG * 32);
 #pragma unroll
     for (int k = 0; k < NV; k++) sts1(r + 4u * ((k * CG + cg) * 32 + lane), vals[k]);
     named_bar(1 + q, CG * 32);
@@ -814,7 +817,7 @@ struct FfnCfg {
     // 256 output columns instead of twice
     static constexpr bool PAIR_N = CL == 1 && D == 256 && DCAT_FFN_PAIR_N;
 #ifndef DCAT_FFN_STAGES256
-#define DCAT_FFN_STAGES256 (DCAT_FFN_PAIR_N ? 4 : 5)
+#define DCAT_FFN_STAGES256 (DCAT_FFN_PAIR_N ? 6 : 5)
 #endif
     static constexpr int STAGES = D == 256 ? DCAT_FFN_STAGES256 : 7;  // weight blocks in flight (L2 latency)
     static_assert(!PAIR_N || STAGES % 2 == 0, "paired N halves need an even ring");
@@ -834,10 +837,12 @@ struct FfnCfg {
     static constexpr int CGF = D >= 128 ? 4 : 2;  // final-epilogue warps per quadrant
     static constexpr int FCOLS = D / CGF;         // final-epilogue columns per warp
     static constexpr int STG = 4096;              // final-epilogue staging per warp (in the H buffers)
-    // b1 (d_ff <= 1024) | b2 | ln_g | ln_b [| bo | ln2_g | ln2_b]
-    static constexpr int PARAM_FLOATS = 1024 + (TAIL ? 6 : 3) * 256 + 32;
-    static constexpr int RED = 4 * 3 * CGF * 32 * 4;
-    static constexpr int SMEM = A_TILE + 2 * H_BUF + STAGES * SLOT + PARAM_FLOATS * 4 + RED + 1024 + 512;
+    // The epilogue parameters (b1 | b2 | ln_g | ln_b [| bo | ln2_g | ln2_b]) are read through L1
+    // (__ldg, every lane of a warp the same address), not staged in shared memory: the 10 KB go
+    // to the weight ring instead. Row statistics: one value per row, [quadrant][cg][lane].
+    static constexpr int RED = 4 * 1 * CGF * 32 * 4;
+    // no alignment slack: the dynamic shared window starts 1 KB-aligned (checked in the kernel)
+    static constexpr int SMEM = A_TILE + 2 * H_BUF + STAGES * SLOT + RED + 512;
     static_assert(EPI_WARPS * STG <= 2 * H_BUF, "final-epilogue staging lives in the H buffers");
     static_assert(FCOLS == 32 || FCOLS == 64, "final epilogue works on one or two 32-column blocks");
     static_assert(CL == 1 || D >= 128, "CTA-pair FFN needs D >= 128");
@@ -883,14 +888,14 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
              const __grid_constant__ CUtensorMap tmW2, const __grid_constant__ CUtensorMap tmWo, int M, int F,
              const __grid_constant__ Epi e, const __grid_constant__ EpiMaps mp) {
     using C = FfnCfg<D, CL, TAIL>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    if (ptx::smem_u32(smem_raw) & 1023) __trap();  // SW128 operands need a 1 KB-aligned window
+    uint8_t* smem = smem_raw;
     uint8_t* sA = smem;
     uint8_t* sH = sA + C::A_TILE;
     uint8_t* ring = sH + 2 * C::H_BUF;
-    const uint32_t s_par = ptx::smem_u32(ring + C::STAGES * C::SLOT);
-    const uint32_t s_red = s_par + C::PARAM_FLOATS * 4;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + C::STAGES * C::SLOT + C::PARAM_FLOATS * 4 + C::RED);
+    const uint32_t s_red = ptx::smem_u32(ring + C::STAGES * C::SLOT);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ring + C::STAGES * C::SLOT + C::RED);
     uint64_t* a_full = bars;
     uint64_t* a_empty = bars + 1;
     uint64_t* full = bars + 2;
@@ -915,8 +920,6 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
     const int units = ((M + 127) / 128 + CL - 1) / CL;  // row tiles of 128 * CL rows
     const int unit0 = blockIdx.x / CL, ustride = gridDim.x / CL;
     const int nch = F / C::CH;
-    const int P_B2 = 1024, P_G = 1024 + 256, P_BB = 1024 + 512;
-    const int P_BO = 1024 + 768, P_G2 = 1024 + 1024, P_BB2 = 1024 + 1280;  // TAIL
     // MMA issue order F1_0 .. F1_{LA-1}, then F1_j, F2_{j-LA}: FFN1 runs LA chunks ahead, so a
     // chunk's GELU overlaps ~2 LA chunk-MMAs and F1_j only needs GELU_{j-2}'s TMEM read.
     constexpr int LA = 2;
@@ -968,20 +971,6 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
     if (warp == 0) {
         if constexpr (CL == 2) ptx::tmem_alloc_pair(tslot, 512);
         else ptx::tmem_alloc(tslot, 512);
-    }
-    if (warp >= 2) {
-        const int tid = threadIdx.x - 64;
-        for (int i = tid; i < 1024; i += 32 * C::EPI_WARPS) sts1(s_par + 4u * i, i < F ? e.bias[i] : 0.f);
-        for (int i = tid; i < 256; i += 32 * C::EPI_WARPS) {
-            sts1(s_par + 4u * (P_B2 + i), i < D ? e.b2[i] : 0.f);
-            sts1(s_par + 4u * (P_G + i), (e.ln_g && i < D) ? e.ln_g[i] : 0.f);
-            sts1(s_par + 4u * (P_BB + i), (e.ln_b && i < D) ? e.ln_b[i] : 0.f);
-            if constexpr (TAIL) {
-                sts1(s_par + 4u * (P_BO + i), i < D ? e.o_bias[i] : 0.f);
-                sts1(s_par + 4u * (P_G2 + i), i < D ? e.ln2_g[i] : 0.f);
-                sts1(s_par + 4u * (P_BB2 + i), i < D ? e.ln2_b[i] : 0.f);
-            }
-        }
     }
     ptx::tc_fence_before();
     if constexpr (CL == 2) ptx::cluster_sync();  // peer barriers initialised before any remote arrival
@@ -1137,7 +1126,9 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                         }
                     }
                     commit(o_full);
+                    FFN_EV(13, 0);
                     ptx::mbar_wait(a2_full, i & 1);  // x_mid in acc2, LN2 rows in the A tile, acc1 free
+                    FFN_EV(14, 0);
                     ptx::tc_fence_after();
                 }
                 for (int j = 0; j < nch + LA; j++) {
@@ -1259,12 +1250,13 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                 bool bad = false;
                 ptx::mbar_wait(o_full, i & 1);
                 ptx::tc_fence_after();
+                if (lane == 0 && ew == 0) FFN_EV(8, 0);
 #pragma unroll 1
                 for (int h = 0; h < C::FCOLS; h += 32) {
                     tmem_load32(tsrc + h, v);
 #pragma unroll
                     for (int j = 0; j < 8; j++) {
-                        const float4 bb = lds4(s_par + 4u * (P_BO + c0 + h + 4 * j));
+                        const float4 bb = ldg4(e.o_bias + c0 + h + 4 * j);
                         float* w = v + 4 * j;
                         w[0] += bb.x;
                         w[1] += bb.y;
@@ -1279,7 +1271,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                     tmem_store32(tacc + h, v);
                 }
                 if (bad && live && e.layer_idx >= 0) atomicMax(&e.st->nonfinite_layer, e.layer_idx + 1);
-                quad_reduce<C::CGF, 1>(s_red, s1, cg, lane, q);
+                quad_reduce<C::CGF, 1, 1>(s_red, s1, cg, lane, q);
                 const float dn = static_cast<float>(D);
                 const float mu = s1[0] / dn;
                 float var[1] = {0.f};
@@ -1292,15 +1284,15 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                         var[0] += d0 * d0;
                     }
                 }
-                quad_reduce<C::CGF, 1>(s_red, var, cg, lane, q);
+                quad_reduce<C::CGF, 1, 1>(s_red, var, cg, lane, q);
                 const float rs = 1.0f / sqrtf(var[0] / dn + 1e-5f);
 #pragma unroll 1
                 for (int h = 0; h < C::FCOLS; h += 32) {
                     tmem_load32(tacc + h, v);
 #pragma unroll
                     for (int j = 0; j < 8; j++) {
-                        const float4 gg = lds4(s_par + 4u * (P_G2 + c0 + h + 4 * j));
-                        const float4 bb = lds4(s_par + 4u * (P_BB2 + c0 + h + 4 * j));
+                        const float4 gg = ldg4(e.ln2_g + c0 + h + 4 * j);
+                        const float4 bb = ldg4(e.ln2_b + c0 + h + 4 * j);
                         float* w = v + 4 * j;
                         w[0] = gg.x * ((w[0] - mu) * rs) + bb.x;
                         w[1] = gg.y * ((w[1] - mu) * rs) + bb.y;
@@ -1320,6 +1312,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(a2_full);
+                if (lane == 0 && ew == 0) FFN_EV(14, 0);
             }
             // ---- GELU chunks: group cg >> 1 takes the chunks in acc1 buffer cg >> 1; this warp
             // owns columns [64 (cg & 1), +64) of them = H k-block cg & 1, all eight 16-byte chunks
@@ -1346,7 +1339,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
 #endif
 #pragma unroll
                     for (int k = 0; k < 32; k += 4) {
-                        float4 bb = lds4(s_par + 4u * (pc + k));
+                        const float4 bb = ldg4(e.bias + pc + k);
                         g[k] = gelu_fast(g[k] + bb.x);
                         g[k + 1] = gelu_fast(g[k + 1] + bb.y);
                         g[k + 2] = gelu_fast(g[k + 2] + bb.z);
@@ -1385,7 +1378,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                     tmem_load32(tacc + h, v);
 #pragma unroll
                     for (int j = 0; j < 8; j++) {  // (resid + acc) + b2
-                        const float4 bb = lds4(s_par + 4u * (P_B2 + c0 + h + 4 * j));
+                        const float4 bb = ldg4(e.b2 + c0 + h + 4 * j);
                         float* w = v + 4 * j;
                         w[0] += bb.x;
                         w[1] += bb.y;
@@ -1414,7 +1407,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                 if (e.ln_out) {
                     float mu = 0.f, rs = 1.f;
                     if (e.ln_g) {
-                        quad_reduce<C::CGF, 1>(s_red, s1, cg, lane, q);
+                        quad_reduce<C::CGF, 1, 1>(s_red, s1, cg, lane, q);
                         const float dn = static_cast<float>(D);
                         mu = s1[0] / dn;
                         float var[1] = {0.f};
@@ -1427,7 +1420,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                                 var[0] += d0 * d0;
                             }
                         }
-                        quad_reduce<C::CGF, 1>(s_red, var, cg, lane, q);
+                        quad_reduce<C::CGF, 1, 1>(s_red, var, cg, lane, q);
                         rs = 1.0f / sqrtf(var[0] / dn + 1e-5f);
                     }
                     staging_free<0>(lane);
@@ -1437,8 +1430,8 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                         if (e.ln_g) {
 #pragma unroll
                             for (int j = 0; j < 8; j++) {
-                                const float4 gg = lds4(s_par + 4u * (P_G + c0 + h + 4 * j));
-                                const float4 bb = lds4(s_par + 4u * (P_BB + c0 + h + 4 * j));
+                                const float4 gg = ldg4(e.ln_g + c0 + h + 4 * j);
+                                const float4 bb = ldg4(e.ln_b + c0 + h + 4 * j);
                                 float* w = v + 4 * j;
                                 w[0] = gg.x * ((w[0] - mu) * rs) + bb.x;
                                 w[1] = gg.y * ((w[1] - mu) * rs) + bb.y;
@@ -1656,6 +1649,20 @@ void launch_ffn(const bf16* A, int lda, const bf16* W1t, const bf16* W2t, int M,
                 const EpiMaps& mp, cudaStream_t s, const bf16* Wot = nullptr) {
     using C = FfnCfg<D, CL, TAIL>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
+    // the epilogues read their parameter vectors as float4 through L1
+    auto vec = [](const float* p, bool need, const char* what) {
+        if ((need && p == nullptr) || (reinterpret_cast<uintptr_t>(p) & 15))
+            throw InvalidArg(std::string("ffn_tc: parameter vector '") + what + "' missing or not 16-byte aligned");
+    };
+    vec(e.bias, true, "b1");
+    vec(e.b2, true, "b2");
+    vec(e.ln_g, false, "ln_g");
+    vec(e.ln_b, e.ln_g != nullptr, "ln_b");
+    if constexpr (TAIL) {
+        vec(e.o_bias, true, "bo");
+        vec(e.ln2_g, true, "ln2_g");
+        vec(e.ln2_b, true, "ln2_b");
+    }
     set_smem_attr(reinterpret_cast<const void*>(k_ffn_tc<D, CL, TAIL>), C::SMEM);
     const CUtensorMap ta = tmap_bf16(A, static_cast<uint64_t>(D), static_cast<uint64_t>(M),
                                      static_cast<uint64_t>(lda) * 2, 128);
@@ -1710,6 +1717,8 @@ int ffn_trace_read(unsigned long long* out, int cap) {
             out[m++] = all[r * FFN_TR_CAP + k] + (static_cast<unsigned long long>(16 * r) << 8);  // code += 16 role
     return m;
 }
+extern "C" void dcat_ffn_trace_reset() { ffn_trace_reset(); }
+extern "C" int dcat_ffn_trace_read(unsigned long long* out, int cap) { return ffn_trace_read(out, cap); }
 #endif
 
 // D = 256 runs FFN1 of two hidden chunks as one N = 256 MMA (PAIR_N): the chunk count F / 128 must

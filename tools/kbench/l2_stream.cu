@@ -269,6 +269,64 @@ void run_multi(EncodeFn enc, void* buf, int grid) {
     std::fflush(stdout);
 }
 
+// One producer WARP, S-slot ring of 16 KB slots, each slot loaded as NL boxes of 128 / NL rows
+// issued by NL different lanes: does splitting a slot across issuing threads raise the rate at a
+// fixed number of bytes in flight (the layer tail's ring is capped at 4 x 16 KB by shared memory)?
+template <int S, int NL>
+__global__ void __launch_bounds__(32, 1) k_stream_lanes(const __grid_constant__ CUtensorMap map, int iters,
+                                                       int blocks_per_region) {
+    extern __shared__ uint8_t raw[];
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t full[S];
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {
+        for (int s = 0; s < S; s++) ptx::mbar_init(&full[s], 1);
+        ptx::fence_barrier_init();
+    }
+    __syncwarp();
+    for (int it = 0; it < iters + S; it++) {
+        const int s = it % S;
+        if (it >= S) ptx::mbar_wait(&full[s], ((it - S) / S) & 1);
+        __syncwarp();
+        if (it < iters) {
+            const int blk = it % blocks_per_region;
+            if (lane == 0) ptx::mbar_expect_tx(&full[s], BOX_BYTES);
+            __syncwarp();
+            if (lane < NL)
+                ptx::tma_load_2d(ring + s * BOX_BYTES + lane * (BOX_BYTES / NL), &map, &full[s], 0,
+                                 blk * BOX_ROWS + lane * (BOX_ROWS / NL));
+        }
+    }
+}
+
+template <int S, int NL>
+void run_lanes(EncodeFn enc, void* buf, int grid) {
+    const int blocks_per_region = (1 << 20) / BOX_BYTES;
+    CUtensorMap m;
+    cuuint64_t dims[2] = {64, static_cast<cuuint64_t>(blocks_per_region) * BOX_ROWS};
+    cuuint64_t strides[1] = {128};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(BOX_ROWS / NL)};
+    cuuint32_t es[2] = {1, 1};
+    enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const int iters = 4096, smem = S * BOX_BYTES + 1024;
+    cudaFuncSetAttribute(k_stream_lanes<S, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_stream_lanes<S, NL><<<grid, 32, smem>>>(m, iters, blocks_per_region);
+    cudaEventRecord(e0);
+    k_stream_lanes<S, NL><<<grid, 32, smem>>>(m, iters, blocks_per_region);
+    cudaEventRecord(e1);
+    cudaDeviceSynchronize();
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double gbs = static_cast<double>(grid) * iters * BOX_BYTES / (ms * 1e-3) / 1e9;
+    std::printf("{\"lanes_per_slot\": %d, \"stages\": %d, \"grid\": %d, \"kernel_GBps\": %.0f, \"per_SM_GBps\": %.1f, \"err\": \"%s\"}\n",
+                NL, S, grid, gbs, gbs / 148, cudaGetErrorString(cudaGetLastError()));
+    std::fflush(stdout);
+}
+
 int main() {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -290,5 +348,11 @@ int main() {
     run_multi<6, 2>(enc, buf, 148);
     run_multi<3, 4>(enc, buf, 148);
     run_multi<2, 4>(enc, buf, 148);
+    run_lanes<4, 1>(enc, buf, 148);
+    run_lanes<4, 2>(enc, buf, 148);
+    run_lanes<4, 4>(enc, buf, 148);
+    run_lanes<4, 8>(enc, buf, 148);
+    run_lanes<6, 1>(enc, buf, 148);
+    run_lanes<6, 4>(enc, buf, 148);
     return 0;
 }
