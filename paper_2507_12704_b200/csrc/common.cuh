@@ -5,12 +5,23 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <mutex>
 #include <set>
 #include <string>
 #include <utility>
 
 namespace dcat {
+
+// NVTX range around a host-side stage (API calls, GEMM / attention / tail launches): named spans
+// in nsys / `ncu --nvtx` timelines; a no-op unless a tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 using bf16 = __nv_bfloat16;
 

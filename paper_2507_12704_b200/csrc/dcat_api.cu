@@ -468,6 +468,7 @@ template <typename T>
 void gemm(dcat_model* m, const char* tag, const T* A, int lda, const Lin& L, int w_off, int N, int M, const Epi& e,
           float* tmp, cudaStream_t s) {
     if (M <= 0) return;
+    NvtxRange nr(tag);
     int t0 = mark(m, s);
     if constexpr (std::is_same<T, bf16>::value) {
         gemm_tc(A, lda, L.wt + static_cast<size_t>(w_off) * L.in, L.in, M, N, L.in, e, s);
@@ -545,6 +546,7 @@ void layer_tail(dcat_model* m, const char* pass, const T* attn_out, const LayerW
         const bool two_kernels = getenv("DCAT_NO_TAIL_FUSION") != nullptr || getenv("DCAT_NO_FUSED_FFN") != nullptr;
         if (!two_kernels && layer_tail_tc_supported(d, F)) {
             if (M <= 0) return;
+            NvtxRange nr(ctx ? "gemm.ctx.tail" : "gemm.cross.tail");
             int t0 = mark(m, s);
             Epi e = base_epi(m, EPI_RESID_LN, l);
             e.bias = L.f1.bias;
@@ -590,6 +592,7 @@ void layer_tail(dcat_model* m, const char* pass, const T* attn_out, const LayerW
 
 template <typename T>
 void attn(dcat_model* m, const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t s) {
+    NvtxRange nr(a.causal ? "attn.ctx" : "attn.cross");
     int t0 = mark(m, s);
     if constexpr (std::is_same<T, bf16>::value) {
         if (a.ldvt > 0) {
@@ -1292,6 +1295,7 @@ int dcat_dedup(dcat_model* m, const dcat_batch* batch, int32_t* rep, int32_t* fi
                void* stream) {
     if (!m || !batch || !rep || !b_u) return set_err(DCAT_EINVAL, "null argument");
     return guarded(m, [&]() -> int {
+        NvtxRange nr("dcat_dedup");
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         bool device = flags & DCAT_INPUT_DEVICE;
         int64_t B = batch->n_rows;
@@ -1358,6 +1362,7 @@ int dcat_rank_forward_batch(dcat_model* m, const dcat_batch* batch, const dcat_f
                             float* module_logits, float* h_cand, int32_t flags, void* stream) {
     if (!m || !batch || !ft || !logits || !module_logits) return set_err(DCAT_EINVAL, "null argument");
     return guarded(m, [&]() -> int {
+        NvtxRange nr("dcat_rank_forward_batch");
         const auto h_entry = std::chrono::steady_clock::now();
         int rc = validate_ft(m, ft, batch);
         if (rc) return rc;
@@ -1524,6 +1529,7 @@ int dcat_context_forward(dcat_model* m, const dcat_batch* uniques, int32_t windo
     if (!m || !uniques || !out) return set_err(DCAT_EINVAL, "null argument");
     *out = nullptr;
     return guarded(m, [&]() -> int {
+        NvtxRange nr("dcat_context_forward");
         // context_forward / context_forward_fixed argument checks (dcat.cpp:141-142, 285-288)
         const char* fn = window > 0 ? "context_forward_fixed" : "context_forward";
         if (window < 0) return set_err(DCAT_EINVAL, "context_forward_fixed: window must be >= 1, got " +
@@ -1660,6 +1666,7 @@ int dcat_candidate_inputs(dcat_model* m, const uint64_t* items, const int32_t* p
                           int32_t flags, void* stream) {
     if (!m || (n > 0 && (!items || !pos || !e_cand))) return set_err(DCAT_EINVAL, "null argument");
     return guarded(m, [&]() -> int {
+        NvtxRange nr("dcat_candidate_inputs");
         if (n <= 0) return DCAT_OK;
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         const bool device = flags & DCAT_INPUT_DEVICE;
@@ -1692,6 +1699,7 @@ int dcat_cross_forward(dcat_model* m, const dcat_kv* kv, const int32_t* rep, con
                        float* h, int32_t flags, void* stream) {
     if (!m || !kv || (n > 0 && (!rep || !e_cand || !h))) return set_err(DCAT_EINVAL, "null argument");
     return guarded(m, [&]() -> int {
+        NvtxRange nr("dcat_cross_forward");
         const char* fn = kv->window > 0 ? "cross_forward_fixed" : "cross_forward";
         if (kv->m != m) return set_err(DCAT_EINVAL, std::string(fn) + ": cache/model config mismatch");
         const bool device = flags & DCAT_INPUT_DEVICE, f32 = flags & DCAT_PRECISION_FP32;

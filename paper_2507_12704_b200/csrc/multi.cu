@@ -410,6 +410,7 @@ int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const
     if (flags & (DCAT_INPUT_DEVICE | DCAT_OUTPUT_DEVICE))
         return merr(DCAT_EINVAL, "dcat_multi_rank_forward_batch takes host buffers");
     try {
+        dcat::NvtxRange nr("dcat_multi_rank_forward_batch");
         const int nd = static_cast<int>(mh->dev.size());
         const int64_t B = batch->n_rows;
         if (B == 0) return DCAT_OK;
