@@ -102,15 +102,20 @@ inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b -
 
 }  // namespace dcat
 
+// A failed runtime call also leaves its code as the thread's "last error" (non-sticky errors such as
+// an invalid device ordinal): it is consumed here, so a later launch check does not report it again.
 #define DCAT_CUDA_CHECK(expr)                                                               \
     do {                                                                                    \
         cudaError_t e__ = (expr);                                                           \
-        if (e__ != cudaSuccess)                                                             \
+        if (e__ != cudaSuccess) {                                                           \
+            (void)cudaGetLastError();                                                       \
             throw ::dcat::CudaError(std::string(#expr) + " (" + __FILE__ + ":" + std::to_string(__LINE__) + "): " + \
                                     cudaGetErrorString(e__));                                  \
+        }                                                                                   \
     } while (0)
 
 #define DCAT_LAUNCH_CHECK() DCAT_CUDA_CHECK(cudaGetLastError())
+
 
 namespace dcat {
 struct CudaError {
@@ -121,6 +126,59 @@ struct InvalidArg {
     std::string msg;
     int code;
     explicit InvalidArg(std::string m, int c = -1) : msg(std::move(m)), code(c) {}
+};
+// true when the calling thread has a current CUDA context (cuCtxGetCurrent through the runtime's
+// driver entry point; the library does not link libcuda directly)
+inline bool thread_has_context() {
+    typedef int (*GetCur)(void**);
+    static GetCur fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuCtxGetCurrent", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            (void)cudaGetLastError();
+            return static_cast<GetCur>(nullptr);
+        }
+        return reinterpret_cast<GetCur>(p);
+    }();
+    if (!fn) return true;  // unknown: restore as if there were one
+    void* ctx = nullptr;
+    return fn(&ctx) == 0 && ctx != nullptr;
+}
+// Makes `dev` the current device for a scope and restores the caller's current device after it
+// (the C ABI never leaves the calling thread on another GPU). dev < 0: no switch. A thread that
+// had no current context is left without a restore (restoring its default device 0 would create a
+// context on GPU 0 in a process that only drives another GPU).
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (!thread_has_context() || cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            (void)cudaGetLastError();
+        }
+        if (dev >= 0 && dev != prev) DCAT_CUDA_CHECK(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+// Teardown form (destroy entry points, possibly run from static destructors at process exit when
+// the runtime may already be unloading): never throws, ignores and clears errors.
+struct DeviceScopeNoThrow {
+    int prev = -1;
+    explicit DeviceScopeNoThrow(int dev) {
+        if (!thread_has_context() || cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+        (void)cudaGetLastError();
+    }
+    ~DeviceScopeNoThrow() {
+        if (prev >= 0) cudaSetDevice(prev);
+        (void)cudaGetLastError();
+    }
+    DeviceScopeNoThrow(const DeviceScopeNoThrow&) = delete;
+    DeviceScopeNoThrow& operator=(const DeviceScopeNoThrow&) = delete;
 };
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device): the attribute
 // belongs to the device context, so a process driving several GPUs (csrc/multi.cu) sets it on every

@@ -1028,7 +1028,7 @@ template <typename F>
 int guarded(dcat_model* m, F&& f) {
     try {
         g_err.clear();
-        if (m) DCAT_CUDA_CHECK(cudaSetDevice(m->device));
+        DeviceGuard dg(m ? m->device : -1);
         return f();
     } catch (const CudaError& e) {
         return set_err(DCAT_ECUDA, e.msg);
@@ -1190,7 +1190,7 @@ int dcat_model_create(const dcat_model_config* cfg, const dcat_params* params, c
         if (c.d_model % 16 || c.d_emb % 8)
             return set_err(DCAT_EUNSUPPORTED, "d_model must be a multiple of 16 and d_emb of 8");
         m->device = device;
-        DCAT_CUDA_CHECK(cudaSetDevice(device));
+        DeviceGuard dg(device);
         m->cfg = c;
         const float* const* t = params->tensors;
         int k = 1;
@@ -1285,7 +1285,7 @@ int dcat_model_create(const dcat_model_config* cfg, const dcat_params* params, c
 
 int dcat_model_destroy(dcat_model* m) {
     if (!m) return DCAT_OK;
-    cudaSetDevice(m->device);
+    DeviceScopeNoThrow ds(m->device);
     cudaDeviceSynchronize();
     delete m;
     return DCAT_OK;
@@ -1632,7 +1632,7 @@ int dcat_host_free(void* p) {
 
 int dcat_kv_destroy(dcat_kv* kv) {
     if (!kv) return DCAT_OK;
-    cudaSetDevice(kv->device);
+    DeviceScopeNoThrow ds(kv->device);
     cudaDeviceSynchronize();
     delete kv;
     return DCAT_OK;

@@ -140,7 +140,10 @@ struct dcat_multi {
     std::vector<int32_t> last_owner;
     std::vector<float> host_scores;
     ~dcat_multi() {
+        dcat::DeviceScopeNoThrow ds(-1);  // restores the caller's current device, clears errors
         for (auto& d : dev) {
+            // a device whose model was never created (e.g. an invalid ordinal) holds nothing
+            if (!d.m && !d.stream && !d.comm && !d.out && !d.gather && !d.arena) continue;
             cudaSetDevice(d.device);
             cudaDeviceSynchronize();
             if (d.comm) nccl().commDestroy(d.comm);
@@ -369,6 +372,7 @@ int dcat_multi_create(const dcat_model_config* cfg, const dcat_params* params, c
         for (int j = 0; j < i; j++)
             if (devices[i] == devices[j]) return merr(DCAT_EINVAL, "dcat_multi_create: devices must be distinct");
     try {
+        dcat::DeviceGuard dg(-1);
         mh->dev.resize(static_cast<size_t>(n_devices));
         for (int i = 0; i < n_devices; i++) {
             DevState& d = mh->dev[static_cast<size_t>(i)];
@@ -411,6 +415,7 @@ int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const
         return merr(DCAT_EINVAL, "dcat_multi_rank_forward_batch takes host buffers");
     try {
         dcat::NvtxRange nr("dcat_multi_rank_forward_batch");
+        dcat::DeviceGuard dg(-1);  // the calling thread's current device is restored on return
         const int nd = static_cast<int>(mh->dev.size());
         const int64_t B = batch->n_rows;
         if (B == 0) return DCAT_OK;

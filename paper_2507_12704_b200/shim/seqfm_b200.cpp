@@ -214,27 +214,47 @@ Scorer::Scorer(const TransformerParams& p, const QuantizedTable& table, const Ra
     init(p, tab, rp, device);
 }
 
-void Scorer::init(const TransformerParams& p, const dcat_table& tab, const RankingHeadParams& rp, int device) {
-    std::vector<const Param*> all = p.all_params();
+namespace {
+// The reference objects as the C ABI's weight description (pointers into p / rp).
+struct CWeights {
     std::vector<const float*> tensors;
-    for (const Param* q : all) tensors.push_back(q->v.a.data());
-    dcat_params prm{tensors.data(), static_cast<int32_t>(tensors.size())};
+    dcat_params prm{};
     dcat_head head{};
-    head.d_module = rp.d_module;
-    head.d_emb = p.cfg.d_emb;
-    head.n_ctx = rp.d_feat - rp.d_module - p.cfg.d_emb;
-    head.hidden = rp.w1.v.cols;
-    head.d_aux = rp.aux_proj.v.rows;
-    head.w1 = rp.w1.v.a.data();
-    head.b1 = rp.b1.v.a.data();
-    head.w2 = rp.w2.v.a.data();
-    head.b2 = rp.b2.v.a.data();
-    head.mod_w = rp.mod_w.v.a.data();
-    head.mod_b = rp.mod_b.v.a.data();
-    head.aux_proj = rp.aux_proj.v.a.data();
-    head.lt = rp.lt.v.a.data();
-    dcat_model_config cfg = to_c(p.cfg);
-    check(dcat_model_create(&cfg, &prm, &tab, &head, device, &m_));
+    dcat_model_config cfg{};
+    CWeights(const TransformerParams& p, const RankingHeadParams& rp) {
+        for (const Param* q : p.all_params()) tensors.push_back(q->v.a.data());
+        prm = dcat_params{tensors.data(), static_cast<int32_t>(tensors.size())};
+        head.d_module = rp.d_module;
+        head.d_emb = p.cfg.d_emb;
+        head.n_ctx = rp.d_feat - rp.d_module - p.cfg.d_emb;
+        head.hidden = rp.w1.v.cols;
+        head.d_aux = rp.aux_proj.v.rows;
+        head.w1 = rp.w1.v.a.data();
+        head.b1 = rp.b1.v.a.data();
+        head.w2 = rp.w2.v.a.data();
+        head.b2 = rp.b2.v.a.data();
+        head.mod_w = rp.mod_w.v.a.data();
+        head.mod_b = rp.mod_b.v.a.data();
+        head.aux_proj = rp.aux_proj.v.a.data();
+        head.lt = rp.lt.v.a.data();
+        cfg = to_c(p.cfg);
+    }
+};
+
+void to_outputs(const std::vector<float>& logits, const std::vector<float>& mlog, std::vector<RankingOutputs>& out) {
+    for (size_t i = 0; i < out.size(); i++)
+        for (int j = 0; j < kRankHeadCount; j++) {
+            double l = logits[i * 3 + j];  // outputs_from, finetune.cpp:350-359
+            out[i].logit[static_cast<size_t>(j)] = l;
+            out[i].prob[static_cast<size_t>(j)] = 1.0 / (1.0 + std::exp(-l));
+            out[i].module_logit[static_cast<size_t>(j)] = mlog[i * 3 + j];
+        }
+}
+}  // namespace
+
+void Scorer::init(const TransformerParams& p, const dcat_table& tab, const RankingHeadParams& rp, int device) {
+    CWeights w(p, rp);
+    check(dcat_model_create(&w.cfg, &w.prm, &tab, &w.head, device, &m_));
     d_model_ = p.cfg.d_model;
     d_emb_ = p.cfg.d_emb;
     n_layers_ = p.cfg.n_layers;
@@ -254,14 +274,55 @@ std::vector<RankingOutputs> Scorer::rank_forward_batch(const std::vector<Ranking
     dcat_finetune_config fc = to_c(cfg);
     std::vector<float> logits(batch.size() * 3), mlog(batch.size() * 3);
     check(dcat_rank_forward_batch(m_, &b.c, &fc, logits.data(), mlog.data(), nullptr, flags_, nullptr));
-    for (size_t i = 0; i < batch.size(); i++)
-        for (int j = 0; j < kRankHeadCount; j++) {
-            double l = logits[i * 3 + j];  // outputs_from, finetune.cpp:350-359
-            out[i].logit[static_cast<size_t>(j)] = l;
-            out[i].prob[static_cast<size_t>(j)] = 1.0 / (1.0 + std::exp(-l));
-            out[i].module_logit[static_cast<size_t>(j)] = mlog[i * 3 + j];
-        }
+    to_outputs(logits, mlog, out);
     return out;
+}
+
+// ---------------------------------------------------------------- MultiScorer
+namespace {
+void mcheck(int rc) {
+    if (rc != DCAT_OK) throw std::runtime_error(dcat_multi_last_error());
+}
+}  // namespace
+
+MultiScorer::MultiScorer(const TransformerParams& p, const HashedEmbeddingTable& table, const RankingHeadParams& rp,
+                         const std::vector<int>& devices) {
+    SEQFM_CHECK(!devices.empty(), "MultiScorer: no devices");
+    std::vector<const float*> subs;
+    for (int j = 0; j < table.num_subtables(); j++) subs.push_back(table.subtable(j).a.data());
+    dcat_table tab{table.num_subtables(), table.rows(), table.d_sub(), table.seeds().data(), subs.data(), 0, nullptr};
+    CWeights w(p, rp);
+    std::vector<int32_t> dev(devices.begin(), devices.end());
+    mcheck(dcat_multi_create(&w.cfg, &w.prm, &tab, &w.head, dev.data(), static_cast<int32_t>(dev.size()), &mh_));
+}
+
+MultiScorer::~MultiScorer() {
+    if (mh_) dcat_multi_destroy(mh_);
+    if (stage_) dcat_host_free(stage_);
+}
+
+std::vector<RankingOutputs> MultiScorer::rank_forward_batch(const std::vector<RankingExample>& batch,
+                                                            const FinetuneConfig& cfg) const {
+    std::vector<RankingOutputs> out(batch.size());
+    if (batch.empty()) return out;
+    std::lock_guard<std::mutex> lk(mu_);
+    BatchSoA b = pack_examples(batch, uses_aux(cfg), stage_, stage_bytes_);
+    dcat_finetune_config fc = to_c(cfg);
+    std::vector<float> logits(batch.size() * 3), mlog(batch.size() * 3);
+    mcheck(dcat_multi_rank_forward_batch(mh_, &b.c, &fc, logits.data(), mlog.data(), flags_));
+    to_outputs(logits, mlog, out);
+    return out;
+}
+
+std::vector<int> MultiScorer::shard(const std::vector<RankingExample>& batch) const {
+    std::vector<int> owner(batch.size());
+    if (batch.empty()) return owner;
+    std::lock_guard<std::mutex> lk(mu_);
+    BatchSoA b = pack_examples(batch, false, stage_, stage_bytes_);
+    std::vector<int32_t> o(batch.size());
+    mcheck(dcat_multi_shard(mh_, &b.c, o.data()));
+    owner.assign(o.begin(), o.end());
+    return owner;
 }
 
 Mat Scorer::candidate_outputs(const std::vector<RankingExample>& batch, const FinetuneConfig& cfg) const {

@@ -26,6 +26,7 @@
 struct dcat_model;
 struct dcat_table;
 struct dcat_kv;
+struct dcat_multi;
 
 namespace seqfm {
 namespace b200 {
@@ -117,6 +118,33 @@ private:
     int flags_ = 0;
     mutable std::mutex mu_;
     mutable void* stage_ = nullptr;  // page-locked staging for packed batches (grown on demand)
+    mutable size_t stage_bytes_ = 0;
+};
+
+// rank_forward_batch over several GPUs of one box from one process: the multi-device drop-in for
+// score_groups (finetune.cpp:766-786). Rows are split user-disjoint by a content hash of their
+// events (equal sequences on one GPU, so each GPU's dedup equals the global one), uniques assigned
+// longest-processing-time first on a config-aware cost, every GPU scores its rows in its own host
+// thread, and the scores come back through one NCCL gather (dcat_multi_*, csrc/multi.cu). One
+// device behaves exactly like a Scorer on it.
+class MultiScorer {
+public:
+    MultiScorer(const TransformerParams& p, const HashedEmbeddingTable& table, const RankingHeadParams& rp,
+                const std::vector<int>& devices);
+    ~MultiScorer();
+    MultiScorer(const MultiScorer&) = delete;
+    MultiScorer& operator=(const MultiScorer&) = delete;
+    std::vector<RankingOutputs> rank_forward_batch(const std::vector<RankingExample>& batch,
+                                                   const FinetuneConfig& cfg) const;
+    // the index into `devices` each example is scored on
+    std::vector<int> shard(const std::vector<RankingExample>& batch) const;
+    void set_fp32(bool on) { flags_ = on ? 0x2 : 0; }
+
+private:
+    struct dcat_multi* mh_ = nullptr;
+    int flags_ = 0;
+    mutable std::mutex mu_;
+    mutable void* stage_ = nullptr;
     mutable size_t stage_bytes_ = 0;
 };
 

@@ -9,6 +9,8 @@
 // Exit code 0 = all checks pass. Run by tests/test_gpu_shim.py on the GPU box.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <memory>
 #include <stdexcept>
 #include <thread>
 #include <vector>
@@ -110,6 +112,7 @@ static void check_rank(const char* name, const ModelConfig& mc, int L, int users
 }
 
 int main() {
+    std::setvbuf(stdout, nullptr, _IONBF, 0);  // progress survives an abort
     // 1. rank_forward_batch parity (test_finetune.cpp:327-364 analogue)
     ModelConfig tiny;
     tiny.d_model = 16;
@@ -388,6 +391,70 @@ int main() {
         EXPECT(m <= 3e-2 && moved > 1e-6, "fingerprinted weight cache");
     }
 
+    // 3b. MultiScorer: the multi-GPU drop-in for score_groups (finetune.cpp:766-786) vs the
+    // reference's single-process rank_forward_batch, on 1 GPU and on 2 when the box has them
+    {
+        ModelConfig mc;
+        mc.d_model = 64;
+        mc.n_layers = 2;
+        mc.n_heads = 4;
+        mc.max_len = 34;
+        mc.d_emb = 64;
+        TransformerParams p;
+        p.init(mc, 61, 0.3f);
+        HashedEmbeddingTable table(4, 256, mc.d_emb / 4, 62);
+        FinetuneConfig cfg;
+        cfg.max_events = 32;
+        cfg.crossing_hidden = 8;
+        cfg.validate(mc);
+        RankingHeadParams rp;
+        rp.init(mc.d_model, mc.d_emb, cfg.d_aux, cfg.n_ctx(), cfg.crossing_hidden, cfg.sel_per_example(), 63);
+        Rng rng(17);
+        auto batch = make_batch(24, 7, 32, 0, rng, false);
+        auto ref = seqfm::rank_forward_batch(p, table, rp, batch, cfg);
+        double scale = 0;
+        for (auto& r : ref)
+            for (int h = 0; h < 3; h++) scale = std::max(scale, std::fabs(r.logit[h]));
+        const char* lim = std::getenv("TEST_SHIM_MULTI_MAX");  // bisection aid: max devices tried (0: none)
+        const int max_dev = lim ? std::atoi(lim) : 2;
+        for (int ndev : {1, 2}) {
+            if (ndev > max_dev) break;
+            std::vector<int> devs;
+            for (int i = 0; i < ndev; i++) devs.push_back(i);
+            std::unique_ptr<b200::MultiScorer> ms;
+            try {
+                ms = std::make_unique<b200::MultiScorer>(p, table, rp, devs);
+            } catch (const std::runtime_error& e) {
+                if (ndev > 1) {  // fewer GPUs on this box
+                    std::printf("MultiScorer x%d: skipped (%s)\n", ndev, e.what());
+                    continue;
+                }
+                EXPECT(false, "MultiScorer x1: %s", e.what());
+                continue;
+            }
+            for (int fp32 = 1; fp32 >= 0; fp32--) {
+                ms->set_fp32(fp32 != 0);
+                auto got = ms->rank_forward_batch(batch, cfg);
+                double err = 0;
+                for (size_t i = 0; i < ref.size(); i++)
+                    for (int h = 0; h < 3; h++) err = std::max(err, rel(got[i].logit[h], ref[i].logit[h], scale));
+                const double tol = fp32 ? 1e-4 : 3e-2;
+                std::printf("MultiScorer x%d %s: max rel err logits %.3e (tol %.0e)\n", ndev, fp32 ? "fp32" : "bf16",
+                            err, tol);
+                EXPECT(err <= tol, "MultiScorer x%d parity", ndev);
+            }
+            // user-disjoint: every example of one user sequence on one device
+            auto owner = ms->shard(batch);
+            bool disjoint = true;
+            for (size_t i = 0; i < batch.size(); i++)
+                for (size_t j = 0; j < i; j++)
+                    if (batch[i].seq.events == batch[j].seq.events && batch[i].seq.valid == batch[j].seq.valid &&
+                        owner[i] != owner[j])
+                        disjoint = false;
+            EXPECT(disjoint, "MultiScorer x%d shards are not user-disjoint", ndev);
+        }
+    }
+
     // 4. errors surface as std::runtime_error (SEQFM_CHECK)
     {
         TransformerParams p;
@@ -406,6 +473,7 @@ int main() {
             b200::rank_forward_batch(p, table, rp, batch, cfg);
         } catch (const std::runtime_error& e) {
             threw = std::string(e.what()).find("unknown action") != std::string::npos;
+            if (!threw) std::printf("unexpected error message: %s\n", e.what());
         }
         EXPECT(threw, "unknown action must throw std::runtime_error");
     }
