@@ -18,7 +18,10 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <queue>
 #include <string>
@@ -169,86 +172,122 @@ double unique_cost(const dcat_model_config& c, double n, double cands) {
     return ctx + cands * (cand / G + l * H * (n + 1) / X);
 }
 
+// What shard() decides: the device of every row, and the distinct event spans (offset, valid) of
+// the batch with the device that owns each (rows sharing a span are one user: one device).
+struct ShardPlan {
+    std::vector<int32_t> owner;  // [B] device of each row
+    std::vector<int32_t> row_g;  // [B] distinct span of each row
+    std::vector<int64_t> g_off;  // [S] distinct spans
+    std::vector<int32_t> g_valid, g_owner;
+};
+
 // owner device of every row: content-keyed uniques, LPT on unique_cost. Host threads take
-// contiguous row ranges: each content-hashes the distinct spans of its range once (rows of one user
-// usually share a span) and groups its rows by content; the per-thread groups are merged, assigned
-// longest-processing-time first, and mapped back to rows in parallel.
-void shard(const dcat_multi* mh, const dcat_batch& b, std::vector<int32_t>& owner) {
+// contiguous row ranges and collect the distinct event spans (offset, valid) of their range; the
+// spans are merged, each distinct span is content-hashed exactly once (in parallel), spans with
+// equal content become one unique, uniques are assigned longest-processing-time first, and rows
+// are mapped back to devices in parallel.
+void shard(const dcat_multi* mh, const dcat_batch& b, ShardPlan& plan) {
     const int64_t B = b.n_rows;
     const int nd = static_cast<int>(mh->dev.size());
+    std::vector<int32_t>& owner = plan.owner;
     owner.assign(static_cast<size_t>(B), 0);
+    plan.row_g.assign(static_cast<size_t>(B), 0);
+    plan.g_off.clear();
+    plan.g_valid.clear();
+    plan.g_owner.clear();
     if (nd == 1 || B == 0) return;
     struct Local {
-        std::vector<uint64_t> ukey;  // content hash of each local unique
-        std::vector<int32_t> n, c;   // its tokens and rows
-        std::vector<int32_t> row_u;  // local unique of each row of the range
+        std::vector<int64_t> off;   // distinct spans of the range
+        std::vector<int32_t> valid, rows;
+        std::vector<int32_t> row_s;  // local span of each row of the range
         std::vector<int32_t> to_global;
     };
     const unsigned T = static_cast<unsigned>(std::min<int64_t>(host_threads(), std::max<int64_t>(1, B / 4096)));
     std::vector<Local> loc(T);
     std::vector<int64_t> r0s(T + 1);
     for (unsigned t = 0; t <= T; t++) r0s[t] = B * t / T;
-    auto group = [&](unsigned t) {
+    auto parallel = [&](unsigned n, const std::function<void(unsigned)>& f) {
+        std::vector<std::thread> th;
+        for (unsigned t = 1; t < n; t++) th.emplace_back(f, t);
+        if (n) f(0);
+        for (auto& x : th) x.join();
+    };
+    // 1. distinct spans per row range
+    parallel(T, [&](unsigned t) {
         Local& L = loc[t];
         const int64_t r0 = r0s[t], r1 = r0s[t + 1];
-        FlatMap spans(static_cast<size_t>(r1 - r0)), uniq(static_cast<size_t>(r1 - r0));
-        std::vector<uint64_t> span_hashes;
-        L.row_u.resize(static_cast<size_t>(r1 - r0));
+        FlatMap spans(static_cast<size_t>(r1 - r0));
+        L.row_s.resize(static_cast<size_t>(r1 - r0));
         for (int64_t r = r0; r < r1; r++) {
             bool fresh;
             int32_t& si = spans.slot(span_key(b.row_offset[r], b.row_valid[r]), &fresh);
             if (fresh) {
-                si = static_cast<int32_t>(span_hashes.size());
-                span_hashes.push_back(span_hash(b, b.row_offset[r], b.row_valid[r]));
+                si = static_cast<int32_t>(L.off.size());
+                L.off.push_back(b.row_offset[r]);
+                L.valid.push_back(b.row_valid[r]);
+                L.rows.push_back(0);
             }
-            const uint64_t h = span_hashes[static_cast<size_t>(si)] | 1;  // non-zero map key
-            int32_t& ui = uniq.slot(h, &fresh);
-            if (fresh) {
-                ui = static_cast<int32_t>(L.ukey.size());
-                L.ukey.push_back(h);
-                L.n.push_back(b.row_valid[r]);
-                L.c.push_back(0);
-            }
-            L.c[static_cast<size_t>(ui)]++;
-            L.row_u[static_cast<size_t>(r - r0)] = ui;
+            L.rows[static_cast<size_t>(si)]++;
+            L.row_s[static_cast<size_t>(r - r0)] = si;
         }
-    };
-    {
-        std::vector<std::thread> th;
-        for (unsigned t = 1; t < T; t++) th.emplace_back(group, t);
-        group(0);
-        for (auto& x : th) x.join();
-    }
-    // merge the per-thread uniques
+    });
+    // 2. merge into global distinct spans
     size_t total = 0;
-    for (auto& L : loc) total += L.ukey.size();
+    for (auto& L : loc) total += L.off.size();
     FlatMap gmap(total);
-    std::vector<uint64_t> gkey;
-    std::vector<double> gn, gc;
+    std::vector<int64_t>& g_off = plan.g_off;
+    std::vector<int32_t>& g_valid = plan.g_valid;
+    std::vector<double> g_rows;
     for (auto& L : loc) {
-        L.to_global.resize(L.ukey.size());
-        for (size_t i = 0; i < L.ukey.size(); i++) {
+        L.to_global.resize(L.off.size());
+        for (size_t i = 0; i < L.off.size(); i++) {
             bool fresh;
-            int32_t& g = gmap.slot(L.ukey[i], &fresh);
+            int32_t& g = gmap.slot(span_key(L.off[i], L.valid[i]), &fresh);
             if (fresh) {
-                g = static_cast<int32_t>(gkey.size());
-                gkey.push_back(L.ukey[i]);
-                gn.push_back(L.n[i]);
-                gc.push_back(0);
+                g = static_cast<int32_t>(g_off.size());
+                g_off.push_back(L.off[i]);
+                g_valid.push_back(L.valid[i]);
+                g_rows.push_back(0);
             }
-            gc[static_cast<size_t>(g)] += L.c[i];
+            g_rows[static_cast<size_t>(g)] += L.rows[i];
             L.to_global[i] = g;
         }
     }
-    const size_t U = gkey.size();
+    // 3. one content hash per distinct span
+    const size_t S = g_off.size();
+    std::vector<uint64_t> g_hash(S);
+    const unsigned TH = static_cast<unsigned>(std::min<size_t>(host_threads(), std::max<size_t>(1, S / 64)));
+    parallel(TH, [&](unsigned t) {
+        for (size_t k = S * t / TH; k < S * (t + 1) / TH; k++)
+            g_hash[k] = span_hash(b, g_off[k], g_valid[k]) | 1;  // non-zero map key
+    });
+    // 4. spans of equal content -> one unique (its tokens, its rows)
+    FlatMap umap(S);
+    std::vector<int32_t> span_u(S);
+    std::vector<uint64_t> ukey;
+    std::vector<double> un, uc;
+    for (size_t k = 0; k < S; k++) {
+        bool fresh;
+        int32_t& u = umap.slot(g_hash[k], &fresh);
+        if (fresh) {
+            u = static_cast<int32_t>(ukey.size());
+            ukey.push_back(g_hash[k]);
+            un.push_back(g_valid[k]);
+            uc.push_back(0);
+        }
+        uc[static_cast<size_t>(u)] += g_rows[k];
+        span_u[k] = u;
+    }
+    // 5. LPT on the config-aware cost
+    const size_t U = ukey.size();
     std::vector<int32_t> order(U);
     std::vector<double> cost(U);
     for (size_t u = 0; u < U; u++) {
         order[u] = static_cast<int32_t>(u);
-        cost[u] = unique_cost(mh->cfg, gn[u], gc[u]);
+        cost[u] = unique_cost(mh->cfg, un[u], uc[u]);
     }
     std::sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
-        return cost[x] != cost[y] ? cost[x] > cost[y] : gkey[x] < gkey[y];
+        return cost[x] != cost[y] ? cost[x] > cost[y] : ukey[x] < ukey[y];
     });
     using Load = std::pair<double, int>;
     std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
@@ -260,15 +299,17 @@ void shard(const dcat_multi* mh, const dcat_batch& b, std::vector<int32_t>& owne
         u_owner[static_cast<size_t>(u)] = top.second;
         heap.push({top.first + cost[static_cast<size_t>(u)], top.second});
     }
-    std::vector<std::thread> th;
-    for (unsigned t = 0; t < T; t++)
-        th.emplace_back([&, t] {
-            const Local& L = loc[t];
-            for (int64_t r = r0s[t]; r < r0s[t + 1]; r++)
-                owner[static_cast<size_t>(r)] =
-                    u_owner[static_cast<size_t>(L.to_global[static_cast<size_t>(L.row_u[static_cast<size_t>(r - r0s[t])])])];
-        });
-    for (auto& x : th) x.join();
+    // 6. spans and rows -> devices
+    plan.g_owner.resize(S);
+    for (size_t k = 0; k < S; k++) plan.g_owner[k] = u_owner[static_cast<size_t>(span_u[k])];
+    parallel(T, [&](unsigned t) {
+        const Local& L = loc[t];
+        for (int64_t r = r0s[t]; r < r0s[t + 1]; r++) {
+            const int32_t g = L.to_global[static_cast<size_t>(L.row_s[static_cast<size_t>(r - r0s[t])])];
+            plan.row_g[static_cast<size_t>(r)] = g;
+            owner[static_cast<size_t>(r)] = plan.g_owner[static_cast<size_t>(g)];
+        }
+    });
 }
 
 // one device's rows as a compact host batch (each used span copied once)
@@ -277,29 +318,22 @@ void shard(const dcat_multi* mh, const dcat_batch& b, std::vector<int32_t>& owne
 struct LocalBatch {
     std::vector<int64_t> rows;
     dcat_batch c{};
-    void build(const dcat_batch& b, const std::vector<int32_t>& owner, int d, void*& arena, size_t& arena_bytes) {
+    // P host threads copy the device's distinct spans (each once) and fill its rows
+    void build(const dcat_batch& b, const ShardPlan& plan, int d, void*& arena, size_t& arena_bytes, unsigned P) {
         rows.clear();
         for (int64_t r = 0; r < b.n_rows; r++)
-            if (owner[static_cast<size_t>(r)] == d) rows.push_back(r);
-        const size_t n = rows.size();
-        // pass 1: distinct spans and their local offsets
-        FlatMap copied(n);
-        std::vector<int32_t> row_span(n);
-        std::vector<std::pair<int64_t, int32_t>> spans;
-        std::vector<int64_t> span_off;
+            if (plan.owner[static_cast<size_t>(r)] == d) rows.push_back(r);
+        const size_t n = rows.size(), S = plan.g_off.size();
+        // the device's distinct spans and their offsets in its compact event pool
+        std::vector<int64_t> span_off(S, -1);
+        std::vector<int32_t> mine;
         size_t E = 0;
-        for (size_t i = 0; i < n; i++) {
-            const int64_t r = rows[i];
-            bool fresh;  // spans of equal start and length are one copy
-            int32_t& si = copied.slot(span_key(b.row_offset[r], b.row_valid[r]), &fresh);
-            if (fresh) {
-                si = static_cast<int32_t>(spans.size());
-                spans.push_back({b.row_offset[r], b.row_valid[r]});
-                span_off.push_back(static_cast<int64_t>(E));
-                E += static_cast<size_t>(b.row_valid[r]);
+        for (size_t k = 0; k < S; k++)
+            if (plan.g_owner[k] == d) {
+                span_off[k] = static_cast<int64_t>(E);
+                E += static_cast<size_t>(plan.g_valid[k]);
+                mine.push_back(static_cast<int32_t>(k));
             }
-            row_span[i] = si;
-        }
         const int da = b.aux ? b.d_aux : 0;
         auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
         const size_t o_off = 0, o_valid = al(8 * n), o_cand = al(o_valid + 4 * n), o_age = al(o_cand + 8 * n),
@@ -323,22 +357,30 @@ struct LocalBatch {
         uint64_t* item = reinterpret_cast<uint64_t*>(base + o_item);
         uint8_t* act = base + o_act;
         uint8_t* surf = base + o_surf;
-        for (size_t k = 0; k < spans.size(); k++) {  // pass 2: the events of every distinct span
-            const int64_t o = spans[k].first, e0 = span_off[k];
-            const size_t v = static_cast<size_t>(spans[k].second);
-            std::memcpy(ts + e0, b.ev_ts + o, 8 * v);
-            std::memcpy(item + e0, b.ev_item + o, 8 * v);
-            std::memcpy(act + e0, b.ev_action + o, v);
-            std::memcpy(surf + e0, b.ev_surface + o, v);
-        }
-        for (size_t i = 0; i < n; i++) {
-            const int64_t r = rows[i];
-            off[i] = span_off[static_cast<size_t>(row_span[i])];
-            valid[i] = b.row_valid[r];
-            cand[i] = b.candidate[r];
-            age[i] = b.age_seconds[r];
-            if (da) std::memcpy(aux + i * da, b.aux + r * da, sizeof(float) * static_cast<size_t>(da));
-        }
+        const unsigned nt = std::max(1u, std::min<unsigned>(P, static_cast<unsigned>((n + E / 64) / 8192 + 1)));
+        std::vector<std::thread> th;
+        auto part = [&](unsigned t) {
+            for (size_t q = mine.size() * t / nt; q < mine.size() * (t + 1) / nt; q++) {  // the span events
+                const size_t k = static_cast<size_t>(mine[q]);
+                const int64_t o = plan.g_off[k], e0 = span_off[k];
+                const size_t v = static_cast<size_t>(plan.g_valid[k]);
+                std::memcpy(ts + e0, b.ev_ts + o, 8 * v);
+                std::memcpy(item + e0, b.ev_item + o, 8 * v);
+                std::memcpy(act + e0, b.ev_action + o, v);
+                std::memcpy(surf + e0, b.ev_surface + o, v);
+            }
+            for (size_t i = n * t / nt; i < n * (t + 1) / nt; i++) {  // the rows
+                const int64_t r = rows[i];
+                off[i] = span_off[static_cast<size_t>(plan.row_g[static_cast<size_t>(r)])];
+                valid[i] = b.row_valid[r];
+                cand[i] = b.candidate[r];
+                age[i] = b.age_seconds[r];
+                if (da) std::memcpy(aux + i * da, b.aux + r * da, sizeof(float) * static_cast<size_t>(da));
+            }
+        };
+        for (unsigned t = 1; t < nt; t++) th.emplace_back(part, t);
+        part(0);
+        for (auto& x : th) x.join();
         c = dcat_batch{};
         c.n_rows = static_cast<int64_t>(n);
         c.row_offset = off;
@@ -402,9 +444,9 @@ int dcat_multi_destroy(dcat_multi* mh) {
 
 int dcat_multi_shard(dcat_multi* mh, const dcat_batch* batch, int32_t* owner) {
     if (!mh || !batch || !owner) return merr(DCAT_EINVAL, "null argument");
-    std::vector<int32_t> o;
-    shard(mh, *batch, o);
-    std::memcpy(owner, o.data(), sizeof(int32_t) * o.size());
+    ShardPlan plan;
+    shard(mh, *batch, plan);
+    std::memcpy(owner, plan.owner.data(), sizeof(int32_t) * plan.owner.size());
     return DCAT_OK;
 }
 
@@ -425,14 +467,26 @@ int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const
                                              flags & DCAT_PRECISION_FP32, mh->dev[0].stream);
             return rc ? merr(rc, dcat_last_error()) : DCAT_OK;
         }
-        shard(mh, *batch, mh->last_owner);
+        // DCAT_MULTI_TIMING=1: host wall time of each phase on stderr (investigation aid)
+        static const bool timing = getenv("DCAT_MULTI_TIMING") != nullptr;
+        using clk = std::chrono::steady_clock;
+        const auto t_start = clk::now();
+        std::vector<double> t_build(static_cast<size_t>(nd)), t_score(static_cast<size_t>(nd));
+        ShardPlan plan;
+        shard(mh, *batch, plan);
+        mh->last_owner = plan.owner;
+        const auto t_shard = clk::now();
         std::vector<LocalBatch> lb(static_cast<size_t>(nd));  // built by each device's own thread
         // 3. every device scores its rows (device outputs, no host round trip), one host thread each
         std::vector<int> rc(static_cast<size_t>(nd), 0);
         std::vector<std::string> msg(static_cast<size_t>(nd));
         auto work = [&](int d) {
             DevState& s = mh->dev[static_cast<size_t>(d)];
-            lb[static_cast<size_t>(d)].build(*batch, mh->last_owner, d, s.arena, s.arena_bytes);
+            const auto b0 = clk::now();
+            lb[static_cast<size_t>(d)].build(*batch, plan, d, s.arena, s.arena_bytes,
+                                             std::max(1u, host_threads() / static_cast<unsigned>(nd)));
+            const auto b1 = clk::now();
+            t_build[static_cast<size_t>(d)] = std::chrono::duration<double, std::milli>(b1 - b0).count();
             const size_t n = lb[static_cast<size_t>(d)].rows.size();
             try {
                 DCAT_CUDA_CHECK(cudaSetDevice(s.device));
@@ -446,6 +500,10 @@ int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const
                     dcat_rank_forward_batch(s.m, &lb[static_cast<size_t>(d)].c, ft, s.out, s.out + n * 3, nullptr,
                                             (flags & DCAT_PRECISION_FP32) | DCAT_OUTPUT_DEVICE, s.stream);
                 if (rc[static_cast<size_t>(d)]) msg[static_cast<size_t>(d)] = dcat_last_error();
+                if (timing) {
+                    DCAT_CUDA_CHECK(cudaStreamSynchronize(s.stream));
+                    t_score[static_cast<size_t>(d)] = std::chrono::duration<double, std::milli>(clk::now() - b1).count();
+                }
             } catch (const dcat::CudaError& e) {
                 rc[static_cast<size_t>(d)] = DCAT_ECUDA;
                 msg[static_cast<size_t>(d)] = e.msg;
@@ -455,6 +513,7 @@ int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const
         for (int d = 1; d < nd; d++) th.emplace_back(work, d);
         work(0);
         for (auto& x : th) x.join();
+        const auto t_scored = clk::now();
         for (int d = 0; d < nd; d++)
             if (rc[static_cast<size_t>(d)]) return merr(rc[static_cast<size_t>(d)], msg[static_cast<size_t>(d)]);
         // 4. gather to the first device: one NCCL group of sends / receives over NVLink
@@ -502,6 +561,15 @@ int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const
                 }
             });
         for (auto& x : sc) x.join();
+        if (timing) {
+            auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "dcat_multi: shard %.3f ms | build", ms(t_start, t_shard));
+            for (double v : t_build) std::fprintf(stderr, " %.3f", v);
+            std::fprintf(stderr, " | score");
+            for (double v : t_score) std::fprintf(stderr, " %.3f", v);
+            std::fprintf(stderr, " | threads joined %.3f | gather+d2h+scatter %.3f | total %.3f ms\n",
+                         ms(t_start, t_scored), ms(t_scored, clk::now()), ms(t_start, clk::now()));
+        }
         return DCAT_OK;
     } catch (const dcat::CudaError& e) {
         return merr(DCAT_ECUDA, e.msg);
