@@ -38,23 +38,128 @@ dcat_model_config to_c(const ModelConfig& c) {
 
 size_t align16(size_t n) { return (n + 15) & ~size_t(15); }
 
+// a row's valid events: equal sequences (the reference's segment_key content, dcat.cpp:45-56)
+bool same_events(const Segment& a, const Segment& b) {
+    return a.valid == b.valid && std::equal(a.events.begin(), a.events.begin() + a.valid, b.events.begin());
+}
+// cheap grouping key of a row's sequence (a few of its events); equality is always verified
+uint64_t seq_key(const Segment& s) {
+    auto mix = [](uint64_t x) {
+        x ^= x >> 30;
+        x *= 0xbf58476d1ce4e5b9ULL;
+        x ^= x >> 27;
+        x *= 0x94d049bb133111ebULL;
+        return x ^ (x >> 31);
+    };
+    uint64_t k = mix(static_cast<uint64_t>(s.valid) + 0x9e3779b97f4a7c15ULL);
+    if (s.valid > 0) {
+        const Event* e = s.events.data();
+        for (int i : {0, s.valid / 2, s.valid - 1})
+            k = mix(k ^ e[i].timestamp ^ (e[i].item_id << 7) ^
+                    (static_cast<uint64_t>(e[i].action) << 56 | static_cast<uint64_t>(e[i].surface) << 60));
+    }
+    return k | 1;  // non-zero map key
+}
+
+// open-addressing map, non-zero 64-bit key -> int32 (single-threaded scratch)
+struct KeyMap {
+    std::vector<uint64_t> key;
+    std::vector<int32_t> val;
+    size_t mask = 0;
+    explicit KeyMap(size_t n) {
+        size_t cap = 16;
+        while (cap < 2 * n) cap <<= 1;
+        key.assign(cap, 0);
+        val.assign(cap, -1);
+        mask = cap - 1;
+    }
+    int32_t& slot(uint64_t k, bool* fresh) {
+        size_t i = (k * 0x9e3779b97f4a7c15ULL) >> 20 & mask;
+        while (key[i] != 0 && key[i] != k) i = (i + 1) & mask;
+        *fresh = key[i] == 0;
+        key[i] = k;
+        return val[i];
+    }
+};
+
 // Structure-of-arrays view of a batch (std::vector<RankingExample>, or bare Segments), packed into
-// the Scorer's page-locked staging buffer so the device copies are asynchronous DMA. Every row
-// carries its own event span, like the reference's per-example Segment; rows are packed by up to
-// 16 host threads when the batch is large (the per-row event copy is the host-side cost of the
-// drop-in API).
+// the Scorer's page-locked staging buffer so the device copies are asynchronous DMA. Every
+// RankingExample owns its Segment, but rows of one user carry equal sequences: rows are grouped
+// by content (a cheap key, then an exact event-by-event comparison with the group's first row, in
+// parallel) and each distinct sequence is packed once, its rows sharing the span (offset, valid).
+// The device dedup then settles those rows by span identity; results are the same as with a
+// private copy per row, and the host copies ~1/C of the events. Up to 16 host threads.
 struct BatchSoA {
     dcat_batch c{};
 
     template <typename SegAt, typename RowAt>
     BatchSoA(size_t B, SegAt seg_at, RowAt row_at, int d_aux, void*& stage, size_t& stage_bytes) {
-        std::vector<int64_t> off(B + 1, 0);
         for (size_t i = 0; i < B; i++) {
             const Segment& s = seg_at(i);
             SEQFM_CHECK(s.valid >= 0 && s.valid <= s.length(), "segment valid out of range");
-            off[i + 1] = off[i] + s.valid;
         }
-        const size_t E = static_cast<size_t>(off[B]);
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const size_t T = std::min<size_t>(std::min<size_t>(hw, 16), std::max<size_t>(1, B / 4096));
+        auto parallel = [&](size_t n, auto&& f) {  // f(lo, hi) over [0, n) in T slices
+            if (T <= 1 || n < 2 * T) {
+                f(size_t(0), n);
+                return;
+            }
+            std::vector<std::thread> th;
+            for (size_t t = 1; t < T; t++) th.emplace_back([&, t] { f(n * t / T, n * (t + 1) / T); });
+            f(size_t(0), n / T);
+            for (auto& x : th) x.join();
+        };
+        // 1. grouping keys (parallel), 2. provisional groups by key (first row = representative)
+        std::vector<uint64_t> key(B);
+        parallel(B, [&](size_t lo, size_t hi) {
+            for (size_t i = lo; i < hi; i++) key[i] = seq_key(seg_at(i));
+        });
+        std::vector<int32_t> grp(B);
+        std::vector<int64_t> rep;  // representative row of each group
+        {
+            KeyMap km(B);
+            for (size_t i = 0; i < B; i++) {
+                bool fresh;
+                int32_t& g = km.slot(key[i], &fresh);
+                if (fresh) {
+                    g = static_cast<int32_t>(rep.size());
+                    rep.push_back(static_cast<int64_t>(i));
+                }
+                grp[i] = g;
+            }
+        }
+        // 3. exact verification against the representative (parallel); rows that differ (a key
+        // collision) are regrouped serially among the groups of their key
+        std::vector<uint8_t> odd(B, 0);
+        parallel(B, [&](size_t lo, size_t hi) {
+            for (size_t i = lo; i < hi; i++) {
+                const int64_t r = rep[static_cast<size_t>(grp[i])];
+                if (static_cast<size_t>(r) != i && !same_events(seg_at(i), seg_at(static_cast<size_t>(r)))) odd[i] = 1;
+            }
+        });
+        std::map<uint64_t, std::vector<int32_t>> extra;  // further groups of a colliding key
+        for (size_t i = 0; i < B; i++) {
+            if (!odd[i]) continue;
+            std::vector<int32_t>& gs = extra[key[i]];
+            int32_t found = -1;
+            for (int32_t g : gs)
+                if (same_events(seg_at(i), seg_at(static_cast<size_t>(rep[static_cast<size_t>(g)])))) {
+                    found = g;
+                    break;
+                }
+            if (found < 0) {
+                found = static_cast<int32_t>(rep.size());
+                rep.push_back(static_cast<int64_t>(i));
+                gs.push_back(found);
+            }
+            grp[i] = found;
+        }
+        // 4. one span per group
+        const size_t G = rep.size();
+        std::vector<int64_t> goff(G + 1, 0);
+        for (size_t g = 0; g < G; g++) goff[g + 1] = goff[g] + seg_at(static_cast<size_t>(rep[g])).valid;
+        const size_t E = static_cast<size_t>(goff[G]);
         // layout: off | valid | ts | item | cand | age | aux | action | surface
         size_t o_off = 0, o_valid = align16(o_off + 8 * B), o_ts = align16(o_valid + 4 * B), o_item = align16(o_ts + 8 * E),
                o_cand = align16(o_item + 8 * E), o_age = align16(o_cand + 8 * B), o_aux = align16(o_age + 8 * B),
@@ -78,12 +183,10 @@ struct BatchSoA {
         float* p_aux = reinterpret_cast<float*>(base + o_aux);
         uint8_t* p_act = base + o_act;
         uint8_t* p_surf = base + o_surf;
-        auto pack = [&](size_t r0, size_t r1) {
-            for (size_t i = r0; i < r1; i++) {
-                const Segment& s = seg_at(i);
-                const size_t e0 = static_cast<size_t>(off[i]);
-                p_off[i] = off[i];
-                p_valid[i] = s.valid;
+        parallel(G, [&](size_t lo, size_t hi) {  // the distinct sequences' events
+            for (size_t g = lo; g < hi; g++) {
+                const Segment& s = seg_at(static_cast<size_t>(rep[g]));
+                const size_t e0 = static_cast<size_t>(goff[g]);
                 for (int e = 0; e < s.valid; e++) {
                     const Event& ev = s.events[static_cast<size_t>(e)];
                     p_ts[e0 + e] = ev.timestamp;
@@ -91,18 +194,15 @@ struct BatchSoA {
                     p_act[e0 + e] = static_cast<uint8_t>(ev.action);
                     p_surf[e0 + e] = static_cast<uint8_t>(ev.surface);
                 }
+            }
+        });
+        parallel(B, [&](size_t lo, size_t hi) {  // the rows
+            for (size_t i = lo; i < hi; i++) {
+                p_off[i] = goff[static_cast<size_t>(grp[i])];
+                p_valid[i] = seg_at(i).valid;
                 row_at(i, p_cand + i, p_age + i, p_aux + i * static_cast<size_t>(d_aux));
             }
-        };
-        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        const size_t T = std::min<size_t>(std::min<size_t>(hw, 16), std::max<size_t>(1, (E + B) / 65536));
-        if (T <= 1) {
-            pack(0, B);
-        } else {
-            std::vector<std::thread> th;
-            for (size_t t = 0; t < T; t++) th.emplace_back(pack, B * t / T, B * (t + 1) / T);
-            for (auto& x : th) x.join();
-        }
+        });
         c.n_rows = static_cast<int64_t>(B);
         c.row_offset = p_off;
         c.row_valid = p_valid;

@@ -391,6 +391,47 @@ int main() {
         EXPECT(m <= 3e-2 && moved > 1e-6, "fingerprinted weight cache");
     }
 
+    // 3a'. the shim packs one span per distinct sequence: rows whose sequences agree on the events
+    // its grouping key samples (first / middle / last) but differ elsewhere must stay apart
+    {
+        TransformerParams p;
+        p.init(tiny, 71, 0.3f);
+        HashedEmbeddingTable table(4, 64, tiny.d_emb / 4, 72);
+        FinetuneConfig cfg;
+        cfg.max_events = 6;
+        cfg.crossing_hidden = 8;
+        RankingHeadParams rp;
+        rp.init(tiny.d_model, tiny.d_emb, cfg.d_aux, cfg.n_ctx(), cfg.crossing_hidden, cfg.sel_per_example(), 73);
+        Rng r4(31);
+        Segment a = random_segment(1, 6, 8, r4);
+        std::vector<Segment> variants{a, a, a};
+        variants[1].events[1].item_id ^= 12345;  // indices 1 and 4 are not sampled by the key (0, 3, 5)
+        variants[2].events[4].action = static_cast<Action>((static_cast<int>(a.events[4].action) + 1) % kActionCount);
+        std::vector<RankingExample> batch;
+        for (int i = 0; i < 30; i++) {
+            RankingExample ex;
+            ex.seq = variants[static_cast<size_t>(i % 3)];
+            ex.candidate = r4.next_u64() % 100000;
+            ex.age_seconds = r4.uniform(0.0, 30 * 86400.0);
+            batch.push_back(ex);
+        }
+        auto ref = seqfm::rank_forward_batch(p, table, rp, batch, cfg);
+        b200::Scorer sc(p, table, rp);
+        sc.set_fp32(true);
+        auto got = sc.rank_forward_batch(batch, cfg);
+        double scale = 0, err = 0;
+        for (auto& r : ref)
+            for (int h = 0; h < 3; h++) scale = std::max(scale, std::fabs(r.logit[h]));
+        for (size_t i = 0; i < ref.size(); i++)
+            for (int h = 0; h < 3; h++) err = std::max(err, rel(got[i].logit[h], ref[i].logit[h], scale));
+        std::printf("span sharing with grouping-key collisions: max rel err %.3e\n", err);
+        EXPECT(err <= 1e-4, "span sharing must keep differing sequences apart");
+        std::vector<Segment> segs;
+        for (auto& ex : batch) segs.push_back(ex.seq);
+        DedupPlan pr = seqfm::dedup_segments(segs, nullptr), pb = sc.dedup_segments(segs, nullptr);
+        EXPECT(pr.b_u == 3 && pb.b_u == 3 && pr.rep == pb.rep, "dedup of colliding keys");
+    }
+
     // 3b. MultiScorer: the multi-GPU drop-in for score_groups (finetune.cpp:766-786) vs the
     // reference's single-process rank_forward_batch, on 1 GPU and on 2 when the box has them
     {
