@@ -794,6 +794,9 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB, SPL>::THREADS, 1)
 #ifndef DCAT_FFN_PAIR_N
 #define DCAT_FFN_PAIR_N 1
 #endif
+#ifndef DCAT_FFN_PRODUCERS
+#define DCAT_FFN_PRODUCERS 2
+#endif
 template <int D, int CL, bool TAIL = false>
 struct FfnCfg {
     static_assert(!TAIL || (CL == 1 && D >= 128), "fused layer tail: single CTA, D = 128 or 256");
@@ -828,7 +831,11 @@ struct FfnCfg {
     // epilogue. Epilogue warp w reads TMEM lane quadrant w % 4; the 4 warps of a quadrant
     // split the columns (GELU: 32 of each 128-column chunk; final: FCOLS of the D outputs).
     static constexpr int EPI_WARPS = 16;
-    static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+    // NPROD TMA producer warps: warp 0 and NPROD - 1 more after the epilogue warps; producer p
+    // issues the ring slots it = p (mod NPROD). One issuing thread's TMA stream caps near 27 B/clk
+    // (tools/kbench/l2_stream.cu), below what the weight stream needs (profiles/r02_tail.md)
+    static constexpr int NPROD = CL == 1 ? DCAT_FFN_PRODUCERS : 1;
+    static constexpr int THREADS = 64 + 32 * EPI_WARPS + 32 * (NPROD - 1);
     // GELU warps per chunk: the epilogue warps form two groups that take alternate chunks
     // (acc1 buffer 0 / 1), 64 columns per warp, so one group's barrier / TMEM-load latency
     // overlaps the other group's math (388 -> 377 us in tools/kbench against all 16 warps on
@@ -912,7 +919,9 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(a2_full + 1);
 
 #if DCAT_FFN_TRACE
-    __shared__ unsigned s_tr_n[4];
+    // trace cursors in the spare tail of the 512-byte barrier block (no static shared memory: the
+    // kernel's dynamic budget is within 512 bytes of the limit)
+    unsigned* s_tr_n = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(bars) + 512 - 16);
     if (threadIdx.x < 4) s_tr_n[threadIdx.x] = 0;
 #endif
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -979,11 +988,19 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
     const uint32_t tmem = *tslot;
     const uint32_t T_ACC2 = tmem, T_ACC1 = tmem + 256;
 
-    if (warp == 0) {
+    const int prod_warp0 = 2 + C::EPI_WARPS;  // producers 1 .. NPROD - 1, after the epilogue warps
+    if (warp == 0 || warp >= prod_warp0) {
         if (lane == 0) {
+            // every producer walks the same slot sequence; producer `me` issues the slots
+            // it = me (mod NPROD), warp 0 also the A tiles
+            const uint32_t me = warp == 0 ? 0u : static_cast<uint32_t>(warp - prod_warp0 + 1);
             uint32_t it = 0, i = 0;
             // one ring slot: `n` weight blocks of `blk` bytes at k offsets k0 + 64 w, rows r0
             auto push = [&](const CUtensorMap* map, int k0, int r0, int n, int blk) {
+                if (C::NPROD > 1 && it % C::NPROD != me) {
+                    it++;
+                    return;
+                }
                 const int s = it % C::STAGES;
                 ptx::mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
                 FFN_EV(11, it & 255);
@@ -1007,6 +1024,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
             };
             for (int u = unit0; u < units; u += ustride, i++) {
                 const int t = u * CL + static_cast<int>(rank);  // this CTA's 128-row tile
+                if (me == 0) {
                 ptx::mbar_wait(a_empty, (i & 1) ^ 1);
                 FFN_EV(10, 0);
                 if constexpr (CL == 2) {
@@ -1016,6 +1034,7 @@ __global__ void __launch_bounds__(FfnCfg<D, CL, TAIL>::THREADS, 1)
                 } else {
                     ptx::mbar_expect_tx(a_full, C::A_TILE);
                     for (int kb = 0; kb < C::KB1; kb++) ptx::tma_load_2d(sA + kb * 16384, &tmA, a_full, kb * 64, t * 128);
+                }
                 }
                 // No L2 prefetch of the next tile's rows: issued a tile (~36 us, ~230 MB of DRAM
                 // traffic) ahead, it is evicted from the 126 MB L2 before use (ncu: +190-250 MB of
