@@ -18,6 +18,9 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <mutex>
+#include <condition_variable>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstring>
@@ -122,6 +125,89 @@ inline uint64_t span_key(int64_t off, int32_t valid) {
     return (static_cast<uint64_t>(off) << 20 | static_cast<uint64_t>(valid)) + 1;
 }
 unsigned host_threads() { return std::max(1u, std::min(16u, std::thread::hardware_concurrency())); }
+
+// Persistent host workers of a multi-device handle: run(n, f) calls f(0 .. n-1) on the workers and
+// the calling thread and returns when all are done. Jobs from several threads are serialised.
+// (Spawning std::threads per phase cost ~20-50 us each, several ms per call at 16 threads.)
+class ThreadPool {
+public:
+    explicit ThreadPool(unsigned workers) {
+        for (unsigned i = 0; i < workers; i++) th_.emplace_back([this] { loop(); });
+    }
+    ~ThreadPool() {
+        {
+            std::lock_guard<std::mutex> lk(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    unsigned size() const { return static_cast<unsigned>(th_.size()) + 1; }
+    void run(unsigned n, const std::function<void(unsigned)>& f) {
+        if (n == 0) return;
+        if (n == 1 || th_.empty()) {
+            for (unsigned i = 0; i < n; i++) f(i);
+            return;
+        }
+        std::lock_guard<std::mutex> job(job_m_);
+        {
+            // no worker of the previous job is still taking items when the counter resets
+            std::unique_lock<std::mutex> lk(m_);
+            idle_cv_.wait(lk, [&] { return active_ == 0; });
+            f_ = &f;
+            n_ = n;
+            next_.store(0);
+            done_ = 0;
+            gen_++;
+        }
+        cv_.notify_all();
+        take(&f, n);
+        std::unique_lock<std::mutex> lk(m_);
+        done_cv_.wait(lk, [&] { return done_ == n; });
+        f_ = nullptr;
+    }
+
+private:
+    void take(const std::function<void(unsigned)>* f, unsigned n) {
+        unsigned k = 0, mine = 0;
+        while ((k = next_.fetch_add(1)) < n) {
+            (*f)(k);
+            mine++;
+        }
+        if (mine) {
+            std::lock_guard<std::mutex> lk(m_);
+            done_ += mine;
+            if (done_ == n) done_cv_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void(unsigned)>* f = nullptr;
+            unsigned n = 0;
+            {
+                std::unique_lock<std::mutex> lk(m_);
+                cv_.wait(lk, [&] { return stop_ || (gen_ != seen && f_ != nullptr); });
+                if (stop_) return;
+                seen = gen_;
+                f = f_;
+                n = n_;
+                active_++;
+            }
+            take(f, n);
+            std::lock_guard<std::mutex> lk(m_);
+            if (--active_ == 0) idle_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_, job_m_;
+    std::condition_variable cv_, done_cv_, idle_cv_;
+    const std::function<void(unsigned)>* f_ = nullptr;
+    unsigned n_ = 0, done_ = 0, active_ = 0;
+    std::atomic<unsigned> next_{0};
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
 struct DevState {
     dcat_model* m = nullptr;
     int device = 0;
@@ -140,6 +226,7 @@ struct DevState {
 struct dcat_multi {
     dcat_model_config cfg{};
     std::vector<DevState> dev;
+    std::unique_ptr<ThreadPool> pool{new ThreadPool(host_threads() - 1)};
     std::vector<int32_t> last_owner;
     std::vector<float> host_scores;
     ~dcat_multi() {
@@ -206,12 +293,7 @@ void shard(const dcat_multi* mh, const dcat_batch& b, ShardPlan& plan) {
     std::vector<Local> loc(T);
     std::vector<int64_t> r0s(T + 1);
     for (unsigned t = 0; t <= T; t++) r0s[t] = B * t / T;
-    auto parallel = [&](unsigned n, const std::function<void(unsigned)>& f) {
-        std::vector<std::thread> th;
-        for (unsigned t = 1; t < n; t++) th.emplace_back(f, t);
-        if (n) f(0);
-        for (auto& x : th) x.join();
-    };
+    auto parallel = [&](unsigned n, const std::function<void(unsigned)>& f) { mh->pool->run(n, f); };
     // 1. distinct spans per row range
     parallel(T, [&](unsigned t) {
         Local& L = loc[t];
@@ -319,7 +401,8 @@ struct LocalBatch {
     std::vector<int64_t> rows;
     dcat_batch c{};
     // P host threads copy the device's distinct spans (each once) and fill its rows
-    void build(const dcat_batch& b, const ShardPlan& plan, int d, void*& arena, size_t& arena_bytes, unsigned P) {
+    void build(const dcat_batch& b, const ShardPlan& plan, int d, void*& arena, size_t& arena_bytes, unsigned P,
+               ThreadPool& pool) {
         rows.clear();
         for (int64_t r = 0; r < b.n_rows; r++)
             if (plan.owner[static_cast<size_t>(r)] == d) rows.push_back(r);
@@ -358,7 +441,6 @@ struct LocalBatch {
         uint8_t* act = base + o_act;
         uint8_t* surf = base + o_surf;
         const unsigned nt = std::max(1u, std::min<unsigned>(P, static_cast<unsigned>((n + E / 64) / 8192 + 1)));
-        std::vector<std::thread> th;
         auto part = [&](unsigned t) {
             for (size_t q = mine.size() * t / nt; q < mine.size() * (t + 1) / nt; q++) {  // the span events
                 const size_t k = static_cast<size_t>(mine[q]);
@@ -378,9 +460,7 @@ struct LocalBatch {
                 if (da) std::memcpy(aux + i * da, b.aux + r * da, sizeof(float) * static_cast<size_t>(da));
             }
         };
-        for (unsigned t = 1; t < nt; t++) th.emplace_back(part, t);
-        part(0);
-        for (auto& x : th) x.join();
+        pool.run(nt, part);
         c = dcat_batch{};
         c.n_rows = static_cast<int64_t>(n);
         c.row_offset = off;
@@ -483,8 +563,7 @@ int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const
         auto work = [&](int d) {
             DevState& s = mh->dev[static_cast<size_t>(d)];
             const auto b0 = clk::now();
-            lb[static_cast<size_t>(d)].build(*batch, plan, d, s.arena, s.arena_bytes,
-                                             std::max(1u, host_threads() / static_cast<unsigned>(nd)));
+            lb[static_cast<size_t>(d)].build(*batch, plan, d, s.arena, s.arena_bytes, mh->pool->size(), *mh->pool);
             const auto b1 = clk::now();
             t_build[static_cast<size_t>(d)] = std::chrono::duration<double, std::milli>(b1 - b0).count();
             const size_t n = lb[static_cast<size_t>(d)].rows.size();
@@ -549,18 +628,18 @@ int dcat_multi_rank_forward_batch(dcat_multi* mh, const dcat_batch* batch, const
             DCAT_CUDA_CHECK(cudaStreamSynchronize(mh->dev[static_cast<size_t>(d)].stream));
         }
         // back to the caller's row order: device d's block holds its n_d rows as [logits | module logits]
-        std::vector<std::thread> sc;
-        for (int d = 0; d < nd; d++)
-            sc.emplace_back([&, d] {
-                const auto& rows = lb[static_cast<size_t>(d)].rows;
-                const float* blk = mh->host_scores.data() + at[d];
-                const size_t n = rows.size();
-                for (size_t i = 0; i < n; i++) {
-                    std::memcpy(logits + rows[i] * 3, blk + i * 3, 3 * sizeof(float));
-                    std::memcpy(module_logits + rows[i] * 3, blk + n * 3 + i * 3, 3 * sizeof(float));
-                }
-            });
-        for (auto& x : sc) x.join();
+        // every device's block in slices across the pool
+        const unsigned per = std::max(1u, mh->pool->size() / static_cast<unsigned>(nd));
+        mh->pool->run(static_cast<unsigned>(nd) * per, [&](unsigned k) {
+            const int d = static_cast<int>(k / per), part = static_cast<int>(k % per);
+            const auto& rows = lb[static_cast<size_t>(d)].rows;
+            const float* blk = mh->host_scores.data() + at[d];
+            const size_t n = rows.size();
+            for (size_t i = n * part / per; i < n * (part + 1) / per; i++) {
+                std::memcpy(logits + rows[i] * 3, blk + i * 3, 3 * sizeof(float));
+                std::memcpy(module_logits + rows[i] * 3, blk + n * 3 + i * 3, 3 * sizeof(float));
+            }
+        });
         if (timing) {
             auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
             std::fprintf(stderr, "dcat_multi: shard %.3f ms | build", ms(t_start, t_shard));
