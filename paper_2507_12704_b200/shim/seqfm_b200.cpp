@@ -2,6 +2,9 @@
 #include "seqfm_b200.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -12,6 +15,7 @@
 #include <tuple>
 
 #include "../../include/dcat_b200.h"
+#include "../csrc/host_pool.hpp"
 
 namespace seqfm {
 namespace b200 {
@@ -37,6 +41,12 @@ dcat_model_config to_c(const ModelConfig& c) {
 }
 
 size_t align16(size_t n) { return (n + 15) & ~size_t(15); }
+
+// process-wide host workers for batch packing (created on first use, joined at exit)
+dcat::ThreadPool& host_pool() {
+    static dcat::ThreadPool pool(std::max(1u, std::min(16u, std::thread::hardware_concurrency())) - 1);
+    return pool;
+}
 
 // a row's valid events: equal sequences (the reference's segment_key content, dcat.cpp:45-56)
 bool same_events(const Segment& a, const Segment& b) {
@@ -100,15 +110,13 @@ struct BatchSoA {
         }
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         const size_t T = std::min<size_t>(std::min<size_t>(hw, 16), std::max<size_t>(1, B / 4096));
-        auto parallel = [&](size_t n, auto&& f) {  // f(lo, hi) over [0, n) in T slices
+        auto parallel = [&](size_t n, auto&& f) {  // f(lo, hi) over [0, n) in T slices, on the shim's pool
             if (T <= 1 || n < 2 * T) {
                 f(size_t(0), n);
                 return;
             }
-            std::vector<std::thread> th;
-            for (size_t t = 1; t < T; t++) th.emplace_back([&, t] { f(n * t / T, n * (t + 1) / T); });
-            f(size_t(0), n / T);
-            for (auto& x : th) x.join();
+            host_pool().run(static_cast<unsigned>(T),
+                            [&](unsigned t) { f(n * t / T, n * (t + 1) / T); });
         };
         // 1. grouping keys (parallel), 2. provisional groups by key (first row = representative)
         std::vector<uint64_t> key(B);
@@ -342,13 +350,22 @@ struct CWeights {
 };
 
 void to_outputs(const std::vector<float>& logits, const std::vector<float>& mlog, std::vector<RankingOutputs>& out) {
-    for (size_t i = 0; i < out.size(); i++)
-        for (int j = 0; j < kRankHeadCount; j++) {
-            double l = logits[i * 3 + j];  // outputs_from, finetune.cpp:350-359
-            out[i].logit[static_cast<size_t>(j)] = l;
-            out[i].prob[static_cast<size_t>(j)] = 1.0 / (1.0 + std::exp(-l));
-            out[i].module_logit[static_cast<size_t>(j)] = mlog[i * 3 + j];
-        }
+    const size_t B = out.size();
+    auto rows = [&](size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi; i++)
+            for (int j = 0; j < kRankHeadCount; j++) {
+                double l = logits[i * 3 + j];  // outputs_from, finetune.cpp:350-359
+                out[i].logit[static_cast<size_t>(j)] = l;
+                out[i].prob[static_cast<size_t>(j)] = 1.0 / (1.0 + std::exp(-l));
+                out[i].module_logit[static_cast<size_t>(j)] = mlog[i * 3 + j];
+            }
+    };
+    const unsigned T = static_cast<unsigned>(std::min<size_t>(host_pool().size(), std::max<size_t>(1, B / 8192)));
+    if (T <= 1) {
+        rows(0, B);
+        return;
+    }
+    host_pool().run(T, [&](unsigned t) { rows(B * t / T, B * (t + 1) / T); });
 }
 }  // namespace
 
@@ -367,14 +384,26 @@ Scorer::~Scorer() {
 
 std::vector<RankingOutputs> Scorer::rank_forward_batch(const std::vector<RankingExample>& batch,
                                                        const FinetuneConfig& cfg) const {
+    // SEQFM_B200_TIMING=1: host wall time of pack / device call / outputs on stderr (investigation aid)
+    static const bool timing = std::getenv("SEQFM_B200_TIMING") != nullptr;
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     std::vector<RankingOutputs> out(batch.size());
     if (batch.empty()) return out;
     std::lock_guard<std::mutex> lk(mu_);
     BatchSoA b = pack_examples(batch, uses_aux(cfg), stage_, stage_bytes_);
+    const auto t1 = clk::now();
     dcat_finetune_config fc = to_c(cfg);
     std::vector<float> logits(batch.size() * 3), mlog(batch.size() * 3);
     check(dcat_rank_forward_batch(m_, &b.c, &fc, logits.data(), mlog.data(), nullptr, flags_, nullptr));
+    const auto t2 = clk::now();
     to_outputs(logits, mlog, out);
+    if (timing) {
+        auto ms = [](clk::time_point a, clk::time_point z) { return std::chrono::duration<double, std::milli>(z - a).count(); };
+        std::fprintf(stderr, "seqfm::b200 rank_forward_batch: alloc+pack %.3f ms (%lld distinct spans of %zu rows), "
+                     "device call %.3f ms, outputs %.3f ms\n", ms(t0, t1), static_cast<long long>(b.c.n_events),
+                     batch.size(), ms(t1, t2), ms(t2, clk::now()));
+    }
     return out;
 }
 
