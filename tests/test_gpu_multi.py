@@ -62,3 +62,23 @@ def test_multi_devices_must_be_distinct(torch_mod):
     orc, spec, w, b = _setup()
     with pytest.raises(RuntimeError, match="distinct"):
         api.MultiDcatModel(w, [0, 0])
+
+
+def test_multi_device_idle_devices(torch_mod):
+    """Fewer distinct users than devices: some devices get no rows (no scoring call, no NCCL
+    transfer for them); the scores still equal the single-device call."""
+    if torch_mod.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from paper_2507_12704_b200 import api
+    orc = pyoracle.oracle()
+    spec = ModelSpec(d_model=64, n_layers=1, n_heads=4, mlp_ratio=2, max_len=34, d_emb=64)
+    w = orc.init_weights(spec, 7, table=(8, 256, 8, 7, 0.05), head_seed=3)
+    b = make_batch(1, 5, 32, seed=9, ragged=True)
+    ft = FinetuneSpec(max_events=32)
+    l1, m1, _ = api.DcatModel(w, device=0).rank_forward_batch(b, ft, precision="fp32")
+    mm = api.MultiDcatModel(w, [0, 1])
+    ln, mn = mm.rank_forward_batch(b, ft, precision="fp32")
+    assert len(set(mm.shard(b).tolist())) == 1
+    assert float(np.abs(ln - l1).max()) <= 1e-5 * max(1e-3, float(np.abs(l1).max()))
+    assert float(np.abs(mn - m1).max()) <= 1e-5 * max(1e-3, float(np.abs(m1).max()))
+    mm.close()
