@@ -660,15 +660,22 @@ int sm_count_f() {
     return n;
 }
 
+// POLY: every POLY-th pair of exponentials on the FMA pipe (ex2p) beside MUFU.EX2. Measured
+// (profiles/r02_attention.md): the crossing kernel gains at POLY = 4 (PinFM-base 0.631 -> 0.607 ms,
+// high-fanout 8.96 -> 8.61 ms per step), the causal kernel loses (0.597 -> 0.681 ms), so only the
+// crossing kernel uses it.
 #ifndef DCAT_FA_POLY
 #define DCAT_FA_POLY 0
+#endif
+#ifndef DCAT_FA_POLY_CROSS
+#define DCAT_FA_POLY_CROSS 4
 #endif
 
 template <int DH, bool CAUSAL>
 void launch_fa(const AttnArgs& a, int64_t q_rows, int64_t kv_rows, cudaStream_t s) {
     using Sm = FaSmem<DH, CAUSAL>;
     static_assert(Sm::TOTAL <= 227 * 1024, "shared memory budget");
-    auto kern = k_attn_fa<DH, CAUSAL, DCAT_FA_POLY>;
+    auto kern = k_attn_fa<DH, CAUSAL, CAUSAL ? DCAT_FA_POLY : DCAT_FA_POLY_CROSS>;
     set_smem_attr(reinterpret_cast<const void*>(kern), Sm::TOTAL);
     const int d = a.n_heads * DH;
     const CUtensorMapSwizzle swq =
