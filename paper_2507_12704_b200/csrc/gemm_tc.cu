@@ -76,12 +76,16 @@ struct EpiMaps {
 // SPL = 2: a full-row epilogue over d = 2 BN columns split across a CTA pair (thread-block cluster
 // of 2): each CTA owns BN columns with double-buffered accumulators, and the per-row statistics
 // (LayerNorm mean / variance, l2 norm) are summed over the pair through distributed shared memory.
-template <int BN, int MODE, bool RB = false, int SPL = 1>
+// LK (with SPL = 2, long K): one epilogue warp per lane quadrant, which frees the shared memory for
+// a third 48 KB operand stage. The operand stream of a long-K GEMM (d = 512 FFN2: 32 k-blocks per
+// tile) needs the depth; a short-K one (o-projection, K = 512) needs the epilogue warps instead.
+template <int BN, int MODE, bool RB = false, int SPL = 1, bool LK = false>
 struct Cfg {
     static_assert(!RB || (MODE == EPI_BIAS && BN == 256), "resident B: EPI_BIAS, BN = 256");
     static_assert(SPL == 1 || ((MODE == EPI_RESID_LN || MODE == EPI_L2NORM) && BN == 256), "split: full-row, BN 256");
     static constexpr bool FULL = MODE == EPI_RESID_LN || MODE == EPI_L2NORM;
-    static constexpr int CG = BN == 64 ? 2 : (FULL ? (BN == 512 ? 1 : 2) : 4);  // epilogue warps per lane quadrant
+    static constexpr bool SPL1 = SPL == 2 && LK;
+    static constexpr int CG = BN == 64 ? 2 : (FULL ? ((BN == 512 || SPL1) ? 1 : 2) : 4);  // epilogue warps per lane quadrant
     static constexpr int EPI_WARPS = 4 * CG;
     static constexpr int EPI_THREADS = 32 * EPI_WARPS;
     static constexpr int THREADS = 128 + EPI_THREADS;
@@ -92,7 +96,7 @@ struct Cfg {
     static constexpr int ACC_BUFS = BN <= 256 ? 2 : 1;
     static constexpr int TMEM_COLS = BN * ACC_BUFS < 32 ? 32 : BN * ACC_BUFS;
     static constexpr int STAGES =
-        RB ? 4 : BN == 64 ? (FULL ? 4 : 6) : BN == 128 ? (FULL ? 3 : 4) : BN == 256 ? (FULL ? 2 : 3) : 2;
+        RB ? 4 : BN == 64 ? (FULL ? 4 : 6) : BN == 128 ? (FULL ? 3 : 4) : BN == 256 ? (FULL ? (SPL1 ? 3 : 2) : 3) : 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int KB_RES = 4;  // resident B: k-blocks (K <= 256)
     static constexpr int RING = RB ? STAGES * A_BYTES + KB_RES * B_BYTES : STAGES * (A_BYTES + B_BYTES);
@@ -359,11 +363,11 @@ struct EpiWarp {
     uint32_t hb;       // next bf16 staging buffer (alternates on every bf16 store)
 };
 
-template <int BN, int MODE, bool RB, int SPL = 1>
+template <int BN, int MODE, bool RB, int SPL = 1, bool LK = false>
 __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, uint32_t tacc, EpiWarp& W,
                                               uint32_t red, uint32_t sp, int q, int cg, int lane, int m0, int n0,
                                               int M, int N, int nvalid, int t, int tiles, int step, PairX& X) {
-    using C = Cfg<BN, MODE, RB, SPL>;
+    using C = Cfg<BN, MODE, RB, SPL, LK>;
     const ParamLayout PL = param_layout(N);
     const int row_base = m0 + q * 32;
     const int row = row_base + lane;
@@ -598,11 +602,11 @@ __device__ __forceinline__ void epilogue_tile(const Epi& e, const EpiMaps& mp, u
     }
 }
 
-template <int BN, int MODE, bool RB, int SPL = 1>
-__global__ void __launch_bounds__(Cfg<BN, MODE, RB, SPL>::THREADS, 1)
+template <int BN, int MODE, bool RB, int SPL = 1, bool LK = false>
+__global__ void __launch_bounds__(Cfg<BN, MODE, RB, SPL, LK>::THREADS, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
               const __grid_constant__ Epi e, const __grid_constant__ EpiMaps mp) {
-    using C = Cfg<BN, MODE, RB, SPL>;
+    using C = Cfg<BN, MODE, RB, SPL, LK>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -758,7 +762,7 @@ __global__ void __launch_bounds__(Cfg<BN, MODE, RB, SPL>::THREADS, 1)
             ptx::mbar_wait(&tfull[buf], (i / C::ACC_BUFS) & 1);
             ptx::tc_fence_after();
             const uint32_t tacc = tmem + buf * BN + (static_cast<uint32_t>(q * 32) << 16);
-            epilogue_tile<BN, MODE, RB, SPL>(e, mp, tacc, W, s_red, s_par, q, cg, lane, m0, n0, M, N,
+            epilogue_tile<BN, MODE, RB, SPL, LK>(e, mp, tacc, W, s_red, s_par, q, cg, lane, m0, n0, M, N,
                                              min(BN, N - n0), t, tiles, step, X);
             ptx::tc_fence_before();
             __syncwarp();
@@ -1576,11 +1580,11 @@ template <int BN, int MODE, bool RB = false>
 void launch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e, cudaStream_t s);
 
 // full-row epilogue over d = 512 on a CTA pair (SPL = 2): BN = 256 columns per CTA
-template <int MODE>
+template <int MODE, bool LK>
 void launch_split(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const Epi& e, cudaStream_t s) {
-    using C = Cfg<256, MODE, false, 2>;
+    using C = Cfg<256, MODE, false, 2, LK>;
     static_assert(C::SMEM <= 227 * 1024, "shared memory budget");
-    auto kern = k_gemm_tc<256, MODE, false, 2>;
+    auto kern = k_gemm_tc<256, MODE, false, 2, LK>;
     set_smem_attr(reinterpret_cast<const void*>(kern), C::SMEM);
     {
         const int npad = (N + 31) & ~31;
@@ -1652,7 +1656,9 @@ void launch_mode(int BN, const CUtensorMap& ta, const CUtensorMap& tb, int M, in
                 // warps per CTA) unless DCAT_NO_PAIR_EPILOGUE selects the one-CTA BN = 512 tile
                 static const bool one_cta = getenv("DCAT_NO_PAIR_EPILOGUE") != nullptr;
                 if (one_cta) launch<512, MODE>(ta, tb, M, N, K, e, s);
-                else launch_split<MODE>(ta, tb, M, N, K, e, s);
+                // long K (FFN2: d_ff = 2048): 3 operand stages, 4 epilogue warps (LK); short K: 2, 8
+                else if (K >= 1024) launch_split<MODE, true>(ta, tb, M, N, K, e, s);
+                else launch_split<MODE, false>(ta, tb, M, N, K, e, s);
                 break;
             }
             [[fallthrough]];
