@@ -79,13 +79,21 @@ struct EpiMaps {
 // LK (with SPL = 2, long K): one epilogue warp per lane quadrant, which frees the shared memory for
 // a third 48 KB operand stage. The operand stream of a long-K GEMM (d = 512 FFN2: 32 k-blocks per
 // tile) needs the depth; a short-K one (o-projection, K = 512) needs the epilogue warps instead.
+#ifndef DCAT_BIAS_STAGES4
+#define DCAT_BIAS_STAGES4 1
+#endif
 template <int BN, int MODE, bool RB = false, int SPL = 1, bool LK = false>
 struct Cfg {
     static_assert(!RB || (MODE == EPI_BIAS && BN == 256), "resident B: EPI_BIAS, BN = 256");
     static_assert(SPL == 1 || ((MODE == EPI_RESID_LN || MODE == EPI_L2NORM) && BN == 256), "split: full-row, BN 256");
     static constexpr bool FULL = MODE == EPI_RESID_LN || MODE == EPI_L2NORM;
     static constexpr bool SPL1 = SPL == 2 && LK;
-    static constexpr int CG = BN == 64 ? 2 : (FULL ? ((BN == 512 || SPL1) ? 1 : 2) : 4);  // epilogue warps per lane quadrant
+    // BIAS4: EPI_BIAS at BN = 256 without resident B (K > 256: the d = 512 QKV and FFN1 GEMMs) trades
+    // two epilogue warps per quadrant and the second staging buffer for a fourth 48 KB operand
+    // stage: long-seq ctx ffn1 4.17 -> 3.77 ms, qkv 3.00 -> 2.55 ms (the operand stream's depth is
+    // what these GEMMs lack, as for the long-K full-row epilogues below)
+    static constexpr bool BIAS4 = DCAT_BIAS_STAGES4 && MODE == EPI_BIAS && BN == 256 && !RB;
+    static constexpr int CG = BN == 64 ? 2 : (FULL ? ((BN == 512 || SPL1) ? 1 : 2) : (BIAS4 ? 2 : 4));  // epilogue warps per lane quadrant
     static constexpr int EPI_WARPS = 4 * CG;
     static constexpr int EPI_THREADS = 32 * EPI_WARPS;
     static constexpr int THREADS = 128 + EPI_THREADS;
@@ -96,11 +104,11 @@ struct Cfg {
     static constexpr int ACC_BUFS = BN <= 256 ? 2 : 1;
     static constexpr int TMEM_COLS = BN * ACC_BUFS < 32 ? 32 : BN * ACC_BUFS;
     static constexpr int STAGES =
-        RB ? 4 : BN == 64 ? (FULL ? 4 : 6) : BN == 128 ? (FULL ? 3 : 4) : BN == 256 ? (FULL ? (SPL1 ? 3 : 2) : 3) : 2;
+        RB ? 4 : BN == 64 ? (FULL ? 4 : 6) : BN == 128 ? (FULL ? 3 : 4) : BN == 256 ? (FULL ? (SPL1 ? 3 : 2) : (BIAS4 ? 4 : 3)) : 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int KB_RES = 4;  // resident B: k-blocks (K <= 256)
     static constexpr int RING = RB ? STAGES * A_BYTES + KB_RES * B_BYTES : STAGES * (A_BYTES + B_BYTES);
-    static constexpr int HBUF = RB ? 1 : 2;  // bf16 staging buffers per epilogue warp
+    static constexpr int HBUF = (RB || BIAS4) ? 1 : 2;  // bf16 staging buffers per epilogue warp
     static constexpr int EW = FULL ? 2 * F_BYTES + 2 * H_BYTES : (MODE == EPI_BIAS ? HBUF * H_BYTES : 0);  // per warp
     static constexpr int EPI_SMEM = EW * EPI_WARPS;
     static constexpr int RED = MODE == EPI_BIAS ? 0 : 4 * 3 * CG * 32 * 4;  // [quadrant][value][cg][lane]
