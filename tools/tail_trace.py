@@ -64,7 +64,7 @@ def main():
         lat = np.array(rdy[:n2]) - np.array(iss[:n2])
         print(f"slot issue->seen-full: median={np.median(lat):.0f} p10={np.percentile(lat, 10):.0f} "
               f"p90={np.percentile(lat, 90):.0f} clk over {n2} slots")
-        stages = 4
+        stages = int(os.environ.get("TAIL_RING_SLOTS", "6"))  # DCAT_FFN_STAGES256 of the traced build
         free = np.array(iss[stages:n2]) - np.array(rdy[:n2 - stages])
         print(f"slot seen-full -> re-issued (MMA consume + commit + producer): median={np.median(free):.0f} clk")
     if len(rdy) > 2:
