@@ -18,6 +18,12 @@
  * The reference throws std::runtime_error (common.hpp:9-16) where this ABI
  * returns DCAT_EINVAL; the C++ shim maps one to the other.
  *
+ * Devices and threads: an entry point makes its handle's GPU current for the
+ * call and restores the calling thread's current device before returning.
+ * Calls on one handle must be serialised by the caller (one handle = one set
+ * of streams, CUDA graphs and work buffers); different handles run
+ * concurrently. Destroy entry points never fail on a shutting-down runtime.
+ *
  * The same structs are consumed by the CPU oracle (oracle/dcat_oracle.h) and
  * by the reference bridge (oracle/ref_bridge.cpp), so one set of host buffers
  * feeds all three implementations.
